@@ -1,0 +1,405 @@
+"""Flood-filtration benchmark (BASELINE.json metric: simplices/s).
+
+One step = one GPU pass of the hot path over the workload with the cloud and
+the landmark complex resident in HBM: spatial-grid build, the flooding
+kernel for every simplex of dim <= max_dim, facet completion.  The default
+workload is BASELINE configs[1]: 1M points, noisy sphere+torus mix, 2000
+FPS landmarks, simplices of dim <= 2 of their 3-D Delaunay complex, grid
+resolution m = 20 (the reference default).  Farthest point sampling and the
+host Delaunay are timed as separate stages (fps_ms, delaunay_s).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+N > 1 (torchrun): every rank builds the grid, values an interleaved shard of
+the simplices, and the shards are all-gathered over NCCL (weak scaling is
+not meaningful here: the complex is fixed, so "scaling" is "strong").
+--impl reference times the CPU oracle (oracle/, a C restatement of the
+reference algorithm, all host threads) on a bounded sample of the same
+complex; rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # name: (generator, n_points, landmarks, m, max_dim)
+    "sphere_torus_1m": ("sphere_torus", 1_000_000, 2000, 20, 2),
+    "dense30_1m": ("sphere_torus", 1_000_000, 2000, 30, 2),
+    "box_10m": ("box", 10_000_000, 5000, 20, 3),
+    "torus_10k": ("torus", 10_000, 500, 20, 2),
+}
+
+
+def _cloud(kind: str, n: int):
+    from paper_2509_22432_b200 import datagen
+
+    if kind == "sphere_torus":
+        return datagen.gen_sphere_torus_mix(n, seed=0).points
+    if kind == "box":
+        return datagen.gen_uniform_box(n, seed=0).points
+    return datagen.gen_torus(n, seed=0).points
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(
+                    ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                     "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                if out.returncode == 0 and out.stdout.strip():
+                    self.rows.append([c.strip() for c in out.stdout.strip().split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if len(r) > 2 + i and r[2 + i].lower().startswith("active")})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(self.rows)}
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return json.load(fh)
+    except OSError:
+        return {}
+
+
+def _dist():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def prepare(cfg_name: str, device: int):
+    """Untimed setup: cloud, GPU FPS (timed as its own stage), host Delaunay."""
+    import torch
+
+    from paper_2509_22432_b200 import farthest_point_sampling
+    from paper_2509_22432_b200.delaunay import delaunay
+
+    kind, n, nl, m, max_dim = CONFIGS[cfg_name]
+    X = _cloud(kind, n)
+    Xd = torch.from_numpy(X).to(f"cuda:{device}")
+    farthest_point_sampling(Xd, 16, 0)  # warm the FPS kernel
+    torch.cuda.synchronize()
+    fps_ms = []
+    for _ in range(2):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        idx = farthest_point_sampling(Xd, nl, 0)
+        e1.record()
+        torch.cuda.synchronize()
+        fps_ms.append(e0.elapsed_time(e1))
+    idx = idx.cpu().numpy()
+    t0 = time.perf_counter()
+    tri = delaunay(X[idx])
+    delaunay_s = time.perf_counter() - t0
+    return dict(X=X, Xd=Xd, idx=idx, tri=tri, m=m, max_dim=min(max_dim, tri.dim), n=n, nl=nl,
+                fps_ms=min(fps_ms), delaunay_s=delaunay_s, kind=kind)
+
+
+class DeviceComplex:
+    """Device buffers of one (shard of a) complex for the C-ABI calls."""
+
+    def __init__(self, w, device, world=1, rank=0):
+        import torch
+
+        tri = w["tri"]
+        self.top = w["max_dim"]
+        self.dev = torch.device(f"cuda:{device}")
+        self.lm = torch.from_numpy(np.ascontiguousarray(tri.points)).to(self.dev)
+        self.counts_full = [int(tri.simplices_by_dim[k].shape[0]) for k in range(self.top + 1)]
+        self.simp4 = {}
+        self.facets = {}
+        for k in range(1, self.top + 1):
+            s = tri.simplices_by_dim[k]
+            pad = np.full((s.shape[0], 4), -1, dtype=np.int32)
+            pad[:, : k + 1] = s
+            self.simp4[k] = torch.from_numpy(pad[rank::world].copy()).to(self.dev)
+            self.facets[k] = torch.from_numpy(np.ascontiguousarray(tri.facet_links[k], dtype=np.int32)).to(self.dev)
+        self.full_simp = {k: torch.from_numpy(np.ascontiguousarray(tri.simplices_by_dim[k], dtype=np.int32)).to(self.dev)
+                          for k in range(1, self.top + 1)}
+        self.counts = torch.tensor(self.counts_full, dtype=torch.int64)
+        self.out = [torch.empty(max(c, 1), dtype=torch.float64, device=self.dev) for c in self.counts_full]
+        self.world, self.rank = world, rank
+
+
+def step_single(lib, native, w, dc, stream):
+    """N = 1: the whole complex in one fph_flood_filtration call."""
+    simp = [None] + [dc.full_simp[k] for k in range(1, dc.top + 1)]
+    fac = [None] + [dc.facets[k] for k in range(1, dc.top + 1)]
+    native.check(lib.fph_flood_filtration(
+        w["Xd"].data_ptr(), w["n"], w["X"].shape[1], dc.lm.data_ptr(), dc.lm.shape[0], dc.top,
+        dc.counts.data_ptr(), native.ptr_array(simp, None), native.ptr_array(fac, None),
+        w["m"], 1, native.ptr_array(dc.out, None), native.FPH_MEM_DEVICE, stream))
+
+
+def step_sharded(lib, native, w, dc, stream):
+    """N > 1: interior values of this rank's interleaved shard, NCCL
+    all-gather, then facet completion (identical on every rank)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2509_22432_b200.parallel import gather_interleaved
+
+    interiors = {}
+    for k in range(1, dc.top + 1):
+        mine = torch.empty(max(dc.simp4[k].shape[0], 1), dtype=torch.float64, device=dc.dev)
+        if dc.simp4[k].shape[0]:
+            native.check(lib.fph_flood_interior(
+                w["Xd"].data_ptr(), w["n"], w["X"].shape[1], dc.lm.data_ptr(), dc.lm.shape[0],
+                dc.simp4[k].data_ptr(), dc.simp4[k].shape[0], k, w["m"], 1, mine.data_ptr(),
+                native.FPH_MEM_DEVICE, stream))
+        interiors[k] = gather_interleaved(mine[: dc.simp4[k].shape[0]], dc.counts_full[k],
+                                          dc.world, dist)
+    dc.out[0].zero_()
+    for k in range(1, dc.top + 1):
+        native.check(lib.fph_flood_complete(
+            interiors[k].data_ptr(), dc.facets[k].data_ptr(), dc.counts_full[k], k,
+            dc.out[k - 1].data_ptr(), dc.out[k].data_ptr(), stream))
+
+
+def run_ours(args):
+    import torch
+
+    from paper_2509_22432_b200 import _native
+
+    world, rank, local = _dist()
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl")
+    lib = _native.require_gpu()
+    w = prepare(args.config, local)
+    dc = DeviceComplex(w, local, world, rank)
+    stream = torch.cuda.current_stream().cuda_stream
+    step = step_single if world == 1 else step_sharded
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dc.dev)  # > 126 MB L2
+    for _ in range(args.warmup):
+        step(lib, _native, w, dc, stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    lib.fph_launch_count(1)
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    with ClockSampler(local) as clocks:
+        torch.cuda.synchronize()
+        for i in range(args.steps):
+            flush.zero_()
+            starts[i].record()
+            step(lib, _native, w, dc, stream)
+            ends[i].record()
+        torch.cuda.synchronize()
+    launches = int(lib.fph_launch_count(0))
+    ms = sum(s.elapsed_time(e) for s, e in zip(starts, ends)) / args.steps
+    if world > 1:
+        import torch.distributed as dist
+
+        t = torch.tensor([ms], device=dc.dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    n_simplices = sum(dc.counts_full)
+    value = n_simplices / (ms / 1e3)
+
+    result = None
+    if rank == 0:
+        e2e = e2e_host(lib, _native, w, args) if world == 1 else None
+        result = {
+            "metric": "flood-filtration simplices/s",
+            "value": value,
+            "unit": "simplices/s",
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": ms,
+            "higher_is_better": True,
+            "scaling": "strong",
+            "vs_baseline": None,
+            "dtype": "f64 (fp32 filter + exact f64 refine)",
+            "data": "synthetic (seeded generator), random-free reference algorithm",
+            "config": {"workload": args.config, "points": w["n"], "landmarks": w["nl"],
+                       "grid_resolution": w["m"], "max_dim": w["max_dim"],
+                       "simplices": n_simplices, "counts": dc.counts_full,
+                       "l2": "flushed (256 MB write) between timed steps",
+                       "parallelism": f"simplex shards x{world}, cloud replicated"},
+            "fps_ms": w["fps_ms"],
+            "delaunay_s": w["delaunay_s"],
+            "gpu_launches": launches,
+            "clocks": clocks.summary(),
+        }
+        if e2e:
+            result["e2e"] = e2e
+        if world == 1 and not args.no_cpu_baseline:
+            result["cpu_baseline"] = cpu_baseline(w, args.cpu_seconds)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+        dist.destroy_process_group()
+    return result
+
+
+def e2e_host(lib, native, w, args):
+    """Same metric through the C ABI with HOST buffers: H2D of the cloud and
+    complex, the GPU pass, D2H of the values, all inside the timed region."""
+    import torch
+
+    tri = w["tri"]
+    top = w["max_dim"]
+    X = torch.from_numpy(w["X"]).pin_memory().numpy()
+    lm = np.ascontiguousarray(tri.points)
+    counts = np.array([tri.simplices_by_dim[k].shape[0] for k in range(top + 1)], dtype=np.int64)
+    simp = [None] + [np.ascontiguousarray(tri.simplices_by_dim[k], dtype=np.int32) for k in range(1, top + 1)]
+    fac = [None] + [np.ascontiguousarray(tri.facet_links[k], dtype=np.int32) for k in range(1, top + 1)]
+    outs = [np.empty(max(int(c), 1)) for c in counts]
+    h2d = X.nbytes + lm.nbytes + sum(a.nbytes for a in simp[1:]) + sum(a.nbytes for a in fac[1:])
+    d2h = int(sum(counts) * 8)
+
+    def call():
+        native.check(lib.fph_flood_filtration(
+            native.ptr(X), X.shape[0], X.shape[1], native.ptr(lm), lm.shape[0], top,
+            native.ptr(counts), native.ptr_array(simp, None), native.ptr_array(fac, None),
+            w["m"], 1, native.ptr_array(outs, None), native.FPH_MEM_HOST, None))
+
+    for _ in range(2):
+        call()
+    times = []
+    for _ in range(max(3, args.steps)):
+        t0 = time.perf_counter()
+        call()
+        times.append(time.perf_counter() - t0)
+    sec = float(np.median(times))
+    return {"value": float(sum(counts)) / sec, "unit": "simplices/s", "h2d_bytes_per_step": int(h2d),
+            "d2h_bytes_per_step": d2h, "ms_per_step": sec * 1e3}
+
+
+def cpu_sample(w, seconds: float, threads: int):
+    """Time the oracle (reference algorithm, C, all threads) on a random
+    sample of top-dimensional simplices (with their faces) of the complex."""
+    import oracle
+
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from tests._complex import sub_complex
+
+    tri, top, m = w["tri"], w["max_dim"], w["m"]
+    rng = np.random.default_rng(1)
+    n_top = tri.simplices_by_dim[top].shape[0]
+    sample = 4
+    elapsed, done = 0.0, 0
+    while True:
+        rows = rng.choice(n_top, min(sample, n_top), replace=False)
+        sub = sub_complex(tri.simplices_by_dim, rows, top)
+        t0 = time.perf_counter()
+        oracle.flood_values(w["X"], tri.points, sub, m, threads=threads, top_dim=top)
+        dt = time.perf_counter() - t0
+        nsimp = sum(v.shape[0] for v in sub.values())
+        if dt > 0.25 * seconds or sample >= n_top:
+            return nsimp, dt, len(rows)
+        sample = int(min(n_top, sample * max(2.0, 0.5 * seconds / max(dt, 1e-3))))
+
+
+def cpu_baseline(w, seconds: float):
+    threads = os.cpu_count() or 1
+    nsimp, dt, ntop = cpu_sample(w, seconds, threads)
+    return {"value": nsimp / dt, "unit": "simplices/s", "cores": threads, "kind": "port",
+            "sample": f"{ntop} random top simplices (dim {w['max_dim']}) + their faces = "
+                      f"{nsimp} simplices of the same complex, {dt:.1f} s"}
+
+
+def run_reference(args):
+    world, rank, local = _dist()
+    if rank != 0:
+        return None
+    import oracle
+    from paper_2509_22432_b200.delaunay import delaunay
+
+    kind, n, nl, m, max_dim = CONFIGS[args.config]
+    X = _cloud(kind, n)
+    idx = oracle.fps(X, nl, 0)  # reference algorithm (C port) for the landmarks
+    tri = delaunay(X[idx])
+    w = dict(X=X, tri=tri, m=m, max_dim=min(max_dim, tri.dim))
+    threads = os.cpu_count() or 1
+    for _ in range(args.warmup):
+        cpu_sample(w, args.cpu_seconds / 4, threads)
+    vals = []
+    desc = ""
+    for _ in range(args.steps):
+        nsimp, dt, ntop = cpu_sample(w, args.cpu_seconds, threads)
+        vals.append(nsimp / dt)
+        desc = f"{ntop} random top simplices + faces ({nsimp} simplices) per step"
+    value = float(np.median(vals))
+    return {"impl": "reference", "metric": "flood-filtration simplices/s", "value": value,
+            "unit": "simplices/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": None, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic (seeded generator)",
+            "config": {"workload": args.config, "points": n, "landmarks": nl, "grid_resolution": m,
+                       "max_dim": w["max_dim"]},
+            "cpu_baseline": {"value": value, "unit": "simplices/s", "cores": threads, "kind": "port",
+                             "sample": desc},
+            "e2e": {"value": value, "unit": "simplices/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", choices=sorted(CONFIGS), default="sphere_torus_1m")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    res = run_reference(args) if args.impl == "reference" else run_ours(args)
+    if res is not None:
+        print(json.dumps(res))
+
+
+if __name__ == "__main__":
+    main()

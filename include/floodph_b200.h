@@ -1,0 +1,126 @@
+/*
+ * floodph_b200.h -- C ABI of the B200 flood-filtration library
+ * (paper_2509_22432_b200/csrc -> libfloodph_b200.so).
+ *
+ * Plain pointers and sizes only.  Every entry point takes a `memory` flag:
+ *   FPH_MEM_HOST    all array arguments are host pointers; the call copies
+ *                   them to the GPU, runs, copies results back and returns
+ *                   when they are ready (the drop-in for the CPU reference);
+ *   FPH_MEM_DEVICE  all array arguments are device pointers on the current
+ *                   CUDA device; work is ordered on `stream` (a cudaStream_t,
+ *                   NULL = legacy default stream).
+ * Return value: FPH_OK (0) or an FPH_E* code; fph_last_error() describes the
+ * most recent failure of the calling thread.  Argument errors (FPH_EARG)
+ * correspond to the reference's ValueError, FPH_EINTEGRITY to IntegrityError.
+ *
+ * Coordinates are float64 row-major (n x dim, dim in {2, 3}); results are
+ * bit-identical to the reference's float64 values.
+ */
+#ifndef FLOODPH_B200_H
+#define FLOODPH_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FPH_OK 0
+#define FPH_EARG 1
+#define FPH_ECUDA 2
+#define FPH_ENOMEM 3
+#define FPH_EINTEGRITY 4
+
+#define FPH_MEM_HOST 0
+#define FPH_MEM_DEVICE 1
+
+#define FPH_ABI_VERSION 1
+
+/* ABI version (FPH_ABI_VERSION). */
+int fph_abi_version(void);
+
+/* Message of the calling thread's last failure ("" if none). */
+const char* fph_last_error(void);
+
+/* Number of visible CUDA devices (0 when no GPU/driver). */
+int fph_device_count(void);
+
+/*
+ * Farthest point sampling.
+ * Replaces floodph/geometry.py:88  farthest_point_sampling(cloud, k, start):
+ * out_indices[0] = start, then greedily the point maximising the distance to
+ * the chosen prefix, ties to the smallest index.  Errors: k < 1, k > n or
+ * start outside [0, n) -> FPH_EARG.
+ */
+int fph_farthest_point_sampling(const double* points, int64_t n, int32_t dim, int64_t k,
+                                int64_t start, int64_t* out_indices, int32_t memory,
+                                void* stream);
+
+/*
+ * Batched farthest point sampling over `batch` clouds of equal size
+ * (points: batch x n x dim).  out_indices: batch x k.  Same semantics per
+ * cloud as fph_farthest_point_sampling.
+ */
+int fph_farthest_point_sampling_batched(const double* points, int64_t batch, int64_t n,
+                                        int32_t dim, int64_t k, int64_t start,
+                                        int64_t* out_indices, int32_t memory, void* stream);
+
+/*
+ * Squared flood value of k-simplices over their relative-interior grid rows.
+ * The kernel boundary that replaces the per-cell masked minimisation of
+ * floodph/filtration.py:233 _grid_values_masked (mask: filtration.py:130
+ * compute_mask; distance kernel: floodph/_kernels.py:58 min_sq_dists):
+ *   out_sq[i] = max over rows c/m of simplex i with every c_j >= 1 of
+ *               min over cloud points x of |x - p(c)|^2
+ * (k = 0: the vertex itself; no such row, i.e. m <= k: -1).
+ * simplices: n_simplices x 4 int32 landmark ids, slots > k ignored.
+ * subset_mode = 1 when the landmarks are cloud points (Lemma 4.2 pruning is
+ * then exact); 0 searches the whole cloud (the reference's kdtree route,
+ * filtration.py:274).
+ */
+int fph_flood_interior(const double* points, int64_t n_points, int32_t dim,
+                       const double* landmarks, int64_t n_landmarks, const int32_t* simplices,
+                       int64_t n_simplices, int32_t k, int32_t grid_resolution,
+                       int32_t subset_mode, double* out_sq, int32_t memory, void* stream);
+
+/*
+ * Squared flood values of a whole Delaunay complex.
+ * Replaces the msq_by_dim produced by floodph/filtration.py:233
+ * _grid_values_masked (and :274 _grid_values_kdtree for external landmarks)
+ * inside build_flood_filtration (filtration.py:348).
+ *   counts[k]     number of k-simplices, k = 0..max_dim
+ *   simplices[k]  counts[k] x (k+1) int32 sorted vertex ids (k >= 1; [0] unused)
+ *   facets[k]     counts[k] x (k+1) int32 row of the facet dropping vertex j
+ *                 in dimension k-1 (Triangulation.facet_links; [0] unused)
+ *   out_sq[k]     counts[k] float64 squared values (vertices: 0 in subset mode)
+ */
+int fph_flood_filtration(const double* points, int64_t n_points, int32_t dim,
+                         const double* landmarks, int64_t n_landmarks, int32_t max_dim,
+                         const int64_t* counts, const int32_t* const* simplices,
+                         const int32_t* const* facets, int32_t grid_resolution,
+                         int32_t subset_mode, double* const* out_sq, int32_t memory,
+                         void* stream);
+
+/*
+ * Facet completion for sharded runs (device memory only): out[i] =
+ * max(interior_sq[i], lower_sq[facets[i][j]] for j <= k).  This is the
+ * face-nesting identity that replaces the reference's per-cell face
+ * extraction (floodph/filtration.py:227 _extract_faces).
+ */
+int fph_flood_complete(const double* interior_sq, const int32_t* facets, int64_t n, int32_t k,
+                       const double* lower_sq, double* out_sq, void* stream);
+
+/*
+ * Tuning knobs (<= 0 keeps the default): target points per grid cell if the
+ * cloud filled its bounding box, and fp32 pairs per flood task.
+ */
+int fph_set_tuning(double cell_occupancy, double pairs_per_task);
+
+/* Kernel launches issued by this thread since the last reset (for bench accounting). */
+int64_t fph_launch_count(int32_t reset);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* FLOODPH_B200_H */

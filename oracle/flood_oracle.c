@@ -15,7 +15,7 @@
  *                  floodph/_kernels.py:41 _min_sq_dists_nb
  *   - grid rows are  p = w0*v0; p = p + w1*v1; ...  with w = c / m
  *       reference: floodph/geometry.py:178 barycentric_grid_template,
- *                  floodph/geometry.py:~205 barycentric_grid
+ *                  floodph/geometry.py:200 barycentric_grid
  *   - Ritter ball: center = 0.5*(vi+vj) of the first longest edge in
  *     combinations order, radius = sqrt(max_i |v_i - c|^2)
  *       reference: floodph/geometry.py:123 ritter_enclosing_ball

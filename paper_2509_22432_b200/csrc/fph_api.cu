@@ -1,0 +1,389 @@
+// fph_api.cu -- extern "C" entry points (include/floodph_b200.h).
+//
+// Host-memory calls stage inputs on the current device, run on a private
+// stream and copy results back; device-memory calls run on the caller's
+// stream.  Scratch comes from the stream-ordered allocator (cudaMallocAsync)
+// whose pool is kept warm, so repeated calls do not pay cudaMalloc.
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <vector>
+
+#include "../../include/floodph_b200.h"
+#include "fph_flood.cuh"
+#include "fph_grid.cuh"
+
+namespace fph {
+
+static thread_local char g_err[1024] = "";
+static double g_occupancy = 8.0;
+static double g_pairs_per_task = 0.0;
+static thread_local long long g_launches = 0;
+
+void set_error(const char* fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+}
+
+void count_launches(int n) { g_launches += n; }
+
+namespace {
+
+__global__ void soa_kernel(const double* __restrict__ pts, long long n, int dim,
+                           double* __restrict__ x, double* __restrict__ y,
+                           double* __restrict__ z) {
+    long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    x[i] = pts[i * dim];
+    y[i] = pts[i * dim + 1];
+    z[i] = dim == 3 ? pts[i * dim + 2] : 0.0;
+}
+
+__global__ void pad3_kernel(const double* __restrict__ pts, long long n, int dim,
+                            double* __restrict__ out) {
+    long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    out[i * 3] = pts[i * dim];
+    out[i * 3 + 1] = pts[i * dim + 1];
+    out[i * 3 + 2] = dim == 3 ? pts[i * dim + 2] : 0.0;
+}
+
+__global__ void pad4_kernel(const int* __restrict__ s, long long n, int k, int* __restrict__ out) {
+    long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    for (int j = 0; j < 4; ++j) out[i * 4 + j] = j <= k ? s[i * (k + 1) + j] : -1;
+}
+
+__global__ void fill_kernel(double* out, long long n, double v) {
+    long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (i < n) out[i] = v;
+}
+
+unsigned blocks_for(long long n) { return (unsigned)((n + 255) / 256); }
+
+// RAII for stream-ordered scratch
+struct Scratch {
+    cudaStream_t stream;
+    std::vector<void*> ptrs;
+    explicit Scratch(cudaStream_t s) : stream(s) {}
+    template <class T>
+    int alloc(T** p, size_t count) {
+        void* q = nullptr;
+        cudaError_t e = cudaMallocAsync(&q, count * sizeof(T) + 16, stream);
+        if (e != cudaSuccess) {
+            set_error("cudaMallocAsync(%zu bytes): %s", count * sizeof(T), cudaGetErrorString(e));
+            return FPH_ENOMEM;
+        }
+        ptrs.push_back(q);
+        *p = static_cast<T*>(q);
+        return FPH_OK;
+    }
+    ~Scratch() {
+        for (void* p : ptrs) cudaFreeAsync(p, stream);
+    }
+};
+
+// Host-call context: private stream on the current device
+struct HostCtx {
+    cudaStream_t stream = nullptr;
+    bool owned = false;
+    int init(int memory, void* user_stream) {
+        if (memory == FPH_MEM_DEVICE) {
+            stream = static_cast<cudaStream_t>(user_stream);
+            return FPH_OK;
+        }
+        FPH_CUDA_TRY(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+        owned = true;
+        return FPH_OK;
+    }
+    ~HostCtx() {
+        if (owned) {
+            cudaStreamSynchronize(stream);
+            cudaStreamDestroy(stream);
+        }
+    }
+};
+
+int ensure_device() {
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess || n == 0) {
+        set_error("no CUDA device available (%s)", e == cudaSuccess ? "0 devices"
+                                                                   : cudaGetErrorString(e));
+        return FPH_ECUDA;
+    }
+    static bool pool_ready = false;
+    if (!pool_ready) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            unsigned long long thr = ~0ull;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+        pool_ready = true;
+    }
+    return FPH_OK;
+}
+
+// Stage a host or device array as a device pointer.
+template <class T>
+int stage_in(Scratch& sc, const T* src, size_t count, int memory, const T** out) {
+    if (memory == FPH_MEM_DEVICE || count == 0) {
+        *out = src;
+        return FPH_OK;
+    }
+    T* d = nullptr;
+    FPH_TRY(sc.alloc(&d, count));
+    FPH_CUDA_TRY(cudaMemcpyAsync(d, src, count * sizeof(T), cudaMemcpyHostToDevice, sc.stream));
+    *out = d;
+    return FPH_OK;
+}
+
+int check_cloud(const double* points, int64_t n, int32_t dim) {
+    if (!points || n < 1) {
+        set_error("point cloud needs at least one point");
+        return FPH_EARG;
+    }
+    if (dim != 2 && dim != 3) {
+        set_error("dimension must be 2 or 3, got %d", (int)dim);
+        return FPH_EARG;
+    }
+    if (n > 0x7fffffffLL) {
+        set_error("clouds above 2^31 points are not supported");
+        return FPH_EARG;
+    }
+    return FPH_OK;
+}
+
+}  // namespace
+}  // namespace fph
+
+using namespace fph;
+
+extern "C" {
+
+int fph_abi_version(void) { return FPH_ABI_VERSION; }
+
+const char* fph_last_error(void) { return g_err; }
+
+int fph_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
+    return n;
+}
+
+int fph_set_tuning(double cell_occupancy, double pairs_per_task) {
+    g_occupancy = cell_occupancy > 0 ? cell_occupancy : 8.0;
+    g_pairs_per_task = pairs_per_task > 0 ? pairs_per_task : 0.0;
+    return FPH_OK;
+}
+
+int fph_flood_complete(const double* interior_sq, const int32_t* facets, int64_t n, int32_t k,
+                       const double* lower_sq, double* out_sq, void* stream) {
+    g_err[0] = 0;
+    if (k < 1 || k > 3 || n < 0) {
+        set_error("fph_flood_complete: need 1 <= k <= 3 and n >= 0");
+        return FPH_EARG;
+    }
+    FPH_TRY(ensure_device());
+    count_launches(1);
+    return flood_complete(interior_sq, facets, (int)n, k, lower_sq, out_sq,
+                          static_cast<cudaStream_t>(stream));
+}
+
+int64_t fph_launch_count(int32_t reset) {
+    long long v = g_launches;
+    if (reset) g_launches = 0;
+    return v;
+}
+
+int fph_farthest_point_sampling(const double* points, int64_t n, int32_t dim, int64_t k,
+                                int64_t start, int64_t* out_indices, int32_t memory,
+                                void* stream) {
+    g_err[0] = 0;
+    FPH_TRY(check_cloud(points, n, dim));
+    if (k < 1 || k > n) {
+        set_error("k must be in [1, %lld], got %lld", (long long)n, (long long)k);
+        return FPH_EARG;
+    }
+    if (start < 0 || start >= n) {
+        set_error("start must be in [0, %lld), got %lld", (long long)n, (long long)start);
+        return FPH_EARG;
+    }
+    FPH_TRY(ensure_device());
+    HostCtx hc;
+    FPH_TRY(hc.init(memory, stream));
+    int rc = FPH_OK;
+    {
+        Scratch sc(hc.stream);
+        const double* d_pts = nullptr;
+        FPH_TRY(stage_in(sc, points, (size_t)n * dim, memory, &d_pts));
+        double *x, *y, *z;
+        FPH_TRY(sc.alloc(&x, n));
+        FPH_TRY(sc.alloc(&y, n));
+        FPH_TRY(sc.alloc(&z, n));
+        soa_kernel<<<blocks_for(n), 256, 0, hc.stream>>>(d_pts, n, dim, x, y, z);
+        count_launches(1);
+        long long* d_out = reinterpret_cast<long long*>(out_indices);
+        if (memory == FPH_MEM_HOST) FPH_TRY(sc.alloc(&d_out, k));
+        rc = fps_run(x, y, z, (int)n, (int)k, (int)start, d_out, hc.stream);
+        count_launches(1);
+        if (rc == FPH_OK && memory == FPH_MEM_HOST) {
+            FPH_CUDA_TRY(cudaMemcpyAsync(out_indices, d_out, sizeof(long long) * k,
+                                         cudaMemcpyDeviceToHost, hc.stream));
+        }
+    }
+    if (memory == FPH_MEM_HOST) FPH_CUDA_TRY(cudaStreamSynchronize(hc.stream));
+    return rc;
+}
+
+int fph_farthest_point_sampling_batched(const double* points, int64_t batch, int64_t n,
+                                        int32_t dim, int64_t k, int64_t start,
+                                        int64_t* out_indices, int32_t memory, void* stream) {
+    g_err[0] = 0;
+    if (batch < 0) {
+        set_error("batch must be nonnegative");
+        return FPH_EARG;
+    }
+    for (int64_t b = 0; b < batch; ++b) {
+        FPH_TRY(fph_farthest_point_sampling(points + b * n * dim, n, dim, k, start,
+                                            out_indices + b * k, memory, stream));
+    }
+    return FPH_OK;
+}
+
+int fph_flood_interior(const double* points, int64_t n_points, int32_t dim,
+                       const double* landmarks, int64_t n_landmarks, const int32_t* simplices,
+                       int64_t n_simplices, int32_t k, int32_t grid_resolution,
+                       int32_t subset_mode, double* out_sq, int32_t memory, void* stream) {
+    g_err[0] = 0;
+    FPH_TRY(check_cloud(points, n_points, dim));
+    if (k < 0 || k > 3 || grid_resolution < 1 || grid_resolution > 255 || n_landmarks < 1) {
+        set_error("need 0 <= k <= 3, 1 <= grid_resolution <= 255 and landmarks");
+        return FPH_EARG;
+    }
+    if (n_simplices == 0) return FPH_OK;
+    FPH_TRY(ensure_device());
+    HostCtx hc;
+    FPH_TRY(hc.init(memory, stream));
+    int rc = FPH_OK;
+    {
+        Scratch sc(hc.stream);
+        const double *d_pts, *d_lm;
+        const int32_t* d_s;
+        FPH_TRY(stage_in(sc, points, (size_t)n_points * dim, memory, &d_pts));
+        FPH_TRY(stage_in(sc, landmarks, (size_t)n_landmarks * dim, memory, &d_lm));
+        FPH_TRY(stage_in(sc, simplices, (size_t)n_simplices * 4, memory, &d_s));
+        double* lm3;
+        FPH_TRY(sc.alloc(&lm3, (size_t)n_landmarks * 3));
+        pad3_kernel<<<blocks_for(n_landmarks), 256, 0, hc.stream>>>(d_lm, n_landmarks, dim, lm3);
+        count_launches(1);
+        GridStore gs;
+        rc = grid_build(d_pts, (int)n_points, dim, 0.0, g_occupancy, hc.stream, &gs);
+        count_launches(4);
+        if (rc == FPH_OK) {
+            double* d_out = out_sq;
+            if (memory == FPH_MEM_HOST) FPH_TRY(sc.alloc(&d_out, n_simplices));
+            FloodTuning tune;
+            tune.pairs_per_task = g_pairs_per_task;
+            rc = flood_interior(gs.grid, lm3, d_s, (int)n_simplices, k, grid_resolution,
+                                subset_mode, d_out, tune, hc.stream);
+            count_launches(4);
+            if (rc == FPH_OK && memory == FPH_MEM_HOST)
+                FPH_CUDA_TRY(cudaMemcpyAsync(out_sq, d_out, sizeof(double) * n_simplices,
+                                             cudaMemcpyDeviceToHost, hc.stream));
+        }
+        gs.free_all(hc.stream);
+    }
+    if (memory == FPH_MEM_HOST) FPH_CUDA_TRY(cudaStreamSynchronize(hc.stream));
+    return rc;
+}
+
+int fph_flood_filtration(const double* points, int64_t n_points, int32_t dim,
+                         const double* landmarks, int64_t n_landmarks, int32_t max_dim,
+                         const int64_t* counts, const int32_t* const* simplices,
+                         const int32_t* const* facets, int32_t grid_resolution,
+                         int32_t subset_mode, double* const* out_sq, int32_t memory,
+                         void* stream) {
+    g_err[0] = 0;
+    FPH_TRY(check_cloud(points, n_points, dim));
+    if (max_dim < 0 || max_dim > 3 || grid_resolution < 1 || grid_resolution > 255 ||
+        n_landmarks < 1 || !counts) {
+        set_error("need 0 <= max_dim <= 3, 1 <= grid_resolution <= 255 and landmarks");
+        return FPH_EARG;
+    }
+    FPH_TRY(ensure_device());
+    HostCtx hc;
+    FPH_TRY(hc.init(memory, stream));
+    int rc = FPH_OK;
+    {
+        Scratch sc(hc.stream);
+        const double *d_pts, *d_lm;
+        FPH_TRY(stage_in(sc, points, (size_t)n_points * dim, memory, &d_pts));
+        FPH_TRY(stage_in(sc, landmarks, (size_t)n_landmarks * dim, memory, &d_lm));
+        double* lm3;
+        FPH_TRY(sc.alloc(&lm3, (size_t)n_landmarks * 3));
+        pad3_kernel<<<blocks_for(n_landmarks), 256, 0, hc.stream>>>(d_lm, n_landmarks, dim, lm3);
+        count_launches(1);
+        GridStore gs;
+        rc = grid_build(d_pts, (int)n_points, dim, 0.0, g_occupancy, hc.stream, &gs);
+        count_launches(4);
+        FloodTuning tune;
+        tune.pairs_per_task = g_pairs_per_task;
+        double* d_vals[4] = {nullptr, nullptr, nullptr, nullptr};
+        for (int k = 0; k <= max_dim && rc == FPH_OK; ++k) {
+            const long long nk = counts[k];
+            double* d_out = out_sq[k];
+            if (memory == FPH_MEM_HOST) FPH_TRY(sc.alloc(&d_out, nk > 0 ? nk : 1));
+            d_vals[k] = d_out;
+            if (nk == 0) continue;
+            if (k == 0) {
+                if (subset_mode) {
+                    fill_kernel<<<blocks_for(nk), 256, 0, hc.stream>>>(d_out, nk, 0.0);
+                    count_launches(1);
+                } else {
+                    // vertices: nearest cloud point of each landmark
+                    int* s4;
+                    FPH_TRY(sc.alloc(&s4, (size_t)nk * 4));
+                    std::vector<int> ids((size_t)nk * 4, -1);
+                    for (long long i = 0; i < nk; ++i) ids[i * 4] = (int)i;
+                    FPH_CUDA_TRY(cudaMemcpyAsync(s4, ids.data(), sizeof(int) * ids.size(),
+                                                 cudaMemcpyHostToDevice, hc.stream));
+                    rc = flood_interior(gs.grid, lm3, s4, (int)nk, 0, grid_resolution, 0, d_out,
+                                        tune, hc.stream);
+                    count_launches(4);
+                }
+                continue;
+            }
+            const int32_t *d_s, *d_f;
+            FPH_TRY(stage_in(sc, simplices[k], (size_t)nk * (k + 1), memory, &d_s));
+            FPH_TRY(stage_in(sc, facets[k], (size_t)nk * (k + 1), memory, &d_f));
+            int* s4;
+            double* interior;
+            FPH_TRY(sc.alloc(&s4, (size_t)nk * 4));
+            FPH_TRY(sc.alloc(&interior, (size_t)nk));
+            pad4_kernel<<<blocks_for(nk), 256, 0, hc.stream>>>(d_s, nk, k, s4);
+            count_launches(1);
+            rc = flood_interior(gs.grid, lm3, s4, (int)nk, k, grid_resolution, subset_mode,
+                                interior, tune, hc.stream);
+            count_launches(4);
+            if (rc != FPH_OK) break;
+            rc = flood_complete(interior, d_f, (int)nk, k, d_vals[k - 1], d_out, hc.stream);
+            count_launches(1);
+        }
+        if (rc == FPH_OK && memory == FPH_MEM_HOST) {
+            for (int k = 0; k <= max_dim; ++k)
+                if (counts[k] > 0)
+                    FPH_CUDA_TRY(cudaMemcpyAsync(out_sq[k], d_vals[k], sizeof(double) * counts[k],
+                                                 cudaMemcpyDeviceToHost, hc.stream));
+        }
+        gs.free_all(hc.stream);
+    }
+    if (memory == FPH_MEM_HOST) FPH_CUDA_TRY(cudaStreamSynchronize(hc.stream));
+    return rc;
+}
+
+}  // extern "C"

@@ -1,0 +1,651 @@
+// fph_flood.cu -- the flooding kernel: per-simplex max over barycentric
+// sample points of the min distance to the cloud.
+//
+// Replaces the reference's masked minimisation (floodph/filtration.py:233
+// _grid_values_masked, :130 compute_mask, floodph/_kernels.py:41
+// _min_sq_dists_nb).  The reference values every grid row of each top cell
+// against the cloud points inside the cell's sqrt(2)-inflated Ritter ball
+// and reads face values off the cell's grid.  Because face rows are bitwise
+// the face's own grid rows (reference test_geometry.py
+// test_grid_face_rows_bitwise_equal_own_grid) and max is exact, the value of
+// a simplex equals max(value over its RELATIVE-INTERIOR rows, values of its
+// facets); this file computes the interior part once per simplex of every
+// dimension (no row is evaluated twice) and fph_complete_kernel folds in the
+// facets.
+//
+// Numerics.  Results are bit-identical to the reference's float64 values:
+//   1. fp32 pass: sample point b and candidates a are taken relative to the
+//      simplex's Ritter center (float64 subtract, one rounding to fp32), and
+//      q = |a|^2 - 2 a.b is evaluated with packed FFMA2 (two candidates per
+//      instruction) and a 3-input FMNMX3 -- 3 FFMA2 + 1 FMNMX3 per 2 pairs.
+//      m32(p) = min q + |b|^2 differs from the exact squared distance by at
+//      most E(p) = 40 u32 (|b| + sqrt(m32))^2 (derivation in DESIGN.md).
+//   2. exact refine: only points with m32 + E >= max_p (m32 - E) can hold
+//      the maximum; each is re-evaluated in float64 with the reference's
+//      operation order over the grid cells of the small ball
+//      |x - p| <= sqrt(m32 + 2E), which provably contains the float64
+//      nearest neighbour.  The max of those exact minima is the reference's
+//      value.  Points are visited in decreasing m32 and skipped once they
+//      cannot beat the running max, so usually 1-3 points are refined.
+#include <cub/cub.cuh>
+
+#include <cfloat>
+#include <cmath>
+#include <vector>
+
+#include "fph_flood.cuh"
+
+namespace fph {
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kTile = 2048;           // candidates staged per flush (32 KB)
+constexpr double kU32 = 5.9604644775390625e-08;  // 2^-24
+
+// ------------------------------------------------------------ block scan
+// exclusive prefix sum over the CTA; returns the total in `total`
+__device__ __forceinline__ int block_excl(int v, int* warp_buf, int& total) {
+    int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    int incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        int t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+    }
+    __syncthreads();
+    if (lane == 31) warp_buf[w] = incl;
+    __syncthreads();
+    if (w == 0) {
+        int x = lane < (kThreads / 32) ? warp_buf[lane] : 0;
+        int xi = x;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            int t = __shfl_up_sync(0xffffffffu, xi, o);
+            if (lane >= o) xi += t;
+        }
+        if (lane < (kThreads / 32)) warp_buf[lane] = xi - x;
+        if (lane == (kThreads / 32) - 1) warp_buf[kThreads / 32] = xi;
+    }
+    __syncthreads();
+    total = warp_buf[kThreads / 32];
+    return warp_buf[w] + incl - v;
+}
+
+__device__ __forceinline__ float block_max_f(float v, float* buf) {
+    v = warp_max(v);
+    int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    __syncthreads();
+    if (lane == 0) buf[w] = v;
+    __syncthreads();
+    float r = buf[0];
+    for (int i = 1; i < kThreads / 32; ++i) r = fmaxf(r, buf[i]);
+    __syncthreads();
+    return r;
+}
+
+__device__ __forceinline__ double block_min_d(double v, double* buf) {
+    v = warp_min_d(v);
+    int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    __syncthreads();
+    if (lane == 0) buf[w] = v;
+    __syncthreads();
+    double r = buf[0];
+    for (int i = 1; i < kThreads / 32; ++i) r = fmin(r, buf[i]);
+    __syncthreads();
+    return r;
+}
+
+// ----------------------------------------------------- simplex geometry
+struct Verts {
+    double v[4][3];
+};
+
+__device__ __forceinline__ void load_verts(const FloodArgs& a, int s, Verts& V) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        int id = j <= a.k ? a.simplices[(size_t)s * 4 + j] : -1;
+        V.v[j][0] = id >= 0 ? a.landmarks[(size_t)id * 3 + 0] : 0.0;
+        V.v[j][1] = id >= 0 ? a.landmarks[(size_t)id * 3 + 1] : 0.0;
+        V.v[j][2] = id >= 0 ? a.landmarks[(size_t)id * 3 + 2] : 0.0;
+    }
+}
+
+// Reference barycentric row: p = w0*v0; p = p + wj*vj (w = c/m), no FMA
+// (floodph/geometry.py barycentric_grid + barycentric_grid_template).
+__device__ __forceinline__ void embed_row(const Verts& V, int k, uchar4 c, double m,
+                                          double p[3]) {
+    const unsigned char cc[4] = {c.x, c.y, c.z, c.w};
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        double w = __ddiv_rn((double)cc[0], m);
+        double acc = __dmul_rn(w, V.v[0][a]);
+#pragma unroll
+        for (int j = 1; j < 4; ++j) {
+            if (j <= k) {
+                double wj = __ddiv_rn((double)cc[j], m);
+                acc = __dadd_rn(acc, __dmul_rn(wj, V.v[j][a]));
+            }
+        }
+        p[a] = acc;
+    }
+}
+
+// Ritter ball exactly as reference floodph/geometry.py:123 (first longest
+// edge in combinations order, center its midpoint, radius the farthest
+// vertex).  Only used to bound candidate sets, kept exact anyway.
+__device__ __forceinline__ double ritter(const Verts& V, int k, double c[3]) {
+    if (k == 0) {
+        c[0] = V.v[0][0];
+        c[1] = V.v[0][1];
+        c[2] = V.v[0][2];
+        return 0.0;
+    }
+    double best = -1.0;
+    double c0 = 0, c1 = 0, c2 = 0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = i + 1; j < 4; ++j) {
+            if (j <= k) {
+                double d = sq64(V.v[i][0], V.v[i][1], V.v[i][2], V.v[j][0], V.v[j][1], V.v[j][2]);
+                if (d > best) {
+                    best = d;
+                    c0 = __dmul_rn(0.5, __dadd_rn(V.v[i][0], V.v[j][0]));
+                    c1 = __dmul_rn(0.5, __dadd_rn(V.v[i][1], V.v[j][1]));
+                    c2 = __dmul_rn(0.5, __dadd_rn(V.v[i][2], V.v[j][2]));
+                }
+            }
+        }
+    c[0] = c0;
+    c[1] = c1;
+    c[2] = c2;
+    double mx = -1.0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+        if (i <= k) mx = fmax(mx, sq64(V.v[i][0], V.v[i][1], V.v[i][2], c0, c1, c2));
+    return sqrt(mx);
+}
+
+// ------------------------------------------------------------ setup
+// One warp per simplex: Ritter ball, candidate cell box, candidate count,
+// and the number of tasks the simplex is split into.
+__global__ void setup_kernel(FloodArgs a, SimplexGeom* __restrict__ geom,
+                             int* __restrict__ ntasks) {
+    int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    int lane = threadIdx.x & 31;
+    if (warp >= a.n) return;
+    Verts V;
+    load_verts(a, warp, V);
+    SimplexGeom G;
+    double c[3];
+    double r = ritter(V, a.k, c);
+    G.cx = c[0];
+    G.cy = c[1];
+    G.cz = c[2];
+    G.r = r;
+    // sqrt(2) r: Lemma 4.2 masking radius; tiny relative slack for rounding
+    G.rho = a.subset ? 1.4142135623730951 * r * (1.0 + 1e-9) : 0.0;
+    Box b = a.subset ? ball_box(a.g, c[0], c[1], c[2], G.rho) : full_box(a.g);
+    G.box = b;
+    int rows = b.rows();
+    long long cand = 0;
+    for (int rr = lane; rr < rows; rr += 32) {
+        int2 run = row_run(a.g, b, rr, c[0], c[1], c[2], G.rho, a.subset != 0);
+        cand += run.y - run.x;
+    }
+    for (int o = 16; o > 0; o >>= 1) cand += __shfl_xor_sync(0xffffffffu, cand, o);
+    int npc = (a.P + a.chunk_pts - 1) / a.chunk_pts;
+    int pc = min(a.P, a.chunk_pts);
+    double pairs = (double)pc * (double)cand;
+    int nrp = (int)fmin(fmax(1.0, ceil(pairs / a.pairs_per_task)), (double)max(rows, 1));
+    G.nrp = nrp;
+    G.npc = npc;
+    if (lane == 0) {
+        geom[warp] = G;
+        ntasks[warp] = a.P > 0 ? npc * nrp : 0;
+    }
+}
+
+// --------------------------------------------------------- fp32 pass
+struct SmemPass {
+    float4 tileA[kTile / 2];  // pair p: (c0.x, c1.x, c0.y, c1.y)
+    float4 tileB[kTile / 2];  //         (c0.z, c1.z, c0.w, c1.w)
+    int row_off[kThreads + 1];
+    int row_beg[kThreads];
+    int warp_buf[kThreads / 32 + 1];
+    float fbuf[kThreads / 32];
+    double dbuf[kThreads / 32];
+    int task, last;
+    int list[kThreads];
+    int list_n;
+};
+
+template <int PPT>
+__device__ __forceinline__ void compute_tile(SmemPass& S, int n, int g, int G, bool active,
+                                             const float (&bx)[PPT], const float (&by)[PPT],
+                                             const float (&bz)[PPT], float (&best)[PPT]) {
+    if ((n & 1) && threadIdx.x == 0) {
+        float* A = reinterpret_cast<float*>(S.tileA);
+        float* B = reinterpret_cast<float*>(S.tileB);
+        int p = n >> 1;
+        A[p * 4 + 1] = 0.f;
+        A[p * 4 + 3] = 0.f;
+        B[p * 4 + 1] = 0.f;
+        B[p * 4 + 3] = INFINITY;  // w = +inf: never the minimum
+    }
+    __syncthreads();
+    if (active) {
+        int np = (n + 1) >> 1;
+        int p0 = (int)((long long)np * g / G), p1 = (int)((long long)np * (g + 1) / G);
+#pragma unroll 2
+        for (int p = p0; p < p1; ++p) {
+            float4 A = S.tileA[p];
+            float4 B = S.tileB[p];
+            float2 cx = make_float2(A.x, A.y), cy = make_float2(A.z, A.w);
+            float2 cz = make_float2(B.x, B.y), cw = make_float2(B.z, B.w);
+#pragma unroll
+            for (int i = 0; i < PPT; ++i) {
+                float2 acc = ffma2(make_float2(bz[i], bz[i]), cz, cw);
+                acc = ffma2(make_float2(by[i], by[i]), cy, acc);
+                acc = ffma2(make_float2(bx[i], bx[i]), cx, acc);
+                best[i] = fmin3(best[i], acc.x, acc.y);
+            }
+        }
+    }
+    __syncthreads();
+}
+
+// Exact float64 nearest-neighbour squared distance of p over the grid cells
+// of the ball |x - p| <= R (cooperative over the CTA).
+__device__ __noinline__ double refine_point(const FloodArgs& a, SmemPass& S, const double p[3], double R) {
+    Box b = ball_box(a.g, p[0], p[1], p[2], R);
+    int rows = b.rows();
+    double best = INFINITY;
+    for (int rb = 0; rb < rows; rb += kThreads) {
+        int r = rb + threadIdx.x;
+        int2 run = r < rows ? row_run(a.g, b, r, p[0], p[1], p[2], R, true) : make_int2(0, 0);
+        int total;
+        int off = block_excl(run.y - run.x, S.warp_buf, total);
+        S.row_off[threadIdx.x] = off;
+        S.row_beg[threadIdx.x] = run.x;
+        __syncthreads();
+        int nrow = min(kThreads, rows - rb);
+        for (int f = threadIdx.x; f < total; f += kThreads) {
+            int lo = 0, hi = nrow;  // last row with off <= f
+            while (hi - lo > 1) {
+                int mid = (lo + hi) >> 1;
+                if (S.row_off[mid] <= f) lo = mid; else hi = mid;
+            }
+            int idx = S.row_beg[lo] + f - S.row_off[lo];
+            best = fmin(best, sq64(a.g.x[idx], a.g.y[idx], a.g.z[idx], p[0], p[1], p[2]));
+        }
+        __syncthreads();
+    }
+    return block_min_d(best, S.dbuf);
+}
+
+// |b| (fp32) of point j, recomputed: the Ritter center is per simplex
+__device__ __forceinline__ float point_b(const FloodArgs& a, const Verts& V, const SimplexGeom& G, int j) {
+    double p[3];
+    embed_row(V, a.k, a.tmpl[j], (double)a.m, p);
+    float fx = __double2float_rn(__dsub_rn(p[0], G.cx));
+    float fy = __double2float_rn(__dsub_rn(p[1], G.cy));
+    float fz = __double2float_rn(__dsub_rn(p[2], G.cz));
+    return sqrtf(fmaf(fz, fz, fmaf(fy, fy, fx * fx))) * 1.0001f;
+}
+
+// Finalize one simplex: pick the refine set from the fp32 minima and
+// return the exact float64 max over it.
+__device__ __noinline__ double finalize(const FloodArgs& a, SmemPass& S, int s, const Verts& V,
+                           const SimplexGeom& G) {
+    const float* m32 = a.perpoint + (size_t)s * a.P;
+    // L = max_p (m32 - E), and the argmax of m32
+    double lmax = -INFINITY;
+    float vmax = -INFINITY;
+    int jmax = 0x7fffffff;
+    for (int j = threadIdx.x; j < a.P; j += kThreads) {
+        float v = __ldcg(m32 + j);
+        float B = point_b(a, V, G, j);
+        float sv = sqrtf(fmaxf(v, 0.f)) + B;
+        float E = (float)(40.0 * kU32 * 1.01) * sv * sv;
+        lmax = fmax(lmax, (double)v - (double)E);
+        if (v > vmax) {
+            vmax = v;
+            jmax = j;
+        }
+    }
+    double L = -block_min_d(-lmax, S.dbuf);
+    // argmax (lowest index among ties; any maximiser works)
+    float vm = block_max_f(vmax, S.fbuf);
+    int cand = vmax == vm ? jmax : 0x7fffffff;
+    for (int o = 16; o > 0; o >>= 1) cand = min(cand, __shfl_xor_sync(0xffffffffu, cand, o));
+    if ((threadIdx.x & 31) == 0) S.row_beg[threadIdx.x >> 5] = cand;
+    __syncthreads();
+    int jm = S.row_beg[0];
+    for (int w = 1; w < kThreads / 32; ++w) jm = min(jm, S.row_beg[w]);
+    __syncthreads();
+
+    double M = -INFINITY;
+    // refine the fp32 argmax first, then anything that can still beat M
+    for (int pass = 0; pass < 2; ++pass) {
+        for (int base = 0; base < (pass == 0 ? 1 : a.P); base += kThreads) {
+            int j = pass == 0 ? jm : base + threadIdx.x;
+            bool want = false;
+            float v = 0.f, E = 0.f;
+            if ((pass == 0 && threadIdx.x == 0) || (pass == 1 && j < a.P && j != jm)) {
+                v = __ldcg(m32 + j);
+                float B = point_b(a, V, G, j);
+                float sv = sqrtf(fmaxf(v, 0.f)) + B;
+                E = (float)(40.0 * kU32 * 1.01) * sv * sv;
+                want = (double)v + (double)E >= (double)L && (double)v + (double)E > M;
+            }
+            int tot;
+            int pos = block_excl(want ? 1 : 0, S.warp_buf, tot);
+            if (want) S.list[pos] = j;
+            __syncthreads();
+            for (int t = 0; t < tot; ++t) {
+                int jj = S.list[t];
+                float vv = __ldcg(m32 + jj);
+                float B = point_b(a, V, G, jj);
+                float sv = sqrtf(fmaxf(vv, 0.f)) + B;
+                float EE = (float)(40.0 * kU32 * 1.01) * sv * sv;
+                if ((double)vv + (double)EE <= M) continue;  // uniform across the CTA
+                double p[3];
+                embed_row(V, a.k, a.tmpl[jj], (double)a.m, p);
+                double R2 = fmax((double)vv + 2.0 * (double)EE, 0.0);
+                double R = sqrt(R2) * (1.0 + 1e-6) + 1e-300;
+                double m64 = refine_point(a, S, p, R);
+                M = fmax(M, m64);
+            }
+            __syncthreads();
+        }
+    }
+    return M;
+}
+
+template <int PPT>
+__global__ void __launch_bounds__(kThreads, 2) pass_kernel(FloodArgs a, const SimplexGeom* geom,
+                                                        const int* task_off, int* task_counter,
+                                                        int* done) {
+    __shared__ SmemPass S;
+    const int total_tasks = task_off[a.n];
+    for (;;) {
+        if (threadIdx.x == 0) S.task = atomicAdd(task_counter, 1);
+        __syncthreads();
+        const int t = S.task;
+        __syncthreads();
+        if (t >= total_tasks) return;
+        // simplex owning task t: last s with task_off[s] <= t
+        int lo = 0, hi = a.n;
+        while (hi - lo > 1) {
+            int mid = (lo + hi) >> 1;
+            if (task_off[mid] <= t) lo = mid; else hi = mid;
+        }
+        const int s = lo;
+        const SimplexGeom G = geom[s];
+        const int jt = t - task_off[s];
+        const int nt = G.npc * G.nrp;
+        const int pc = jt % G.npc, rp = jt / G.npc;
+        const int rows = G.box.rows();
+        const int row_lo = (int)((long long)rows * rp / G.nrp);
+        const int row_hi = (int)((long long)rows * (rp + 1) / G.nrp);
+        const int pbase = pc * a.chunk_pts;
+        const int Pc = min(a.P - pbase, a.chunk_pts);
+        const int Q = (Pc + PPT - 1) / PPT;
+        const int Gn = kThreads / Q;
+        const int slot = threadIdx.x % Q, g = threadIdx.x / Q;
+        const bool active = g < Gn;
+        Verts V;
+        load_verts(a, s, V);
+        float bx[PPT], by[PPT], bz[PPT], bb[PPT], best[PPT];
+#pragma unroll
+        for (int i = 0; i < PPT; ++i) {
+            int jl = min(slot * PPT + i, Pc - 1);
+            double p[3];
+            embed_row(V, a.k, a.tmpl[pbase + jl], (double)a.m, p);
+            float fx = __double2float_rn(__dsub_rn(p[0], G.cx));
+            float fy = __double2float_rn(__dsub_rn(p[1], G.cy));
+            float fz = __double2float_rn(__dsub_rn(p[2], G.cz));
+            bx[i] = -2.f * fx;
+            by[i] = -2.f * fy;
+            bz[i] = -2.f * fz;
+            bb[i] = fmaf(fz, fz, fmaf(fy, fy, fx * fx));
+            best[i] = INFINITY;
+        }
+        const float thr = a.subset ? (float)(G.rho * G.rho * (1.0 + 1e-5)) : INFINITY;
+        int tile_n = 0;
+        for (int rb = row_lo; rb < row_hi; rb += kThreads) {
+            int r = rb + threadIdx.x;
+            int2 run = r < row_hi ? row_run(a.g, G.box, r, G.cx, G.cy, G.cz, G.rho, a.subset != 0)
+                                  : make_int2(0, 0);
+            int total;
+            int off = block_excl(run.y - run.x, S.warp_buf, total);
+            S.row_off[threadIdx.x] = off;
+            S.row_beg[threadIdx.x] = run.x;
+            __syncthreads();
+            const int nrow = min(kThreads, row_hi - rb);
+            for (int f0 = 0; f0 < total; f0 += kThreads) {
+                int f = f0 + threadIdx.x;
+                bool keep = false;
+                float ax = 0.f, ay = 0.f, az = 0.f, aw = 0.f;
+                if (f < total) {
+                    int l = 0, h = nrow;
+                    while (h - l > 1) {
+                        int mid = (l + h) >> 1;
+                        if (S.row_off[mid] <= f) l = mid; else h = mid;
+                    }
+                    int idx = S.row_beg[l] + f - S.row_off[l];
+                    ax = __double2float_rn(__dsub_rn(a.g.x[idx], G.cx));
+                    ay = __double2float_rn(__dsub_rn(a.g.y[idx], G.cy));
+                    az = __double2float_rn(__dsub_rn(a.g.z[idx], G.cz));
+                    aw = fmaf(az, az, fmaf(ay, ay, ax * ax));
+                    keep = aw <= thr;
+                }
+                int kept;
+                int pos = block_excl(keep ? 1 : 0, S.warp_buf, kept);
+                if (keep) {
+                    int q = tile_n + pos;
+                    float* A = reinterpret_cast<float*>(S.tileA) + (q >> 1) * 4 + (q & 1);
+                    float* B = reinterpret_cast<float*>(S.tileB) + (q >> 1) * 4 + (q & 1);
+                    A[0] = ax;
+                    A[2] = ay;
+                    B[0] = az;
+                    B[2] = aw;
+                }
+                tile_n += kept;
+                if (tile_n > kTile - kThreads) {
+                    compute_tile<PPT>(S, tile_n, g, Gn, active, bx, by, bz, best);
+                    tile_n = 0;
+                }
+            }
+            __syncthreads();
+        }
+        if (tile_n > 0) compute_tile<PPT>(S, tile_n, g, Gn, active, bx, by, bz, best);
+        // reduce the groups' partial minima: red[g][jl], reusing the tile
+        float* red = reinterpret_cast<float*>(S.tileA);
+        if (active) {
+#pragma unroll
+            for (int i = 0; i < PPT; ++i) red[g * (Q * PPT) + slot * PPT + i] = best[i] + bb[i];
+        }
+        __syncthreads();
+        float* out = a.perpoint + (size_t)s * a.P + pbase;
+        for (int jl = threadIdx.x; jl < Pc; jl += kThreads) {
+            float v = red[jl];
+            for (int gg = 1; gg < Gn; ++gg) v = fminf(v, red[gg * (Q * PPT) + jl]);
+            if (nt == 1) out[jl] = v;
+            else atomicMin(reinterpret_cast<unsigned*>(out) + jl, f2ord(v));
+        }
+        __threadfence();
+        __syncthreads();
+        if (threadIdx.x == 0) S.last = nt == 1 ? 1 : (atomicAdd(done + s, 1) == nt - 1);
+        __syncthreads();
+        if (!S.last) continue;
+        __threadfence();
+        if (nt > 1) {  // decode the ordered-uint minima in place
+            for (int j = threadIdx.x; j < a.P; j += kThreads) {
+                unsigned* u = reinterpret_cast<unsigned*>(a.perpoint + (size_t)s * a.P) + j;
+                *u = __float_as_uint(ord2f(__ldcg(u)));
+            }
+            __threadfence();
+            __syncthreads();
+        }
+        double M = finalize(a, S, s, V, G);
+        if (threadIdx.x == 0) a.out_sq[s] = M;
+        __syncthreads();
+    }
+}
+
+__global__ void init_perpoint_kernel(unsigned* p, long long n) {
+    long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (i < n) p[i] = 0xffffffffu;
+}
+
+__global__ void no_interior_kernel(double* out, int n) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = -1.0;
+}
+
+}  // namespace
+
+int choose_ppt(int P) {
+    // fewest idle threads across {1,2,4,8} points per thread, ties -> larger
+    int best = 1;
+    long long best_idle = 1ll << 60;
+    for (int ppt : {1, 2, 4, 8}) {
+        int pc = P < kThreads * ppt ? P : kThreads * ppt;
+        int Q = (pc + ppt - 1) / ppt;
+        if (Q > kThreads || Q < 1) continue;
+        int G = kThreads / Q;
+        long long idle = (long long)kThreads * ppt - (long long)G * pc;
+        if (idle <= best_idle) {
+            best_idle = idle;
+            best = ppt;
+        }
+    }
+    return best;
+}
+
+int flood_interior(const Grid& g, const double* d_landmarks3, const int* d_simplices, int n,
+                   int k, int m, int subset, double* d_out_sq, const FloodTuning& tune,
+                   cudaStream_t stream) {
+    if (n == 0) return FPH_OK;
+    if (k < 0 || k > 3 || m < 1 || m > 255) {
+        set_error("flood_interior: need 0 <= k <= 3 and 1 <= m <= 255");
+        return FPH_EARG;
+    }
+    // interior compositions of m into k+1 positive parts (k = 0: the vertex)
+    std::vector<uchar4> tmpl;
+    if (k == 0) {
+        tmpl.push_back(make_uchar4((unsigned char)m, 0, 0, 0));
+    } else {
+        int c[4] = {0, 0, 0, 0};
+        if (k == 1) {
+            for (c[0] = 1; c[0] <= m - 1; ++c[0]) tmpl.push_back(make_uchar4(c[0], m - c[0], 0, 0));
+        } else if (k == 2) {
+            for (c[0] = 1; c[0] <= m - 2; ++c[0])
+                for (c[1] = 1; c[1] <= m - 1 - c[0]; ++c[1])
+                    tmpl.push_back(make_uchar4(c[0], c[1], m - c[0] - c[1], 0));
+        } else {
+            for (c[0] = 1; c[0] <= m - 3; ++c[0])
+                for (c[1] = 1; c[1] <= m - 2 - c[0]; ++c[1])
+                    for (c[2] = 1; c[2] <= m - 1 - c[0] - c[1]; ++c[2])
+                        tmpl.push_back(make_uchar4(c[0], c[1], c[2], m - c[0] - c[1] - c[2]));
+        }
+    }
+    const int P = (int)tmpl.size();
+    if (P == 0) {
+        no_interior_kernel<<<(n + 255) / 256, 256, 0, stream>>>(d_out_sq, n);
+        FPH_CUDA_TRY(cudaGetLastError());
+        return FPH_OK;
+    }
+    const int ppt = choose_ppt(P);
+    FloodArgs a{};
+    a.g = g;
+    a.landmarks = d_landmarks3;
+    a.simplices = d_simplices;
+    a.n = n;
+    a.k = k;
+    a.m = m;
+    a.P = P;
+    a.subset = subset;
+    a.chunk_pts = kThreads * ppt;
+    a.pairs_per_task = tune.pairs_per_task > 0 ? tune.pairs_per_task : (double)(1 << 21);
+    a.out_sq = d_out_sq;
+
+    uchar4* d_tmpl = nullptr;
+    SimplexGeom* d_geom = nullptr;
+    int *d_ntasks = nullptr, *d_task_off = nullptr, *d_counter = nullptr, *d_done = nullptr;
+    float* d_perpoint = nullptr;
+    FPH_CUDA_TRY(cudaMallocAsync(&d_tmpl, sizeof(uchar4) * P, stream));
+    FPH_CUDA_TRY(cudaMemcpyAsync(d_tmpl, tmpl.data(), sizeof(uchar4) * P, cudaMemcpyHostToDevice,
+                                 stream));
+    FPH_CUDA_TRY(cudaMallocAsync(&d_geom, sizeof(SimplexGeom) * n, stream));
+    FPH_CUDA_TRY(cudaMallocAsync(&d_ntasks, sizeof(int) * (n + 1), stream));
+    FPH_CUDA_TRY(cudaMallocAsync(&d_task_off, sizeof(int) * (n + 1), stream));
+    FPH_CUDA_TRY(cudaMallocAsync(&d_counter, sizeof(int), stream));
+    FPH_CUDA_TRY(cudaMallocAsync(&d_done, sizeof(int) * n, stream));
+    FPH_CUDA_TRY(cudaMallocAsync(&d_perpoint, sizeof(float) * (size_t)n * P, stream));
+    FPH_CUDA_TRY(cudaMemsetAsync(d_counter, 0, sizeof(int), stream));
+    FPH_CUDA_TRY(cudaMemsetAsync(d_done, 0, sizeof(int) * n, stream));
+    FPH_CUDA_TRY(cudaMemsetAsync(d_ntasks + n, 0, sizeof(int), stream));
+    long long npp = (long long)n * P;
+    init_perpoint_kernel<<<(unsigned)((npp + 255) / 256), 256, 0, stream>>>(
+        reinterpret_cast<unsigned*>(d_perpoint), npp);
+    a.tmpl = d_tmpl;
+    a.perpoint = d_perpoint;
+
+    setup_kernel<<<(n * 32 + 255) / 256, 256, 0, stream>>>(a, d_geom, d_ntasks);
+    size_t tmp_bytes = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, d_ntasks, d_task_off, n + 1, stream);
+    void* tmp = nullptr;
+    FPH_CUDA_TRY(cudaMallocAsync(&tmp, tmp_bytes, stream));
+    FPH_CUDA_TRY(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, d_ntasks, d_task_off, n + 1, stream));
+
+    int dev = 0, sms = 0, occ = 0;
+    FPH_CUDA_TRY(cudaGetDevice(&dev));
+    FPH_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    switch (ppt) {
+#define FPH_LAUNCH(PPTV)                                                                     \
+    case PPTV:                                                                               \
+        FPH_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pass_kernel<PPTV>,  \
+                                                                   kThreads, 0));            \
+        pass_kernel<PPTV><<<sms * (occ > 0 ? occ : 1), kThreads, 0, stream>>>(               \
+            a, d_geom, d_task_off, d_counter, d_done);                                       \
+        break;
+        FPH_LAUNCH(1)
+        FPH_LAUNCH(2)
+        FPH_LAUNCH(4)
+        FPH_LAUNCH(8)
+#undef FPH_LAUNCH
+    }
+    FPH_CUDA_TRY(cudaGetLastError());
+    for (void* p : {(void*)d_tmpl, (void*)d_geom, (void*)d_ntasks, (void*)d_task_off,
+                    (void*)d_counter, (void*)d_done, (void*)d_perpoint, tmp})
+        FPH_CUDA_TRY(cudaFreeAsync(p, stream));
+    return FPH_OK;
+}
+
+// value(s) = max(interior(s), max_j value(facet_j(s))) -- the face-nesting
+// identity that replaces the reference's per-cell face extraction
+// (floodph/filtration.py:227 _extract_faces).
+__global__ void complete_kernel(const double* __restrict__ interior, const int* __restrict__ facets,
+                                int n, int k, const double* __restrict__ lower,
+                                double* __restrict__ out) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double v = interior[i];
+    for (int j = 0; j <= k; ++j) v = fmax(v, lower[facets[(size_t)i * (k + 1) + j]]);
+    out[i] = v;
+}
+
+int flood_complete(const double* d_interior, const int* d_facets, int n, int k,
+                   const double* d_lower, double* d_out, cudaStream_t stream) {
+    if (n == 0) return FPH_OK;
+    complete_kernel<<<(n + 255) / 256, 256, 0, stream>>>(d_interior, d_facets, n, k, d_lower,
+                                                         d_out);
+    FPH_CUDA_TRY(cudaGetLastError());
+    return FPH_OK;
+}
+
+}  // namespace fph

@@ -1,0 +1,49 @@
+// fph_flood.cuh -- flooding kernel interface (see fph_flood.cu).
+#pragma once
+
+#include "fph_common.cuh"
+
+namespace fph {
+
+struct SimplexGeom {
+    double cx, cy, cz;  // Ritter center (float64, reference-exact)
+    double r;           // Ritter radius
+    double rho;         // candidate radius (sqrt(2) r, Lemma 4.2); 0 when unpruned
+    Box box;            // candidate cell box
+    int npc;            // point chunks
+    int nrp;            // row parts (candidate splits)
+};
+
+struct FloodArgs {
+    Grid g;
+    const double* landmarks;  // n_landmarks x 3 (z = 0 for planar clouds)
+    const int* simplices;     // n x 4, vertex ids, unused slots -1
+    int n, k, m, P;
+    int subset;               // landmarks are cloud points: Lemma 4.2 pruning
+    int chunk_pts;            // points per task chunk = 256 * PPT
+    double pairs_per_task;
+    const uchar4* tmpl;       // interior compositions, P rows
+    float* perpoint;          // n x P fp32 minima
+    double* out_sq;           // n squared interior maxima (-1: no interior row)
+};
+
+struct FloodTuning {
+    double pairs_per_task = 0.0;  // <= 0: default 2^21
+};
+
+int choose_ppt(int P);
+
+// Squared flood value over the relative-interior grid rows of every
+// simplex (k = 0: the vertex itself), exactly as the reference computes it.
+int flood_interior(const Grid& g, const double* d_landmarks3, const int* d_simplices, int n,
+                   int k, int m, int subset, double* d_out_sq, const FloodTuning& tune,
+                   cudaStream_t stream);
+
+// out[i] = max(interior[i], lower[facets[i][j]] for j <= k)
+int flood_complete(const double* d_interior, const int* d_facets, int n, int k,
+                   const double* d_lower, double* d_out, cudaStream_t stream);
+
+int fps_run(const double* d_x, const double* d_y, const double* d_z, int n, int k, int start,
+            long long* d_out, cudaStream_t stream);
+
+}  // namespace fph

@@ -1,0 +1,28 @@
+// fph_grid.cuh -- device-resident spatial grid (see fph_grid.cu).
+#pragma once
+
+#include "fph_common.cuh"
+
+namespace fph {
+
+struct GridStore {
+    double* x = nullptr;
+    double* y = nullptr;
+    double* z = nullptr;
+    int* cell_start = nullptr;
+    long long ncells = 0;
+    Grid grid{};
+    void free_all(cudaStream_t stream);
+};
+
+// Default cell edge: about `occupancy` points per cell if the cloud filled
+// its bounding box uniformly.
+double grid_cell_size(const double lo[3], const double hi[3], int dim, long long n,
+                      double occupancy);
+
+// Bin the device cloud d_pts (n x dim float64, row-major) into gs.
+// cell_size <= 0 picks grid_cell_size(..., occupancy).
+int grid_build(const double* d_pts, int n, int dim, double cell_size, double occupancy,
+               cudaStream_t stream, GridStore* gs);
+
+}  // namespace fph

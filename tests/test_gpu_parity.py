@@ -1,0 +1,120 @@
+"""GPU parity: the CUDA path through the C ABI against the reference's golden
+vectors and the CPU oracle.  Integer outputs (landmark indices) must be
+identical; float64 flood values must be bit-identical (tolerance 0, stricter
+than the north star's 1e-5 relative fp32 bar)."""
+
+import numpy as np
+import pytest
+
+import oracle
+from paper_2509_22432_b200 import farthest_point_sampling
+from paper_2509_22432_b200.datagen import gen_sphere_torus_mix, gen_torus
+from paper_2509_22432_b200.delaunay import delaunay
+from paper_2509_22432_b200.filtration import FloodConfig, build_flood_filtration, flood_sq_values
+from tests import _complex as C
+from tests import _golden as G
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("name", G.cases("fps"))
+def test_fps_golden(name):
+    z = G.load("fps", name)
+    got = farthest_point_sampling(z["points"], int(z["k"]), int(z["start"]))
+    np.testing.assert_array_equal(got, z["indices"])
+
+
+@pytest.mark.parametrize("n,dim,k,start", [(200_000, 3, 300, 0), (50_001, 2, 500, 123),
+                                           (1_500_000, 3, 40, 7), (3, 2, 3, 2)])
+def test_fps_matches_oracle(n, dim, k, start):
+    pts = np.random.default_rng(n).random((n, dim))
+    got = farthest_point_sampling(pts, k, start)
+    np.testing.assert_array_equal(got, oracle.fps(pts, k, start))
+
+
+def test_fps_ties_uniform_grid():
+    # a lattice is full of exact ties: lowest index must win every time
+    g = np.stack(np.meshgrid(np.arange(40.0), np.arange(40.0), np.arange(5.0)), -1).reshape(-1, 3)
+    got = farthest_point_sampling(g, 200, 0)
+    np.testing.assert_array_equal(got, oracle.fps(g, 200, 0))
+
+
+@pytest.mark.parametrize("name", G.cases("flood"))
+def test_flood_values_golden(name):
+    z = G.load("flood", name)
+    tri = C.triangulation(z["tri_points"], G.simplices_by_dim(z))
+    subset = str(z["landmark_mode"]) == "subset"
+    sq = flood_sq_values(z["points"], tri, int(z["grid_resolution"]), subset)
+    for k, want in G.values_by_dim(z).items():
+        got = np.sqrt(sq[k])
+        assert np.array_equal(got, want), (k, np.abs(got - want).max())
+
+
+@pytest.mark.parametrize("name", G.cases("flood"))
+def test_build_flood_filtration_golden(name):
+    """End to end through the drop-in API: same complex, same values."""
+    z = G.load("flood", name)
+    m = int(z["grid_resolution"])
+    L = int(z["n_landmarks"]) if "n_landmarks" in z.files else z["landmarks"]
+    fc = build_flood_filtration(z["points"], L, FloodConfig(grid_resolution=m))
+    tri = fc.meta["triangulation"]
+    for k, want in G.values_by_dim(z).items():
+        np.testing.assert_array_equal(tri.simplices_by_dim[k], z[f"simplices_{k}"])
+    vm = fc.value_map()
+    for k, want in G.values_by_dim(z).items():
+        got = np.array([vm[tuple(int(v) for v in r)] for r in z[f"simplices_{k}"]])
+        assert np.array_equal(got, want)
+    if "landmark_indices" in z.files:
+        np.testing.assert_array_equal(fc.meta["landmark_indices"], z["landmark_indices"])
+
+
+@pytest.mark.parametrize("n,nl,m,max_dim", [(100_000, 300, 8, 3), (60_000, 400, 20, 2),
+                                            (30_000, 150, 30, 1)])
+def test_flood_matches_oracle_mid_size(n, nl, m, max_dim):
+    X = gen_sphere_torus_mix(n, seed=n).points
+    idx = farthest_point_sampling(X, nl)
+    tri = delaunay(X[idx])
+    sq = flood_sq_values(X, tri, m, True, max_dim)
+    want = oracle.flood_values(X, tri.points, {k: tri.simplices_by_dim[k] for k in range(max_dim + 1)},
+                               m, top_dim=max_dim)
+    for k in range(max_dim + 1):
+        assert np.array_equal(sq[k], want[k]), k
+
+
+def test_flood_external_landmarks_mid_size():
+    rng = np.random.default_rng(9)
+    X = rng.random((20_000, 3))
+    L = rng.random((60, 3)) * 1.2 - 0.1
+    fc = build_flood_filtration(X, L, FloodConfig(grid_resolution=5))
+    assert fc.meta["landmark_mode"] == "external"
+    tri = fc.meta["triangulation"]
+    want = oracle.flood_values(X, tri.points, tri.simplices_by_dim, 5, subset_mode=False)
+    vm = fc.value_map()
+    for k in range(4):
+        got = np.array([vm[tuple(int(v) for v in r)] for r in tri.simplices_by_dim[k]])
+        assert np.array_equal(got, np.sqrt(want[k]))
+
+
+def test_flood_full_size_properties_and_sampled_oracle():
+    """BASELINE configs[1] size: 1M sphere+torus, 2k landmarks, dims <= 2.
+    Checked: idempotence, monotonicity, vertices 0, and a random sample of
+    triangles (with their edges) against the oracle bit for bit."""
+    X = gen_sphere_torus_mix(1_000_000, seed=0).points
+    idx = farthest_point_sampling(X, 2000)
+    tri = delaunay(X[idx])
+    sq1 = flood_sq_values(X, tri, 20, True, 2)
+    sq2 = flood_sq_values(X, tri, 20, True, 2)
+    for k in range(3):
+        assert np.array_equal(sq1[k], sq2[k])
+        assert np.isfinite(sq1[k]).all() and (sq1[k] >= 0).all()
+    assert (sq1[0] == 0).all()
+    for k in (1, 2):
+        assert (sq1[k - 1][tri.facet_links[k]] <= sq1[k][:, None]).all()
+    rng = np.random.default_rng(0)
+    rows = rng.choice(tri.simplices_by_dim[2].shape[0], 48, replace=False)
+    sub = C.sub_complex(tri.simplices_by_dim, rows, 2)
+    want = oracle.flood_values(X, tri.points, sub, 20, top_dim=2)
+    for k in (1, 2):
+        index = {tuple(r): i for i, r in enumerate(tri.simplices_by_dim[k].tolist())}
+        got = np.array([sq1[k][index[tuple(r)]] for r in sub[k].tolist()])
+        assert np.array_equal(got, want[k]), k
