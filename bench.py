@@ -224,6 +224,9 @@ def run_ours(args):
     if world > 1:
         torch.distributed.barrier()
     lib.fph_launch_count(1)
+    stats = np.zeros(8)
+    lib.fph_set_profiling(1)
+    lib.fph_flood_stats(stats.ctypes.data, 1)
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     with ClockSampler(local) as clocks:
@@ -235,6 +238,8 @@ def run_ours(args):
             ends[i].record()
         torch.cuda.synchronize()
     launches = int(lib.fph_launch_count(0))
+    lib.fph_flood_stats(stats.ctypes.data, 1)
+    lib.fph_set_profiling(0)
     ms = sum(s.elapsed_time(e) for s, e in zip(starts, ends)) / args.steps
     if world > 1:
         import torch.distributed as dist
@@ -273,6 +278,13 @@ def run_ours(args):
         }
         if e2e:
             result["e2e"] = e2e
+        result["roofline"] = roofline(lib, stats, ms, args.steps, clocks.summary())
+        result["work_per_step"] = {"fp32_pairs": stats[0] / args.steps,
+                                   "candidates_staged": stats[1] / args.steps,
+                                   "candidates_scanned": stats[2] / args.steps,
+                                   "refined_points": stats[3] / args.steps,
+                                   "f64_refine_distances": stats[4] / args.steps,
+                                   "tasks": stats[5] / args.steps}
         if world == 1 and not args.no_cpu_baseline:
             result["cpu_baseline"] = cpu_baseline(w, args.cpu_seconds)
     if world > 1:
@@ -281,6 +293,21 @@ def run_ours(args):
         dist.barrier()
         dist.destroy_process_group()
     return result
+
+
+def roofline(lib, stats, step_ms, steps, clocks):
+    """Flooding kernel (pass_kernel): FP32-pipe bound.  Algorithmic work =
+    6 flop (three FMAs of |a|^2 - 2 a.b) per (sample point, candidate) pair
+    actually evaluated, counted on the device; time = CUDA events around
+    every pass_kernel launch on its stream during the timed steps."""
+    pairs, pass_ms = stats[0], stats[6]
+    achieved = 6.0 * pairs / (pass_ms * 1e-3) / 1e12 if pass_ms > 0 else 0.0
+    peak = float(lib.fph_fp32_peak_tflops())
+    return {"bound": "fp32", "kernel": "pass_kernel", "achieved": achieved, "peak": peak,
+            "unit": "TFLOP/s", "frac": achieved / peak if peak else None, "traffic": None,
+            "peak_source": "measured FFMA2 microbenchmark on this GPU (fph_fp32_peak_tflops); "
+                           "MEASURED_PEAKS.json has no FP32 figure",
+            "kernel_ms_per_step": pass_ms / steps, "kernel_share_of_step": pass_ms / steps / step_ms}
 
 
 def e2e_host(lib, native, w, args):
@@ -384,6 +411,21 @@ def run_reference(args):
                     "d2h_bytes_per_step": 0}}
 
 
+def run_profile(args):
+    import torch
+
+    from paper_2509_22432_b200 import _native
+
+    lib = _native.require_gpu()
+    w = prepare(args.config, 0)
+    dc = DeviceComplex(w, 0)
+    stream = torch.cuda.current_stream().cuda_stream
+    for _ in range(2):
+        step_single(lib, _native, w, dc, stream)
+    torch.cuda.synchronize()
+    print("profile run done", dc.counts_full)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -393,9 +435,13 @@ def main():
     ap.add_argument("--config", choices=sorted(CONFIGS), default="sphere_torus_1m")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--profile", action="store_true",
+                    help="minimal run for ncu: setup, 1 warm-up step, 1 step, no e2e/cpu")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if args.profile:
+        return run_profile(args)
     res = run_reference(args) if args.impl == "reference" else run_ours(args)
     if res is not None:
         print(json.dumps(res))

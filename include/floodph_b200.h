@@ -116,6 +116,20 @@ int fph_flood_complete(const double* interior_sq, const int32_t* facets, int64_t
  */
 int fph_set_tuning(double cell_occupancy, double pairs_per_task);
 
+/* Time every flooding-kernel launch with CUDA events (profiling aid). */
+int fph_set_profiling(int32_t on);
+
+/*
+ * Work counters since the last reset: out[0] fp32 (point, candidate) pairs
+ * evaluated, [1] candidates staged, [2] candidates scanned, [3] refined
+ * points, [4] float64 refine distances, [5] tasks, [6] flooding-kernel ms
+ * (with profiling on).  out must hold 8 doubles.
+ */
+int fph_flood_stats(double* out, int32_t reset);
+
+/* Measured FP32 (FFMA2) throughput of the current device, TFLOP/s. */
+double fph_fp32_peak_tflops(void);
+
 /* Kernel launches issued by this thread since the last reset (for bench accounting). */
 int64_t fph_launch_count(int32_t reset);
 

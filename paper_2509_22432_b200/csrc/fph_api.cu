@@ -18,6 +18,7 @@ namespace fph {
 static thread_local char g_err[1024] = "";
 static double g_occupancy = 8.0;
 static double g_pairs_per_task = 0.0;
+static bool g_profile = false;
 static thread_local long long g_launches = 0;
 
 void set_error(const char* fmt, ...) {
@@ -194,6 +195,24 @@ int fph_flood_complete(const double* interior_sq, const int32_t* facets, int64_t
                           static_cast<cudaStream_t>(stream));
 }
 
+int fph_set_profiling(int32_t on) {
+    g_profile = on != 0;
+    return FPH_OK;
+}
+
+int fph_flood_stats(double* out, int32_t reset) {
+    g_err[0] = 0;
+    FPH_TRY(ensure_device());
+    return flood_stats(out, reset);
+}
+
+double fph_fp32_peak_tflops(void) {
+    if (ensure_device() != FPH_OK) return 0.0;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    return ffma2_peak_tflops(dev);
+}
+
 int64_t fph_launch_count(int32_t reset) {
     long long v = g_launches;
     if (reset) g_launches = 0;
@@ -289,6 +308,7 @@ int fph_flood_interior(const double* points, int64_t n_points, int32_t dim,
             if (memory == FPH_MEM_HOST) FPH_TRY(sc.alloc(&d_out, n_simplices));
             FloodTuning tune;
             tune.pairs_per_task = g_pairs_per_task;
+            tune.profile = g_profile;
             rc = flood_interior(gs.grid, lm3, d_s, (int)n_simplices, k, grid_resolution,
                                 subset_mode, d_out, tune, hc.stream);
             count_launches(4);
@@ -333,6 +353,7 @@ int fph_flood_filtration(const double* points, int64_t n_points, int32_t dim,
         count_launches(4);
         FloodTuning tune;
         tune.pairs_per_task = g_pairs_per_task;
+        tune.profile = g_profile;
         double* d_vals[4] = {nullptr, nullptr, nullptr, nullptr};
         for (int k = 0; k <= max_dim && rc == FPH_OK; ++k) {
             const long long nk = counts[k];

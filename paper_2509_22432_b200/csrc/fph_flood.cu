@@ -43,6 +43,11 @@ constexpr int kThreads = 256;
 constexpr int kTile = 2048;           // candidates staged per flush (32 KB)
 constexpr double kU32 = 5.9604644775390625e-08;  // 2^-24
 
+// work counters (profiling aid, read by fph_flood_stats):
+// 0 fp32 pairs evaluated, 1 candidates staged, 2 candidates scanned,
+// 3 refined points, 4 float64 refine distances, 5 tasks
+__device__ unsigned long long g_stats[8];
+
 // ------------------------------------------------------------ block scan
 // exclusive prefix sum over the CTA; returns the total in `total`
 __device__ __forceinline__ int block_excl(int v, int* warp_buf, int& total) {
@@ -262,6 +267,7 @@ __device__ __noinline__ double refine_point(const FloodArgs& a, SmemPass& S, con
     Box b = ball_box(a.g, p[0], p[1], p[2], R);
     int rows = b.rows();
     double best = INFINITY;
+    unsigned long long scanned = 0;
     for (int rb = 0; rb < rows; rb += kThreads) {
         int r = rb + threadIdx.x;
         int2 run = r < rows ? row_run(a.g, b, r, p[0], p[1], p[2], R, true) : make_int2(0, 0);
@@ -271,6 +277,7 @@ __device__ __noinline__ double refine_point(const FloodArgs& a, SmemPass& S, con
         S.row_beg[threadIdx.x] = run.x;
         __syncthreads();
         int nrow = min(kThreads, rows - rb);
+        scanned += total;
         for (int f = threadIdx.x; f < total; f += kThreads) {
             int lo = 0, hi = nrow;  // last row with off <= f
             while (hi - lo > 1) {
@@ -281,6 +288,10 @@ __device__ __noinline__ double refine_point(const FloodArgs& a, SmemPass& S, con
             best = fmin(best, sq64(a.g.x[idx], a.g.y[idx], a.g.z[idx], p[0], p[1], p[2]));
         }
         __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        atomicAdd(&g_stats[3], 1ull);
+        atomicAdd(&g_stats[4], scanned);
     }
     return block_min_d(best, S.dbuf);
 }
@@ -415,6 +426,7 @@ __global__ void __launch_bounds__(kThreads, 2) pass_kernel(FloodArgs a, const Si
         }
         const float thr = a.subset ? (float)(G.rho * G.rho * (1.0 + 1e-5)) : INFINITY;
         int tile_n = 0;
+        unsigned long long n_staged = 0, n_scanned = 0;
         for (int rb = row_lo; rb < row_hi; rb += kThreads) {
             int r = rb + threadIdx.x;
             int2 run = r < row_hi ? row_run(a.g, G.box, r, G.cx, G.cy, G.cz, G.rho, a.subset != 0)
@@ -425,6 +437,7 @@ __global__ void __launch_bounds__(kThreads, 2) pass_kernel(FloodArgs a, const Si
             S.row_beg[threadIdx.x] = run.x;
             __syncthreads();
             const int nrow = min(kThreads, row_hi - rb);
+            n_scanned += total;
             for (int f0 = 0; f0 < total; f0 += kThreads) {
                 int f = f0 + threadIdx.x;
                 bool keep = false;
@@ -454,6 +467,7 @@ __global__ void __launch_bounds__(kThreads, 2) pass_kernel(FloodArgs a, const Si
                     B[2] = aw;
                 }
                 tile_n += kept;
+                n_staged += kept;
                 if (tile_n > kTile - kThreads) {
                     compute_tile<PPT>(S, tile_n, g, Gn, active, bx, by, bz, best);
                     tile_n = 0;
@@ -462,6 +476,12 @@ __global__ void __launch_bounds__(kThreads, 2) pass_kernel(FloodArgs a, const Si
             __syncthreads();
         }
         if (tile_n > 0) compute_tile<PPT>(S, tile_n, g, Gn, active, bx, by, bz, best);
+        if (threadIdx.x == 0) {
+            atomicAdd(&g_stats[0], n_staged * (unsigned long long)Pc);
+            atomicAdd(&g_stats[1], n_staged);
+            atomicAdd(&g_stats[2], n_scanned);
+            atomicAdd(&g_stats[5], 1ull);
+        }
         // reduce the groups' partial minima: red[g][jl], reusing the tile
         float* red = reinterpret_cast<float*>(S.tileA);
         if (active) {
@@ -509,21 +529,57 @@ __global__ void no_interior_kernel(double* out, int n) {
 }  // namespace
 
 int choose_ppt(int P) {
-    // fewest idle threads across {1,2,4,8} points per thread, ties -> larger
+    // Issue-slot model of the inner loop: per candidate pair a thread issues
+    // 2 LDS.128 + PPT x (3 FFMA2 + 1 FMNMX3); the G = kThreads / Q groups of
+    // a task (Q = ceil(pc / PPT) threads each) split the tile.  Minimise the
+    // summed per-pair cost over all point chunks.  Groups narrower than 4
+    // threads would scatter a warp's tile reads over too many addresses.
     int best = 1;
-    long long best_idle = 1ll << 60;
+    double best_cost = 1e300;
     for (int ppt : {1, 2, 4, 8}) {
-        int pc = P < kThreads * ppt ? P : kThreads * ppt;
-        int Q = (pc + ppt - 1) / ppt;
-        if (Q > kThreads || Q < 1) continue;
-        int G = kThreads / Q;
-        long long idle = (long long)kThreads * ppt - (long long)G * pc;
-        if (idle <= best_idle) {
-            best_idle = idle;
+        const int chunk = kThreads * ppt;
+        double cost = 0.0;
+        bool ok = true;
+        for (int base = 0; base < P; base += chunk) {
+            int pc = P - base < chunk ? P - base : chunk;
+            int Q = (pc + ppt - 1) / ppt;
+            if (Q < 4 && ppt > 1) ok = false;
+            cost += (2.0 + 4.0 * ppt) / (kThreads / Q);
+        }
+        if (ok && cost < best_cost - 1e-12) {
+            best_cost = cost;
             best = ppt;
         }
     }
     return best;
+}
+
+// ---------------------------------------------------------- profiling
+static std::vector<std::pair<cudaEvent_t, cudaEvent_t>> g_pass_events;
+static double g_pass_ms = 0.0;
+
+void profile_push(cudaEvent_t a, cudaEvent_t b) { g_pass_events.emplace_back(a, b); }
+
+int flood_stats(double* out, int reset) {
+    for (auto& e : g_pass_events) {
+        FPH_CUDA_TRY(cudaEventSynchronize(e.second));
+        float ms = 0.f;
+        FPH_CUDA_TRY(cudaEventElapsedTime(&ms, e.first, e.second));
+        g_pass_ms += ms;
+        cudaEventDestroy(e.first);
+        cudaEventDestroy(e.second);
+    }
+    g_pass_events.clear();
+    unsigned long long h[8];
+    FPH_CUDA_TRY(cudaMemcpyFromSymbol(h, g_stats, sizeof(h)));
+    for (int i = 0; i < 8; ++i) out[i] = (double)h[i];
+    out[6] = g_pass_ms;
+    if (reset) {
+        unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        FPH_CUDA_TRY(cudaMemcpyToSymbol(g_stats, z, sizeof(z)));
+        g_pass_ms = 0.0;
+    }
+    return FPH_OK;
 }
 
 int flood_interior(const Grid& g, const double* d_landmarks3, const int* d_simplices, int n,
@@ -603,6 +659,12 @@ int flood_interior(const Grid& g, const double* d_landmarks3, const int* d_simpl
     FPH_CUDA_TRY(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, d_ntasks, d_task_off, n + 1, stream));
 
     int dev = 0, sms = 0, occ = 0;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    if (tune.profile) {
+        FPH_CUDA_TRY(cudaEventCreate(&ev0));
+        FPH_CUDA_TRY(cudaEventCreate(&ev1));
+        FPH_CUDA_TRY(cudaEventRecord(ev0, stream));
+    }
     FPH_CUDA_TRY(cudaGetDevice(&dev));
     FPH_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     switch (ppt) {
@@ -620,6 +682,10 @@ int flood_interior(const Grid& g, const double* d_landmarks3, const int* d_simpl
 #undef FPH_LAUNCH
     }
     FPH_CUDA_TRY(cudaGetLastError());
+    if (tune.profile) {
+        FPH_CUDA_TRY(cudaEventRecord(ev1, stream));
+        profile_push(ev0, ev1);
+    }
     for (void* p : {(void*)d_tmpl, (void*)d_geom, (void*)d_ntasks, (void*)d_task_off,
                     (void*)d_counter, (void*)d_done, (void*)d_perpoint, tmp})
         FPH_CUDA_TRY(cudaFreeAsync(p, stream));

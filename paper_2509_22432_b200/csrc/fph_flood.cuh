@@ -29,7 +29,13 @@ struct FloodArgs {
 
 struct FloodTuning {
     double pairs_per_task = 0.0;  // <= 0: default 2^21
+    bool profile = false;         // time pass kernels with events
 };
+
+// out[0..5]: work counters (see g_stats), out[6]: pass-kernel ms
+int flood_stats(double* out, int reset);
+void profile_push(cudaEvent_t a, cudaEvent_t b);
+double ffma2_peak_tflops(int device);
 
 int choose_ppt(int P);
 

@@ -12,12 +12,12 @@
 // coordinates live in shared memory (SoA) and the running minimum in
 // registers for the whole run -- a 1M-point cloud never touches HBM after
 // the first load.  Larger clouds stream coordinates and the running minimum
-// through L2/HBM.  Per iteration each CTA publishes (value, index, tag) to a
-// double-buffered slot array; every CTA polls the tags of the current
-// iteration, and all CTAs reduce the same slots in the same order, so they
-// agree on the next landmark without a separate broadcast.
-#include <cooperative_groups.h>
-
+// through L2/HBM.  Per iteration each CTA publishes its (value, index) to a
+// double-buffered slot array and bumps one monotone arrival counter; one
+// thread per CTA polls the counter (ld.acquire) until all CTAs of this
+// iteration arrived, then the CTA reads every slot in one coalesced pass.
+// All CTAs reduce the same slots in the same order, so they agree on the
+// next landmark without a second broadcast.
 #include "fph_common.cuh"
 
 namespace fph {
@@ -30,8 +30,14 @@ constexpr int kFpsMaxPT = 9;  // points per thread in the shared-memory variant
 struct __align__(16) Slot {
     double val;
     int idx;
-    int tag;
+    int pad;
 };
+
+__device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
 
 __device__ __forceinline__ void better(double& bv, int& bi, double v, int i) {
     if (v > bv || (v == bv && i < bi)) {
@@ -78,7 +84,8 @@ template <bool kSmem>
 __global__ void __launch_bounds__(kFpsThreads, 1)
     fps_kernel(const double* __restrict__ px, const double* __restrict__ py,
                const double* __restrict__ pz, int n, int k, int start, int chunk,
-               double* __restrict__ mind, Slot* slots, long long* __restrict__ out) {
+               double* __restrict__ mind, Slot* slots, unsigned long long* arrived,
+               long long* __restrict__ out) {
     extern __shared__ double sm[];
     __shared__ double red_v[32];
     __shared__ int red_i[32];
@@ -133,22 +140,22 @@ __global__ void __launch_bounds__(kFpsThreads, 1)
         block_argmax(bv, bi, red_v, red_i);
         Slot* buf = slots + (it & 1) * G;
         if (threadIdx.x == 0) {
-            volatile Slot* s = buf + blockIdx.x;
-            s->val = bv;
-            s->idx = bi;
+            buf[blockIdx.x].val = bv;
+            buf[blockIdx.x].idx = bi;
             __threadfence();
-            atomicExch((int*)&buf[blockIdx.x].tag, it);
+            atomicAdd(arrived, 1ull);
+            const unsigned long long target = (unsigned long long)G * it;
+            while (ld_acquire(arrived) < target) {
+            }
         }
-        // gather every CTA's candidate for this iteration
+        __syncthreads();
+        // every CTA has published this iteration's candidate
         double v = -INFINITY;
         int i = 0x7fffffff;
         for (int b = threadIdx.x; b < G; b += blockDim.x) {
-            volatile int* tag = &buf[b].tag;
-            while (*tag != it) {
-            }
-            __threadfence();
-            volatile Slot* s = buf + b;
-            better(v, i, s->val, s->idx);
+            double sv = __ldcg(&buf[b].val);
+            int si = __ldcg(&buf[b].idx);
+            better(v, i, sv, si);
         }
         block_argmax(v, i, red_v, red_i);
         cur = i;
@@ -182,11 +189,14 @@ int fps_run(const double* d_x, const double* d_y, const double* d_z, int n, int 
     }
     Slot* slots = nullptr;
     double* mind = nullptr;
+    unsigned long long* arrived = nullptr;
     FPH_CUDA_TRY(cudaMallocAsync(&slots, sizeof(Slot) * 2 * G, stream));
-    FPH_CUDA_TRY(cudaMemsetAsync(slots, 0xff, sizeof(Slot) * 2 * G, stream));
+    FPH_CUDA_TRY(cudaMallocAsync(&arrived, sizeof(unsigned long long), stream));
+    FPH_CUDA_TRY(cudaMemsetAsync(arrived, 0, sizeof(unsigned long long), stream));
     if (!use_smem) FPH_CUDA_TRY(cudaMallocAsync(&mind, sizeof(double) * n, stream));
-    void* args[] = {(void*)&d_x, (void*)&d_y, (void*)&d_z, (void*)&n,     (void*)&k,
-                    (void*)&start, (void*)&chunk, (void*)&mind, (void*)&slots, (void*)&d_out};
+    void* args[] = {(void*)&d_x,   (void*)&d_y,  (void*)&d_z,   (void*)&n,
+                    (void*)&k,     (void*)&start, (void*)&chunk, (void*)&mind,
+                    (void*)&slots, (void*)&arrived, (void*)&d_out};
     if (use_smem) {
         FPH_CUDA_TRY(cudaFuncSetAttribute(fps_kernel<true>,
                                           cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -199,6 +209,7 @@ int fps_run(const double* d_x, const double* d_y, const double* d_z, int n, int 
     }
     FPH_CUDA_TRY(cudaGetLastError());
     FPH_CUDA_TRY(cudaFreeAsync(slots, stream));
+    FPH_CUDA_TRY(cudaFreeAsync(arrived, stream));
     if (mind) FPH_CUDA_TRY(cudaFreeAsync(mind, stream));
     return FPH_OK;
 }

@@ -14,7 +14,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 def _declared():
     with open(os.path.join(ROOT, "include", "floodph_b200.h")) as fh:
         text = fh.read()
-    return sorted(set(re.findall(r"\b(fph_[a-z_]+)\s*\(", text)))
+    return sorted(set(re.findall(r"\b(fph_[a-z_0-9]+)\s*\(", text)))
 
 
 def test_library_builds_and_loads():

@@ -1,0 +1,81 @@
+"""Multi-rank host logic of the sharded flood filtration, world size 2, gloo
+on CPU.  Interior values come from the CPU oracle (test infrastructure);
+the code under test is the sharding, the all-gather back into row order and
+the facet completion identity used by bench.py / parallel.py."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2509_22432_b200.parallel import gather_interleaved, shard_clouds, shard_rows
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def test_shard_rows_partition():
+    for n in (0, 1, 7, 100):
+        for world in (1, 2, 3, 8):
+            parts = [shard_rows(n, world, r) for r in range(world)]
+            allrows = np.sort(np.concatenate(parts))
+            np.testing.assert_array_equal(allrows, np.arange(n))
+    with pytest.raises(ValueError):
+        shard_rows(4, 2, 2)
+    np.testing.assert_array_equal(shard_clouds(5, 2, 1), [1, 3])
+
+
+def _worker(rank, world, port, payload, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        interior = payload["interior"]
+        facets = payload["facets"]
+        values = {0: np.zeros(payload["n0"])}
+        for k in sorted(interior):
+            full = interior[k]
+            mine = torch.from_numpy(full[shard_rows(full.shape[0], world, rank)])
+            got = gather_interleaved(mine, full.shape[0], world, dist).numpy()
+            assert np.array_equal(got, full)
+            values[k] = np.maximum(got, values[k - 1][facets[k]].max(axis=1))
+        q.put((rank, {k: v.tolist() for k, v in values.items()}))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_sharded_gather_and_completion_world2():
+    import oracle
+    from tests import _complex as C
+    from tests import _golden as G
+
+    z = G.load("flood", "rand3d_m4")
+    by_dim = G.simplices_by_dim(z)
+    tri = C.triangulation(z["tri_points"], by_dim)
+    m = int(z["grid_resolution"])
+    # full values are valid "interior" inputs: completion is idempotent on
+    # a monotone complex (max(f(s), f(facets)) == f(s))
+    full = oracle.flood_values(z["points"], z["tri_points"], by_dim, m)
+    interior = {k: full[k] for k in range(1, 4)}
+    payload = {"interior": interior, "facets": tri.facet_links, "n0": by_dim[0].shape[0]}
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, payload, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    results = dict(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for r in range(2):
+        for k in range(1, 4):
+            assert np.array_equal(np.asarray(results[r][k]), full[k])
+            assert np.array_equal(np.sqrt(np.asarray(results[r][k])), z[f"values_{k}"])
