@@ -224,7 +224,7 @@ def run_ours(args):
     if world > 1:
         torch.distributed.barrier()
     lib.fph_launch_count(1)
-    stats = np.zeros(8)
+    stats = np.zeros(24)
     lib.fph_set_profiling(1)
     lib.fph_flood_stats(stats.ctypes.data, 1)
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
@@ -284,7 +284,11 @@ def run_ours(args):
                                    "candidates_scanned": stats[2] / args.steps,
                                    "refined_points": stats[3] / args.steps,
                                    "f64_refine_distances": stats[4] / args.steps,
-                                   "tasks": stats[5] / args.steps}
+                                   "tasks": stats[5] / args.steps,
+                                   "search": {name: stats[i] / args.steps for i, name in enumerate(
+                                       ["blocks", "blocks_pruned", "r1_certified", "need_after_r1",
+                                        "reps_passes", "r2_passes", "scanned_r1", "scanned_reps",
+                                        "scanned_r2", "staged_r1", "staged_reps", "staged_r2"], start=7)}}
         if world == 1 and not args.no_cpu_baseline:
             result["cpu_baseline"] = cpu_baseline(w, args.cpu_seconds)
     if world > 1:

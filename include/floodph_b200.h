@@ -116,6 +116,17 @@ int fph_flood_complete(const double* interior_sq, const int32_t* facets, int64_t
  */
 int fph_set_tuning(double cell_occupancy, double pairs_per_task);
 
+/*
+ * Flooding algorithm: 1 (default) bounded search -- per simplex, sampled
+ * upper bounds, an exact lower bound, and exact search of only the point
+ * blocks that can still hold the maximum; 0 brute force over every point of
+ * the Lemma-4.2 ball.  Both are exact (identical values).
+ * reps_target: candidates per representative (sampling) pass;
+ * team_threshold: simplices with more candidates are searched by a whole
+ * CTA instead of one warp.  <= 0 keeps the defaults (1024, 32768).
+ */
+int fph_set_search(int32_t algo, int32_t reps_target, int32_t team_threshold);
+
 /* Time every flooding-kernel launch with CUDA events (profiling aid). */
 int fph_set_profiling(int32_t on);
 
@@ -123,7 +134,11 @@ int fph_set_profiling(int32_t on);
  * Work counters since the last reset: out[0] fp32 (point, candidate) pairs
  * evaluated, [1] candidates staged, [2] candidates scanned, [3] refined
  * points, [4] float64 refine distances, [5] tasks, [6] flooding-kernel ms
- * (with profiling on).  out must hold 8 doubles.
+ * (with profiling on); block search: [7] blocks, [8] blocks pruned whole,
+ * [9] points certified in round 1, [10] points still needed after round 1,
+ * [11] representative passes, [12] round-2 passes, [13..15] candidates
+ * scanned in round 1 / representative / round 2, [16..18] staged likewise.
+ * out must hold 24 doubles.
  */
 int fph_flood_stats(double* out, int32_t reset);
 

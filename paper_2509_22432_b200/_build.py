@@ -14,8 +14,9 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB_DIR = os.path.join(HERE, "_lib")
 LIB_PATH = os.path.join(LIB_DIR, "libfloodph_b200.so")
-SOURCES = ["fph_api.cu", "fph_flood.cu", "fph_fps.cu", "fph_grid.cu", "fph_diag.cu"]
-HEADERS = ["fph_common.cuh", "fph_flood.cuh", "fph_grid.cuh"]
+SOURCES = ["fph_api.cu", "fph_flood.cu", "fph_search.cu", "fph_fps.cu", "fph_grid.cu",
+           "fph_diag.cu"]
+HEADERS = ["fph_common.cuh", "fph_dev.cuh", "fph_flood.cuh", "fph_grid.cuh"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

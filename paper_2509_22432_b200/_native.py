@@ -47,6 +47,7 @@ SIGNATURES = {
     "fph_flood_complete": (ctypes.c_int, [_vp, _vp, ctypes.c_int64, ctypes.c_int32, _vp, _vp,
                                           _vp]),
     "fph_set_tuning": (ctypes.c_int, [ctypes.c_double, ctypes.c_double]),
+    "fph_set_search": (ctypes.c_int, [ctypes.c_int32, ctypes.c_int32, ctypes.c_int32]),
     "fph_set_profiling": (ctypes.c_int, [ctypes.c_int32]),
     "fph_flood_stats": (ctypes.c_int, [_vp, ctypes.c_int32]),
     "fph_fp32_peak_tflops": (ctypes.c_double, []),

@@ -19,6 +19,10 @@ static thread_local char g_err[1024] = "";
 static double g_occupancy = 8.0;
 static double g_pairs_per_task = 0.0;
 static bool g_profile = false;
+static int g_algo = 1;
+static double g_probe_cells = 1.0;
+static int g_reps_target = 1024;
+static int g_team_threshold = 32768;
 static thread_local long long g_launches = 0;
 
 void set_error(const char* fmt, ...) {
@@ -195,6 +199,17 @@ int fph_flood_complete(const double* interior_sq, const int32_t* facets, int64_t
                           static_cast<cudaStream_t>(stream));
 }
 
+int fph_set_search(int32_t algo, int32_t reps_target, int32_t team_threshold) {
+    if (algo != 0 && algo != 1) {
+        set_error("algo must be 0 (brute force) or 1 (bounded search)");
+        return FPH_EARG;
+    }
+    g_algo = algo;
+    g_reps_target = reps_target > 0 ? reps_target : 1024;
+    g_team_threshold = team_threshold > 0 ? team_threshold : 32768;
+    return FPH_OK;
+}
+
 int fph_set_profiling(int32_t on) {
     g_profile = on != 0;
     return FPH_OK;
@@ -309,6 +324,10 @@ int fph_flood_interior(const double* points, int64_t n_points, int32_t dim,
             FloodTuning tune;
             tune.pairs_per_task = g_pairs_per_task;
             tune.profile = g_profile;
+            tune.algo = g_algo;
+            tune.probe_cells = g_probe_cells;
+            tune.reps_target = g_reps_target;
+            tune.team_threshold = g_team_threshold;
             rc = flood_interior(gs.grid, lm3, d_s, (int)n_simplices, k, grid_resolution,
                                 subset_mode, d_out, tune, hc.stream);
             count_launches(4);
@@ -354,6 +373,10 @@ int fph_flood_filtration(const double* points, int64_t n_points, int32_t dim,
         FloodTuning tune;
         tune.pairs_per_task = g_pairs_per_task;
         tune.profile = g_profile;
+        tune.algo = g_algo;
+        tune.probe_cells = g_probe_cells;
+        tune.reps_target = g_reps_target;
+        tune.team_threshold = g_team_threshold;
         double* d_vals[4] = {nullptr, nullptr, nullptr, nullptr};
         for (int k = 0; k <= max_dim && rc == FPH_OK; ++k) {
             const long long nk = counts[k];

@@ -31,8 +31,10 @@
 
 #include <cfloat>
 #include <cmath>
+#include <algorithm>
 #include <vector>
 
+#include "fph_dev.cuh"
 #include "fph_flood.cuh"
 
 namespace fph {
@@ -41,12 +43,16 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kTile = 2048;           // candidates staged per flush (32 KB)
-constexpr double kU32 = 5.9604644775390625e-08;  // 2^-24
 
 // work counters (profiling aid, read by fph_flood_stats):
 // 0 fp32 pairs evaluated, 1 candidates staged, 2 candidates scanned,
 // 3 refined points, 4 float64 refine distances, 5 tasks
-__device__ unsigned long long g_stats[8];
+// block search: 7 blocks, 8 blocks pruned whole, 9 points certified in
+// round 1, 10 points needing more after round 1, 11 representative passes,
+// 12 round-2 passes, 13/14/15 candidates scanned in round 1 / reps (incl.
+// counting) / round 2, 16/17/18 staged in round 1 / reps / round 2
+constexpr int kStats = 24;
+__device__ unsigned long long g_stats[kStats];
 
 // ------------------------------------------------------------ block scan
 // exclusive prefix sum over the CTA; returns the total in `total`
@@ -101,77 +107,6 @@ __device__ __forceinline__ double block_min_d(double v, double* buf) {
     return r;
 }
 
-// ----------------------------------------------------- simplex geometry
-struct Verts {
-    double v[4][3];
-};
-
-__device__ __forceinline__ void load_verts(const FloodArgs& a, int s, Verts& V) {
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-        int id = j <= a.k ? a.simplices[(size_t)s * 4 + j] : -1;
-        V.v[j][0] = id >= 0 ? a.landmarks[(size_t)id * 3 + 0] : 0.0;
-        V.v[j][1] = id >= 0 ? a.landmarks[(size_t)id * 3 + 1] : 0.0;
-        V.v[j][2] = id >= 0 ? a.landmarks[(size_t)id * 3 + 2] : 0.0;
-    }
-}
-
-// Reference barycentric row: p = w0*v0; p = p + wj*vj (w = c/m), no FMA
-// (floodph/geometry.py barycentric_grid + barycentric_grid_template).
-__device__ __forceinline__ void embed_row(const Verts& V, int k, uchar4 c, double m,
-                                          double p[3]) {
-    const unsigned char cc[4] = {c.x, c.y, c.z, c.w};
-#pragma unroll
-    for (int a = 0; a < 3; ++a) {
-        double w = __ddiv_rn((double)cc[0], m);
-        double acc = __dmul_rn(w, V.v[0][a]);
-#pragma unroll
-        for (int j = 1; j < 4; ++j) {
-            if (j <= k) {
-                double wj = __ddiv_rn((double)cc[j], m);
-                acc = __dadd_rn(acc, __dmul_rn(wj, V.v[j][a]));
-            }
-        }
-        p[a] = acc;
-    }
-}
-
-// Ritter ball exactly as reference floodph/geometry.py:123 (first longest
-// edge in combinations order, center its midpoint, radius the farthest
-// vertex).  Only used to bound candidate sets, kept exact anyway.
-__device__ __forceinline__ double ritter(const Verts& V, int k, double c[3]) {
-    if (k == 0) {
-        c[0] = V.v[0][0];
-        c[1] = V.v[0][1];
-        c[2] = V.v[0][2];
-        return 0.0;
-    }
-    double best = -1.0;
-    double c0 = 0, c1 = 0, c2 = 0;
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = i + 1; j < 4; ++j) {
-            if (j <= k) {
-                double d = sq64(V.v[i][0], V.v[i][1], V.v[i][2], V.v[j][0], V.v[j][1], V.v[j][2]);
-                if (d > best) {
-                    best = d;
-                    c0 = __dmul_rn(0.5, __dadd_rn(V.v[i][0], V.v[j][0]));
-                    c1 = __dmul_rn(0.5, __dadd_rn(V.v[i][1], V.v[j][1]));
-                    c2 = __dmul_rn(0.5, __dadd_rn(V.v[i][2], V.v[j][2]));
-                }
-            }
-        }
-    c[0] = c0;
-    c[1] = c1;
-    c[2] = c2;
-    double mx = -1.0;
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-        if (i <= k) mx = fmax(mx, sq64(V.v[i][0], V.v[i][1], V.v[i][2], c0, c1, c2));
-    return sqrt(mx);
-}
-
 // ------------------------------------------------------------ setup
 // One warp per simplex: Ritter ball, candidate cell box, candidate count,
 // and the number of tasks the simplex is split into.
@@ -209,6 +144,7 @@ __global__ void setup_kernel(FloodArgs a, SimplexGeom* __restrict__ geom,
     if (lane == 0) {
         geom[warp] = G;
         ntasks[warp] = a.P > 0 ? npc * nrp : 0;
+        if (a.cand_count) a.cand_count[warp] = (int)min(cand, (long long)0x7fffffff);
     }
 }
 
@@ -516,6 +452,7 @@ __global__ void __launch_bounds__(kThreads, 2) pass_kernel(FloodArgs a, const Si
     }
 }
 
+
 __global__ void init_perpoint_kernel(unsigned* p, long long n) {
     long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     if (i < n) p[i] = 0xffffffffu;
@@ -570,12 +507,12 @@ int flood_stats(double* out, int reset) {
         cudaEventDestroy(e.second);
     }
     g_pass_events.clear();
-    unsigned long long h[8];
+    unsigned long long h[kStats];
     FPH_CUDA_TRY(cudaMemcpyFromSymbol(h, g_stats, sizeof(h)));
-    for (int i = 0; i < 8; ++i) out[i] = (double)h[i];
+    for (int i = 0; i < kStats; ++i) out[i] = (double)h[i];
     out[6] = g_pass_ms;
     if (reset) {
-        unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        unsigned long long z[kStats] = {};
         FPH_CUDA_TRY(cudaMemcpyToSymbol(g_stats, z, sizeof(z)));
         g_pass_ms = 0.0;
     }
@@ -590,25 +527,64 @@ int flood_interior(const Grid& g, const double* d_landmarks3, const int* d_simpl
         set_error("flood_interior: need 0 <= k <= 3 and 1 <= m <= 255");
         return FPH_EARG;
     }
-    // interior compositions of m into k+1 positive parts (k = 0: the vertex)
-    std::vector<uchar4> tmpl;
+    // interior compositions of m into k+1 positive parts (k = 0: the vertex),
+    // grouped into lattice tiles of <= 32 rows (t^k rows, t = 32, 5, 3 for
+    // k = 1, 2, 3) and ordered center-first: blocks near the barycenter tend
+    // to hold the maximum, which raises the shared lower bound early.
+    std::vector<uchar4> rows;
     if (k == 0) {
-        tmpl.push_back(make_uchar4((unsigned char)m, 0, 0, 0));
+        rows.push_back(make_uchar4((unsigned char)m, 0, 0, 0));
+    } else if (k == 1) {
+        for (int c0 = 1; c0 <= m - 1; ++c0) rows.push_back(make_uchar4(c0, m - c0, 0, 0));
+    } else if (k == 2) {
+        for (int c0 = 1; c0 <= m - 2; ++c0)
+            for (int c1 = 1; c1 <= m - 1 - c0; ++c1)
+                rows.push_back(make_uchar4(c0, c1, m - c0 - c1, 0));
     } else {
-        int c[4] = {0, 0, 0, 0};
-        if (k == 1) {
-            for (c[0] = 1; c[0] <= m - 1; ++c[0]) tmpl.push_back(make_uchar4(c[0], m - c[0], 0, 0));
-        } else if (k == 2) {
-            for (c[0] = 1; c[0] <= m - 2; ++c[0])
-                for (c[1] = 1; c[1] <= m - 1 - c[0]; ++c[1])
-                    tmpl.push_back(make_uchar4(c[0], c[1], m - c[0] - c[1], 0));
-        } else {
-            for (c[0] = 1; c[0] <= m - 3; ++c[0])
-                for (c[1] = 1; c[1] <= m - 2 - c[0]; ++c[1])
-                    for (c[2] = 1; c[2] <= m - 1 - c[0] - c[1]; ++c[2])
-                        tmpl.push_back(make_uchar4(c[0], c[1], c[2], m - c[0] - c[1] - c[2]));
-        }
+        for (int c0 = 1; c0 <= m - 3; ++c0)
+            for (int c1 = 1; c1 <= m - 2 - c0; ++c1)
+                for (int c2 = 1; c2 <= m - 1 - c0 - c1; ++c2)
+                    rows.push_back(make_uchar4(c0, c1, c2, m - c0 - c1 - c2));
     }
+    const int tile = k <= 1 ? 32 : (k == 2 ? 5 : 3);
+    std::vector<std::pair<long long, int>> keyed;  // (tile key, row)
+    for (int i = 0; i < (int)rows.size(); ++i) {
+        const uchar4 c = rows[i];
+        long long key = k <= 1 ? (c.x - 1) / tile
+                               : ((long long)(c.x / tile) * 256 + c.y / tile) * 256 +
+                                     (k == 3 ? c.z / tile : 0);
+        keyed.emplace_back(key, i);
+    }
+    std::stable_sort(keyed.begin(), keyed.end(),
+                     [](const std::pair<long long, int>& x, const std::pair<long long, int>& y) {
+                         return x.first < y.first;
+                     });
+    struct Blk { double dist; int beg, end; };
+    std::vector<Blk> blks;
+    for (int i = 0; i < (int)keyed.size();) {
+        int j = i;
+        double mc[4] = {0, 0, 0, 0};
+        while (j < (int)keyed.size() && keyed[j].first == keyed[i].first) {
+            const uchar4 c = rows[keyed[j].second];
+            mc[0] += c.x; mc[1] += c.y; mc[2] += c.z; mc[3] += c.w;
+            ++j;
+        }
+        double d = 0.0;
+        for (int t = 0; t <= k; ++t) {
+            double e = mc[t] / (j - i) / m - 1.0 / (k + 1);
+            d += e * e;
+        }
+        blks.push_back({d, i, j});
+        i = j;
+    }
+    std::stable_sort(blks.begin(), blks.end(), [](const Blk& x, const Blk& y) { return x.dist < y.dist; });
+    std::vector<uchar4> tmpl;
+    std::vector<int> blk_off;
+    for (const Blk& b : blks) {
+        blk_off.push_back((int)tmpl.size());
+        for (int i = b.beg; i < b.end; ++i) tmpl.push_back(rows[keyed[i].second]);
+    }
+    blk_off.push_back((int)tmpl.size());
     const int P = (int)tmpl.size();
     if (P == 0) {
         no_interior_kernel<<<(n + 255) / 256, 256, 0, stream>>>(d_out_sq, n);
@@ -628,6 +604,12 @@ int flood_interior(const Grid& g, const double* d_landmarks3, const int* d_simpl
     a.chunk_pts = kThreads * ppt;
     a.pairs_per_task = tune.pairs_per_task > 0 ? tune.pairs_per_task : (double)(1 << 21);
     a.out_sq = d_out_sq;
+    const bool search = tune.algo == 1;
+    a.nblk = search ? (int)blk_off.size() - 1 : 0;
+    a.probe = tune.probe_cells * g.h;
+    a.reps_target = tune.reps_target > 0 ? tune.reps_target : 384;
+    a.team_threshold = tune.team_threshold > 0 ? tune.team_threshold : 32768;
+    int* d_blk = nullptr;
 
     uchar4* d_tmpl = nullptr;
     SimplexGeom* d_geom = nullptr;
@@ -646,10 +628,19 @@ int flood_interior(const Grid& g, const double* d_landmarks3, const int* d_simpl
     FPH_CUDA_TRY(cudaMemsetAsync(d_done, 0, sizeof(int) * n, stream));
     FPH_CUDA_TRY(cudaMemsetAsync(d_ntasks + n, 0, sizeof(int), stream));
     long long npp = (long long)n * P;
-    init_perpoint_kernel<<<(unsigned)((npp + 255) / 256), 256, 0, stream>>>(
-        reinterpret_cast<unsigned*>(d_perpoint), npp);
+    if (!search)
+        init_perpoint_kernel<<<(unsigned)((npp + 255) / 256), 256, 0, stream>>>(
+            reinterpret_cast<unsigned*>(d_perpoint), npp);
+    FPH_CUDA_TRY(cudaMallocAsync(&d_blk, sizeof(int) * blk_off.size(), stream));
+    int* d_cand = nullptr;
+    if (search) FPH_CUDA_TRY(cudaMallocAsync(&d_cand, sizeof(int) * n, stream));
+    a.cand_count = d_cand;
+    FPH_CUDA_TRY(cudaGetSymbolAddress((void**)&a.stats, g_stats));
+    FPH_CUDA_TRY(cudaMemcpyAsync(d_blk, blk_off.data(), sizeof(int) * blk_off.size(),
+                                 cudaMemcpyHostToDevice, stream));
     a.tmpl = d_tmpl;
     a.perpoint = d_perpoint;
+    a.blk_off = d_blk;
 
     setup_kernel<<<(n * 32 + 255) / 256, 256, 0, stream>>>(a, d_geom, d_ntasks);
     size_t tmp_bytes = 0;
@@ -667,7 +658,9 @@ int flood_interior(const Grid& g, const double* d_landmarks3, const int* d_simpl
     }
     FPH_CUDA_TRY(cudaGetDevice(&dev));
     FPH_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    switch (ppt) {
+    if (search) {
+        FPH_TRY(launch_search(a, d_geom, a.cand_count, stream));
+    } else switch (ppt) {
 #define FPH_LAUNCH(PPTV)                                                                     \
     case PPTV:                                                                               \
         FPH_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pass_kernel<PPTV>,  \
@@ -687,8 +680,9 @@ int flood_interior(const Grid& g, const double* d_landmarks3, const int* d_simpl
         profile_push(ev0, ev1);
     }
     for (void* p : {(void*)d_tmpl, (void*)d_geom, (void*)d_ntasks, (void*)d_task_off,
-                    (void*)d_counter, (void*)d_done, (void*)d_perpoint, tmp})
+                    (void*)d_counter, (void*)d_done, (void*)d_perpoint, tmp, (void*)d_blk})
         FPH_CUDA_TRY(cudaFreeAsync(p, stream));
+    if (d_cand) FPH_CUDA_TRY(cudaFreeAsync(d_cand, stream));
     return FPH_OK;
 }
 

@@ -22,14 +22,30 @@ struct FloodArgs {
     int subset;               // landmarks are cloud points: Lemma 4.2 pruning
     int chunk_pts;            // points per task chunk = 256 * PPT
     double pairs_per_task;
-    const uchar4* tmpl;       // interior compositions, P rows
+    const uchar4* tmpl;       // interior compositions, P rows (block-ordered)
     float* perpoint;          // n x P fp32 minima
     double* out_sq;           // n squared interior maxima (-1: no interior row)
+    // block search (algo 1): point blocks of <= 32 rows, probe radius, reps
+    const int* blk_off;       // nblk + 1 offsets into tmpl
+    int nblk;
+    double probe;             // first-round margin around a block (absolute)
+    int reps_target;          // candidates per representative pass
+    int* cand_count;          // per simplex: candidates in the Lemma-4.2 ball rows
+    unsigned long long* stats;  // work counters (fph_flood_stats)
+    int team_threshold;       // candidates above which a whole CTA takes the simplex
 };
+
+// algorithm 1 (fph_search.cu): warp-per-simplex bounded search
+int launch_search(const FloodArgs& a, const SimplexGeom* d_geom, const int* d_cand,
+                  cudaStream_t stream);
 
 struct FloodTuning {
     double pairs_per_task = 0.0;  // <= 0: default 2^21
     bool profile = false;         // time pass kernels with events
+    int algo = 1;                 // 0: brute force over the Lemma-4.2 ball, 1: block search
+    double probe_cells = 1.0;     // block search: first-round margin in grid cells
+    int reps_target = 384;        // block search: candidates per representative pass
+    int team_threshold = 32768;   // block search: CTA-cooperative simplices above this
 };
 
 // out[0..5]: work counters (see g_stats), out[6]: pass-kernel ms

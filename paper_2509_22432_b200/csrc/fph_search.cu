@@ -1,0 +1,745 @@
+// fph_search.cu -- flooding kernel, algorithm 1 (default): one warp per
+// simplex, exact max of nearest-neighbour distances by bounded search.
+//
+// The brute-force pass (fph_flood.cu, algorithm 0) evaluates every sample
+// point against every cloud point of the simplex's Lemma-4.2 ball.  Most of
+// that work cannot change the result: f(sigma) is a MAX over sample points,
+// and each point's minimum only needs the cloud points near it.  Per
+// simplex, one warp runs (all steps exact; no CTA barriers, so warps never
+// wait for each other):
+//
+//  A  representatives: a stride-s sample (~reps_target points) of the
+//     candidate set, against every sample point -> an upper bound
+//     U(p) >= nn^2(p) (+ the nearest-vertex bound: vertices are cloud
+//     points).  With s = 1 this IS the brute-force pass: done.
+//  B  the point with the largest U is searched exactly over the ball of
+//     radius sqrt(U) around it -> a certified lower bound L <= f^2.
+//  C  point blocks (<= 32 lattice-adjacent rows) in decreasing max-U order:
+//     stop as soon as the best remaining block's max U < L; otherwise
+//     search the block's points with U >= L exactly over the region that
+//     covers their U-balls (sampled first if that region is large) and
+//     raise L.
+//  F  finalize: candidates for the maximum (m32 + E >= max(m32 - E)) in
+//     decreasing order, each refined to the reference's float64 value over
+//     the grid cells of its small ball; stop once no candidate can beat the
+//     running maximum.
+// fp32 values carry the rigorous error bound E of err_bound(); every bound
+// above is taken with it, so the result is the reference's float64 value.
+#include <cub/cub.cuh>
+
+#include "fph_dev.cuh"
+
+namespace fph {
+
+namespace {
+
+constexpr int kSW = 8;          // warps per CTA
+constexpr int kSThreads = 32 * kSW;
+constexpr int kWT = 512;        // candidates per warp tile
+constexpr int kMaxBlk = 160;    // blocks ordered best-first per simplex
+
+struct WarpSmem {
+    float4 tA[kWT / 2];  // pair p: (c0.x, c1.x, c0.y, c1.y)
+    float4 tB[kWT / 2];  //         (c0.z, c1.z, |c0|^2, |c1|^2)
+    int row_off[32];
+    int row_beg[32];
+    float key[kMaxBlk];
+};
+
+// cross-warp scratch of a CTA working on one simplex together
+struct TeamSmem {
+    float f[kSW][32];
+    double d[kSW];
+    long long ll[kSW];
+    float key[kMaxBlk];
+    int t;
+};
+
+struct SearchSmem {
+    double wt[256];  // c / m, exactly as the reference's template weights
+    WarpSmem w[kSW];
+    TeamSmem team;
+};
+
+// A team is one warp (size 1) or all warps of the CTA (size kSW) working on
+// one simplex: row batches are dealt round-robin to the team's warps and the
+// partial results combined through shared memory.
+struct Team {
+    int rank, size;
+    TeamSmem* ts;
+    __device__ __forceinline__ void sync() const {
+        if (size > 1) __syncthreads(); else __syncwarp();
+    }
+    // per-lane minimum across the team's warps
+    __device__ __forceinline__ float lane_min(float v) const {
+        if (size == 1) return v;
+        const int lane = threadIdx.x & 31;
+        __syncthreads();
+        ts->f[rank][lane] = v;
+        __syncthreads();
+        float r = ts->f[0][lane];
+        for (int i = 1; i < size; ++i) r = fminf(r, ts->f[i][lane]);
+        return r;
+    }
+    __device__ __forceinline__ double min_d(double v) const {  // warp-uniform v
+        if (size == 1) return v;
+        __syncthreads();
+        if ((threadIdx.x & 31) == 0) ts->d[rank] = v;
+        __syncthreads();
+        double r = ts->d[0];
+        for (int i = 1; i < size; ++i) r = fmin(r, ts->d[i]);
+        return r;
+    }
+    __device__ __forceinline__ float min_f(float v) const { return (float)min_d((double)v); }
+    __device__ __forceinline__ float max_f(float v) const { return -(float)min_d(-(double)v); }
+    __device__ __forceinline__ long long sum(long long v) const {  // warp-uniform v
+        if (size == 1) return v;
+        __syncthreads();
+        if ((threadIdx.x & 31) == 0) ts->ll[rank] = v;
+        __syncthreads();
+        long long r = 0;
+        for (int i = 0; i < size; ++i) r += ts->ll[i];
+        return r;
+    }
+};
+
+struct Ctx {
+    const FloodArgs* a;
+    SimplexGeom G;
+    Verts V;
+    const double* wt;
+    float thr;  // simplex ball (Lemma 4.2) on |a|^2; +inf when unpruned
+    int s;
+};
+
+struct PointF {
+    float bx, by, bz, bb, px2, py2, pz2, B;
+};
+
+__device__ __forceinline__ PointF point_at(const Ctx& c, int j, double p64[3]) {
+    embed_w(c.V, c.a->k, c.a->tmpl[j], c.wt, p64);
+    PointF q;
+    q.bx = __double2float_rn(__dsub_rn(p64[0], c.G.cx));
+    q.by = __double2float_rn(__dsub_rn(p64[1], c.G.cy));
+    q.bz = __double2float_rn(__dsub_rn(p64[2], c.G.cz));
+    q.bb = fmaf(q.bz, q.bz, fmaf(q.by, q.by, q.bx * q.bx));
+    q.px2 = -2.f * q.bx;
+    q.py2 = -2.f * q.by;
+    q.pz2 = -2.f * q.bz;
+    q.B = sqrtf(q.bb) * 1.0001f;
+    return q;
+}
+
+__device__ __forceinline__ PointF point_at(const Ctx& c, int j) {
+    double p64[3];
+    return point_at(c, j, p64);
+}
+
+// nearest vertex (a cloud point in subset mode): an upper bound on nn^2
+__device__ __forceinline__ float vertex_bound(const Ctx& c, const PointF& q) {
+    if (!c.a->subset) return INFINITY;
+    float dmin = INFINITY, vmax = 0.f;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        if (i <= c.a->k) {
+            const float vx = __double2float_rn(__dsub_rn(c.V.v[i][0], c.G.cx));
+            const float vy = __double2float_rn(__dsub_rn(c.V.v[i][1], c.G.cy));
+            const float vz = __double2float_rn(__dsub_rn(c.V.v[i][2], c.G.cz));
+            const float dx = q.bx - vx, dy = q.by - vy, dz = q.bz - vz;
+            dmin = fminf(dmin, fmaf(dz, dz, fmaf(dy, dy, dx * dx)));
+            vmax = fmaxf(vmax, fmaf(vz, vz, fmaf(vy, vy, vx * vx)));
+        }
+    }
+    const float sv = q.B + sqrtf(vmax) * 1.0001f;
+    return dmin * 1.00001f + (float)(16.0 * kU32) * sv * sv;
+}
+
+// ----------------------------------------------------- warp enumeration
+// Rows of a cell box, 32 at a time: lane r computes row r's run; the runs'
+// exclusive offsets go to shared memory so any lane can map a flattened
+// candidate position to its point index.
+struct Rows {
+    const Grid* g;
+    Box box;
+    double qx, qy, qz, R;
+    bool clip;
+};
+
+__device__ __forceinline__ Rows make_rows(const Grid& g, double qx, double qy, double qz,
+                                          double R) {
+    Rows r;
+    r.g = &g;
+    r.qx = qx;
+    r.qy = qy;
+    r.qz = qz;
+    r.R = R;
+    r.clip = R < 1e300;
+    r.box = r.clip ? ball_box(g, qx, qy, qz, R) : full_box(g);
+    return r;
+}
+
+__device__ __forceinline__ int row_batch(const Rows& rw, WarpSmem& W, int rb) {
+    const int lane = threadIdx.x & 31;
+    const int rows = rw.box.rows();
+    const int r = rb + lane;
+    const int2 run = r < rows ? row_run(*rw.g, rw.box, r, rw.qx, rw.qy, rw.qz, rw.R, rw.clip)
+                              : make_int2(0, 0);
+    const int len = run.y - run.x;
+    int incl = len;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+    }
+    __syncwarp();
+    W.row_off[lane] = incl - len;
+    W.row_beg[lane] = run.x;
+    __syncwarp();
+    return __shfl_sync(0xffffffffu, incl, 31);
+}
+
+__device__ __forceinline__ int cand_index(const WarpSmem& W, int nrow, int f) {
+    int lo = 0, hi = nrow;
+    while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (W.row_off[mid] <= f) lo = mid; else hi = mid;
+    }
+    return W.row_beg[lo] + f - W.row_off[lo];
+}
+
+__device__ __forceinline__ void load_rel(const Ctx& c, int idx, float& ax, float& ay, float& az,
+                                         float& aw) {
+    const Grid& g = c.a->g;
+    ax = __double2float_rn(__dsub_rn(g.x[idx], c.G.cx));
+    ay = __double2float_rn(__dsub_rn(g.y[idx], c.G.cy));
+    az = __double2float_rn(__dsub_rn(g.z[idx], c.G.cz));
+    aw = fmaf(az, az, fmaf(ay, ay, ax * ax));
+}
+
+// append the kept candidates of the warp to the tile; returns the new size
+__device__ __forceinline__ int tile_push(WarpSmem& W, int n, bool keep, float ax, float ay,
+                                         float az, float aw) {
+    const int lane = threadIdx.x & 31;
+    const unsigned bal = __ballot_sync(0xffffffffu, keep);
+    if (keep) {
+        const int q = n + __popc(bal & ((1u << lane) - 1u));
+        float* A = reinterpret_cast<float*>(W.tA) + (q >> 1) * 4 + (q & 1);
+        float* B = reinterpret_cast<float*>(W.tB) + (q >> 1) * 4 + (q & 1);
+        A[0] = ax;
+        A[2] = ay;
+        B[0] = az;
+        B[2] = aw;
+    }
+    return n + __popc(bal);
+}
+
+__device__ __forceinline__ void tile_pad(WarpSmem& W, int n) {
+    __syncwarp();
+    if ((n & 1) && (threadIdx.x & 31) == 0) {
+        float* A = reinterpret_cast<float*>(W.tA) + (n >> 1) * 4;
+        float* B = reinterpret_cast<float*>(W.tB) + (n >> 1) * 4;
+        A[1] = 0.f;
+        A[3] = 0.f;
+        B[1] = 0.f;
+        B[3] = INFINITY;  // |c|^2 = inf: never the minimum
+    }
+    __syncwarp();
+}
+
+// min over the tile of |a|^2 - 2 a.b for one point (3 FFMA2 + 1 FMNMX3 per
+// candidate pair, two independent chains)
+__device__ __forceinline__ float tile_min(const WarpSmem& W, int n, const PointF& q, float best) {
+    const float2 bx = make_float2(q.px2, q.px2), by = make_float2(q.py2, q.py2),
+                 bz = make_float2(q.pz2, q.pz2);
+    const int np = (n + 1) >> 1;
+    float b0 = best, b1 = INFINITY;
+    int p = 0;
+    for (; p + 1 < np; p += 2) {
+        const float4 A0 = W.tA[p], B0 = W.tB[p], A1 = W.tA[p + 1], B1 = W.tB[p + 1];
+        float2 u = ffma2(bz, make_float2(B0.x, B0.y), make_float2(B0.z, B0.w));
+        float2 v = ffma2(bz, make_float2(B1.x, B1.y), make_float2(B1.z, B1.w));
+        u = ffma2(by, make_float2(A0.z, A0.w), u);
+        v = ffma2(by, make_float2(A1.z, A1.w), v);
+        u = ffma2(bx, make_float2(A0.x, A0.y), u);
+        v = ffma2(bx, make_float2(A1.x, A1.y), v);
+        b0 = fmin3(b0, u.x, u.y);
+        b1 = fmin3(b1, v.x, v.y);
+    }
+    if (p < np) {
+        const float4 A0 = W.tA[p], B0 = W.tB[p];
+        float2 u = ffma2(bz, make_float2(B0.x, B0.y), make_float2(B0.z, B0.w));
+        u = ffma2(by, make_float2(A0.z, A0.w), u);
+        u = ffma2(bx, make_float2(A0.x, A0.y), u);
+        b0 = fmin3(b0, u.x, u.y);
+    }
+    return fminf(b0, b1);
+}
+
+// ------------------------------------------------------------ phase A
+// fold a full tile into the running minima of ALL sample points; a team
+// folds with atomicMin on order-preserving uints (vals_ord)
+__device__ void fold_all(const Ctx& c, WarpSmem& W, int n, float* vals, const Team& tm,
+                         unsigned long long& pairs) {
+    const int lane = threadIdx.x & 31;
+    tile_pad(W, n);
+    const int P = c.a->P;
+    for (int j0 = 0; j0 < P; j0 += 32) {
+        const int j = j0 + lane;
+        if (j < P) {
+            const PointF q = point_at(c, j);
+            const float v = tile_min(W, n, q, INFINITY) + q.bb;
+            if (tm.size == 1) vals[j] = fminf(vals[j], v);
+            else atomicMin(reinterpret_cast<unsigned*>(vals) + j, f2ord(v));
+        }
+    }
+    pairs += (unsigned long long)n * P;
+    __syncwarp();
+}
+
+__device__ void reps_pass(const Ctx& c, WarpSmem& W, int stride, float* vals, const Team& tm,
+                          unsigned long long& pairs, unsigned long long& staged) {
+    const int lane = threadIdx.x & 31;
+    const FloodArgs& a = *c.a;
+    const Rows rw = make_rows(a.g, c.G.cx, c.G.cy, c.G.cz, a.subset ? c.G.rho : 1e301);
+    const int rows = rw.box.rows();
+    int tile_n = 0;
+    long long fbase = 0;  // this warp's own enumeration: any subset is a valid sample
+    for (int rb = tm.rank * 32; rb < rows; rb += tm.size * 32) {
+        const int total = row_batch(rw, W, rb);
+        const int nrow = min(32, rows - rb);
+        const int first = (int)((stride - fbase % stride) % stride);
+        const int nsel = total > first ? (total - first - 1) / stride + 1 : 0;
+        for (int i0 = 0; i0 < nsel; i0 += 32) {
+            bool keep = false;
+            float ax = 0.f, ay = 0.f, az = 0.f, aw = 0.f;
+            if (i0 + lane < nsel) {
+                load_rel(c, cand_index(W, nrow, first + (i0 + lane) * stride), ax, ay, az, aw);
+                keep = aw <= c.thr;
+            }
+            tile_n = tile_push(W, tile_n, keep, ax, ay, az, aw);
+            if (tile_n > kWT - 32) {
+                staged += tile_n;
+                fold_all(c, W, tile_n, vals, tm, pairs);
+                tile_n = 0;
+            }
+        }
+        fbase += total;
+    }
+    if (tile_n > 0) {
+        staged += tile_n;
+        fold_all(c, W, tile_n, vals, tm, pairs);
+    }
+}
+
+// ------------------------------------------------------- single points
+// exact fp32 minimum of |a|^2 - 2 a.b over every candidate within R of q
+__device__ float point_min32(const Ctx& c, WarpSmem& W, const PointF& q, double R, const Team& tm,
+                             unsigned long long& scanned) {
+    const int lane = threadIdx.x & 31;
+    const double qx = c.G.cx + (double)q.bx, qy = c.G.cy + (double)q.by,
+                 qz = c.G.cz + (double)q.bz;
+    const double Rrow = R * (1.0 + 1e-4) + 1e-5 * ((double)q.B + R) + c.a->g.margin;
+    const Rows rw = make_rows(c.a->g, qx, qy, qz, Rrow);
+    const int rows = rw.box.rows();
+    float best = INFINITY;
+    for (int rb = tm.rank * 32; rb < rows; rb += tm.size * 32) {
+        const int total = row_batch(rw, W, rb);
+        const int nrow = min(32, rows - rb);
+        scanned += total;
+        for (int f = lane; f < total; f += 32) {
+            float ax, ay, az, aw;
+            load_rel(c, cand_index(W, nrow, f), ax, ay, az, aw);
+            if (aw <= c.thr) best = fminf(best, fmaf(q.px2, ax, fmaf(q.py2, ay, fmaf(q.pz2, az, aw))));
+        }
+    }
+    return tm.min_f(warp_min_f(best));
+}
+
+// the reference's float64 squared distance minimised over the grid cells of
+// the ball |x - p| <= R (contains every float64 nearest neighbour)
+__device__ double point_min64(const Ctx& c, WarpSmem& W, const double p[3], double R,
+                              const Team& tm, unsigned long long& scanned) {
+    const int lane = threadIdx.x & 31;
+    const Rows rw = make_rows(c.a->g, p[0], p[1], p[2], R);
+    const int rows = rw.box.rows();
+    const Grid& g = c.a->g;
+    double best = INFINITY;
+    for (int rb = tm.rank * 32; rb < rows; rb += tm.size * 32) {
+        const int total = row_batch(rw, W, rb);
+        const int nrow = min(32, rows - rb);
+        scanned += total;
+        for (int f = lane; f < total; f += 32) {
+            const int idx = cand_index(W, nrow, f);
+            best = fmin(best, sq64(g.x[idx], g.y[idx], g.z[idx], p[0], p[1], p[2]));
+        }
+    }
+    return tm.min_d(warp_min_d(best));
+}
+
+// ------------------------------------------------------------ phase C
+// One block: the points with U >= L searched exactly over the region that
+// covers their U-balls.  Updates vals (certified m32, or -inf when the
+// point cannot reach L) and L (identical in every warp of the team).
+__device__ void search_block(const Ctx& c, WarpSmem& W, int blk, float* vals, float& L,
+                             const Team& tm, unsigned long long* st) {
+    const int lane = threadIdx.x & 31;
+    const FloodArgs& a = *c.a;
+    const int j0 = a.blk_off[blk], nb = a.blk_off[blk + 1] - j0;
+    const bool valid = lane < nb;
+    const int j = j0 + (valid ? lane : nb - 1);
+    const PointF q = point_at(c, j);
+    float U2 = vals[j];
+    bool active = valid && U2 >= L;
+    const float inv = 1.f / (float)nb;
+    float sx = valid ? q.bx : 0.f, sy = valid ? q.by : 0.f, sz = valid ? q.bz : 0.f;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        sx += __shfl_xor_sync(0xffffffffu, sx, o);
+        sy += __shfl_xor_sync(0xffffffffu, sy, o);
+        sz += __shfl_xor_sync(0xffffffffu, sz, o);
+    }
+    const float cbx = sx * inv, cby = sy * inv, cbz = sz * inv;
+    const float ddx = q.bx - cbx, ddy = q.by - cby, ddz = q.bz - cbz;
+    const double dB = sqrt((double)ddx * ddx + (double)ddy * ddy + (double)ddz * ddz) * (1.0 + 1e-5) +
+                      1e-6 * (double)q.B;
+    const double cbn = sqrt((double)cbx * cbx + (double)cby * cby + (double)cbz * cbz);
+    // The fp32 region test below accepts every candidate whose true
+    // distance to the block center is <= R (1 - 1e-4) - 1e-5 (|cb| + R);
+    // cover()'s 1e-3 inflation exceeds that shrink, so each covered U-ball
+    // is entirely inside the accepted region: the point is certified.
+    auto cover = [&](bool act, float u2) {
+        double r = act ? dB + sqrt((double)u2) : 0.0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) r = fmax(r, __shfl_xor_sync(0xffffffffu, r, o));
+        return r * (1.0 + 1e-3) + 1e-4 * cbn;
+    };
+    const double qx = c.G.cx + (double)cbx, qy = c.G.cy + (double)cby, qz = c.G.cz + (double)cbz;
+    double R = cover(active, U2);
+    float best = INFINITY;
+    for (int pass = 0; pass < 2; ++pass) {
+        const bool full = !(R < 1e300);
+        const double Rrow = full ? 1e301 : R * (1.0 + 1e-4) + 1e-5 * (cbn + R) + a.g.margin;
+        const float rout2 = full ? INFINITY : (float)(R * R);
+        const Rows rw = make_rows(a.g, qx, qy, qz, Rrow);
+        const int rows = rw.box.rows();
+        int stride = 1;
+        if (pass == 0) {
+            // count the region; a large one is sampled first to tighten U
+            long long cnt = 0;
+            for (int rb = tm.rank * 32; rb < rows; rb += tm.size * 32) cnt += row_batch(rw, W, rb);
+            cnt = tm.sum(cnt);
+            if (cnt > 4ll * a.reps_target) stride = (int)((cnt + a.reps_target - 1) / a.reps_target);
+        }
+        if (pass == 1 || stride > 1) {
+            int tile_n = 0;
+            long long fbase = 0;
+            unsigned long long stg = 0;
+            for (int rb = tm.rank * 32; rb < rows; rb += tm.size * 32) {
+                const int total = row_batch(rw, W, rb);
+                const int nrow = min(32, rows - rb);
+                const int first = (int)((stride - fbase % stride) % stride);
+                const int nsel = total > first ? (total - first - 1) / stride + 1 : 0;
+                for (int i0 = 0; i0 < nsel; i0 += 32) {
+                    bool keep = false;
+                    float ax = 0.f, ay = 0.f, az = 0.f, aw = 0.f;
+                    if (i0 + lane < nsel) {
+                        load_rel(c, cand_index(W, nrow, first + (i0 + lane) * stride), ax, ay, az, aw);
+                        const float dx = ax - cbx, dy = ay - cby, dz = az - cbz;
+                        keep = fmaf(dz, dz, fmaf(dy, dy, dx * dx)) <= rout2 && aw <= c.thr;
+                    }
+                    tile_n = tile_push(W, tile_n, keep, ax, ay, az, aw);
+                    if (tile_n > kWT - 32) {
+                        tile_pad(W, tile_n);
+                        best = tile_min(W, tile_n, q, best);
+                        stg += tile_n;
+                        tile_n = 0;
+                        __syncwarp();
+                    }
+                }
+                fbase += total;
+            }
+            if (tile_n > 0) {
+                tile_pad(W, tile_n);
+                best = tile_min(W, tile_n, q, best);
+                stg += tile_n;
+                __syncwarp();
+            }
+            st[pass] += stg;
+            st[2] += stg * (unsigned long long)nb;
+            best = tm.lane_min(best);
+        }
+        if (pass == 0) {
+            if (stride > 1) {
+                const float m = best + q.bb;
+                U2 = fminf(U2, m + err_bound(m, q.B));
+                active = active && U2 >= L;
+                if (!__any_sync(0xffffffffu, active)) break;
+                R = cover(active, U2);
+            }
+            continue;
+        }
+        const float m32 = best + q.bb;
+        if (valid && tm.rank == 0) vals[j] = active ? m32 : -INFINITY;
+        const float lb = warp_max(active ? m32 - err_bound(m32, q.B) : -INFINITY);
+        L = fmaxf(L, lb);
+        tm.sync();
+        return;
+    }
+    if (valid && tm.rank == 0) vals[j] = -INFINITY;  // pruned after sampling
+    tm.sync();
+}
+
+// ------------------------------------------------------------- finalize
+// vals: certified m32 or -inf.  Returns the reference's float64 value.
+__device__ double finalize_team(const Ctx& c, WarpSmem& W, float* vals, const Team& tm,
+                                unsigned long long& refined, unsigned long long& scanned) {
+    const int lane = threadIdx.x & 31;
+    const int P = c.a->P;
+    // keys m32 + E (upper bounds), L2 = max(m32 - E) (lower bound)
+    float lmax = -INFINITY;
+    for (int j = tm.rank * 32 + lane; j < P; j += tm.size * 32) {
+        const float v = vals[j];
+        if (v > -INFINITY) {
+            const PointF q = point_at(c, j);
+            const float E = err_bound(v, q.B);
+            lmax = fmaxf(lmax, v - E);
+            vals[j] = v + E;
+        }
+    }
+    const float L2 = tm.max_f(warp_max(lmax));
+    tm.sync();
+    double M = -INFINITY;
+    for (;;) {
+        float kmax = -INFINITY;
+        int jm = 0x7fffffff;
+        for (int j = tm.rank * 32 + lane; j < P; j += tm.size * 32) {
+            const float v = vals[j];
+            if (v > kmax) {
+                kmax = v;
+                jm = j;
+            }
+        }
+        const float kw = warp_max(kmax);
+        const float km = tm.max_f(kw);
+        if (!(km >= L2) || (double)km <= M) break;
+        int jw = __reduce_min_sync(0xffffffffu, kmax == km ? jm : 0x7fffffff);
+        jm = -(int)tm.max_f(-(float)jw);  // lowest index holding km (exact in fp32 below 2^24)
+        double p[3];
+        const PointF q = point_at(c, jm, p);
+        const float E = err_bound(km, q.B) * 1.01f;
+        const double R = sqrt((double)km + (double)E) * (1.0 + 1e-6) + 1e-300;
+        M = fmax(M, point_min64(c, W, p, R, tm, scanned));
+        ++refined;
+        tm.sync();
+        if (tm.rank == 0 && lane == 0) vals[jm] = -INFINITY;
+        tm.sync();
+    }
+    return M;
+}
+
+// ------------------------------------------------------- one simplex
+__device__ void run_simplex(const Ctx& c, WarpSmem& W, const Team& tm) {
+    const int lane = threadIdx.x & 31;
+    const FloodArgs& a = *c.a;
+    float* vals = a.perpoint + (size_t)c.s * a.P;
+    unsigned long long pairs = 0, staged = 0, st[3] = {0, 0, 0}, refined = 0, scanned = 0,
+                       blocks = 0, pruned = 0;
+    // ---- A
+    for (int j = tm.rank * 32 + lane; j < a.P; j += tm.size * 32)
+        vals[j] = tm.size == 1 ? INFINITY : __uint_as_float(f2ord(INFINITY));
+    tm.sync();
+    const long long C = a.cand_count[c.s];
+    const int stride = (int)max(1ll, (C + a.reps_target - 1) / a.reps_target);
+    reps_pass(c, W, stride, vals, tm, pairs, staged);
+    tm.sync();
+    if (tm.size > 1) {  // decode the ordered minima
+        __threadfence_block();
+        for (int j = tm.rank * 32 + lane; j < a.P; j += tm.size * 32)
+            vals[j] = ord2f(__float_as_uint(vals[j]));
+        tm.sync();
+    }
+    if (stride > 1) {
+        // ---- B: upper bounds; exact search of the top point
+        float umax = -INFINITY;
+        int jmax = 0x7fffffff;
+        for (int j = tm.rank * 32 + lane; j < a.P; j += tm.size * 32) {
+            const PointF q = point_at(c, j);
+            const float m = vals[j];
+            const float u = fminf(m + err_bound(m, q.B), vertex_bound(c, q));
+            vals[j] = u;
+            if (u > umax) {
+                umax = u;
+                jmax = j;
+            }
+        }
+        const float um = tm.max_f(warp_max(umax));
+        const int jw = __reduce_min_sync(0xffffffffu, umax == um ? jmax : 0x7fffffff);
+        const int jt = -(int)tm.max_f(-(float)jw);
+        tm.sync();
+        float L;
+        {
+            const PointF q = point_at(c, jt);
+            const double R = sqrt((double)um) * (1.0 + 1e-3) + 1e-4 * (double)q.B;
+            const float m = point_min32(c, W, q, R, tm, scanned) + q.bb;
+            L = m - err_bound(m, q.B);
+        }
+        // ---- C: blocks best-first
+        const int nblk = a.nblk;
+        float* key = tm.size == 1 ? W.key : tm.ts->key;
+        if (nblk <= kMaxBlk) {
+            for (int b = tm.rank * 32 + lane; b < nblk; b += tm.size * 32) {
+                float k2 = -INFINITY;
+                for (int i = a.blk_off[b]; i < a.blk_off[b + 1]; ++i) k2 = fmaxf(k2, vals[i]);
+                key[b] = k2;
+            }
+            tm.sync();
+            for (;;) {
+                float kb = -INFINITY;
+                int bb = 0x7fffffff;
+                for (int b = lane; b < nblk; b += 32)
+                    if (key[b] > kb) {
+                        kb = key[b];
+                        bb = b;
+                    }
+                const float km = warp_max(kb);
+                if (!(km >= L)) break;  // every remaining block is below L
+                const int b = __reduce_min_sync(0xffffffffu, kb == km ? bb : 0x7fffffff);
+                tm.sync();
+                if (tm.rank == 0 && lane == 0) key[b] = -INFINITY;
+                tm.sync();
+                search_block(c, W, b, vals, L, tm, st);
+                ++blocks;
+            }
+            // blocks never searched cannot reach L
+            for (int b = 0; b < nblk; ++b) {
+                if (key[b] > -INFINITY) {
+                    ++pruned;
+                    for (int i = a.blk_off[b] + tm.rank * 32 + lane; i < a.blk_off[b + 1];
+                         i += tm.size * 32)
+                        vals[i] = -INFINITY;
+                }
+            }
+            tm.sync();
+        } else {
+            for (int b = 0; b < nblk; ++b) {
+                search_block(c, W, b, vals, L, tm, st);
+                ++blocks;
+            }
+        }
+    }
+    tm.sync();
+    const double M = finalize_team(c, W, vals, tm, refined, scanned);
+    unsigned long long* stats = a.stats;
+    if (lane == 0) {
+        if (tm.rank == 0) {
+            a.out_sq[c.s] = M;
+            atomicAdd(&stats[5], 1ull);
+            atomicAdd(&stats[7], blocks);
+            atomicAdd(&stats[8], pruned);
+            atomicAdd(&stats[3], refined);
+            if (tm.size > 1) atomicAdd(&stats[9], 1ull);
+        }
+        atomicAdd(&stats[0], pairs + st[2]);
+        atomicAdd(&stats[1], staged + st[0] + st[1]);
+        atomicAdd(&stats[4], scanned);
+        atomicAdd(&stats[16], staged);
+        atomicAdd(&stats[17], st[0]);
+        atomicAdd(&stats[18], st[1]);
+    }
+    tm.sync();
+}
+
+__global__ void __launch_bounds__(kSThreads, 2)
+    search_kernel(const __grid_constant__ FloodArgs a, const SimplexGeom* __restrict__ geom,
+                  const int* __restrict__ order, int* counter) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    SearchSmem& S = *reinterpret_cast<SearchSmem*>(smem_raw);
+    for (int i = threadIdx.x; i <= a.m; i += blockDim.x) S.wt[i] = __ddiv_rn((double)i, (double)a.m);
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    WarpSmem& W = S.w[w];
+    Ctx c;
+    c.a = &a;
+    c.wt = S.wt;
+    // team mode: the whole CTA per simplex while the queue (sorted by
+    // candidate count, largest first) holds big simplices
+    int pending = -1;
+    for (;;) {
+        __syncthreads();
+        if (threadIdx.x == 0) S.team.t = atomicAdd(counter, 1);
+        __syncthreads();
+        const int t = S.team.t;
+        if (t >= a.n) return;
+        const int s = order[t];
+        if (a.cand_count[s] <= a.team_threshold) {
+            pending = t;  // first small simplex: handed to warp 0
+            break;
+        }
+        c.s = s;
+        c.G = geom[s];
+        c.thr = a.subset ? (float)(c.G.rho * c.G.rho * (1.0 + 1e-5)) : INFINITY;
+        load_verts(a, s, c.V);
+        const Team tm{w, kSW, &S.team};
+        run_simplex(c, W, tm);
+    }
+    // warp mode
+    const Team tm{0, 1, nullptr};
+    for (;;) {
+        int t = 0;
+        if (w == 0 && pending >= 0) {
+            t = pending;
+            pending = -1;
+        } else {
+            if (lane == 0) t = atomicAdd(counter, 1);
+            t = __shfl_sync(0xffffffffu, t, 0);
+        }
+        if (t >= a.n) return;
+        c.s = order[t];
+        c.G = geom[c.s];
+        c.thr = a.subset ? (float)(c.G.rho * c.G.rho * (1.0 + 1e-5)) : INFINITY;
+        load_verts(a, c.s, c.V);
+        run_simplex(c, W, tm);
+    }
+}
+
+__global__ void iota_kernel(int* out, int n) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = i;
+}
+
+}  // namespace
+
+int launch_search(const FloodArgs& a, const SimplexGeom* d_geom, const int* d_cand,
+                  cudaStream_t stream) {
+    // order simplices by candidate count, largest first: the longest
+    // searches start early and the tail is made of small ones
+    int *d_keys = nullptr, *d_order = nullptr, *d_iota = nullptr, *d_counter = nullptr;
+    FPH_CUDA_TRY(cudaMallocAsync(&d_keys, sizeof(int) * a.n, stream));
+    FPH_CUDA_TRY(cudaMallocAsync(&d_order, sizeof(int) * a.n, stream));
+    FPH_CUDA_TRY(cudaMallocAsync(&d_iota, sizeof(int) * a.n, stream));
+    iota_kernel<<<(a.n + 255) / 256, 256, 0, stream>>>(d_iota, a.n);
+    FPH_CUDA_TRY(cudaMallocAsync(&d_counter, sizeof(int), stream));
+    FPH_CUDA_TRY(cudaMemsetAsync(d_counter, 0, sizeof(int), stream));
+    size_t tmp_bytes = 0;
+    cub::DeviceRadixSort::SortPairsDescending(nullptr, tmp_bytes, d_cand, d_keys, d_iota, d_order,
+                                              a.n, 0, 31, stream);
+    void* tmp = nullptr;
+    FPH_CUDA_TRY(cudaMallocAsync(&tmp, tmp_bytes, stream));
+    FPH_CUDA_TRY(cub::DeviceRadixSort::SortPairsDescending(tmp, tmp_bytes, d_cand, d_keys, d_iota,
+                                                           d_order, a.n, 0, 31, stream));
+    int dev = 0, sms = 0, occ = 0;
+    FPH_CUDA_TRY(cudaGetDevice(&dev));
+    FPH_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    const int smem = (int)sizeof(SearchSmem);
+    FPH_CUDA_TRY(cudaFuncSetAttribute(search_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    FPH_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, search_kernel, kSThreads, smem));
+    const int warps_needed = a.n;
+    int blocks = sms * (occ > 0 ? occ : 1);
+    blocks = blocks < (warps_needed + kSW - 1) / kSW ? blocks : (warps_needed + kSW - 1) / kSW;
+    search_kernel<<<blocks, kSThreads, smem, stream>>>(a, d_geom, d_order, d_counter);
+    FPH_CUDA_TRY(cudaGetLastError());
+    for (void* p : {(void*)d_keys, (void*)d_order, (void*)d_iota, (void*)d_counter, tmp})
+        FPH_CUDA_TRY(cudaFreeAsync(p, stream));
+    return FPH_OK;
+}
+
+}  // namespace fph

@@ -118,3 +118,44 @@ def test_flood_full_size_properties_and_sampled_oracle():
         index = {tuple(r): i for i, r in enumerate(tri.simplices_by_dim[k].tolist())}
         got = np.array([sq1[k][index[tuple(r)]] for r in sub[k].tolist()])
         assert np.array_equal(got, want[k]), k
+
+
+@pytest.fixture
+def algo_switch():
+    from paper_2509_22432_b200 import _native
+
+    lib = _native.require_gpu()
+
+    def use(algo, reps=0, team=0):
+        _native.check(lib.fph_set_search(algo, reps, team))
+
+    yield use
+    use(1)
+
+
+@pytest.mark.parametrize("reps,team", [(1024, 32768), (64, 1000), (4096, 2**30), (300, 1)])
+def test_block_search_equals_brute_force_full_size(algo_switch, reps, team):
+    """The two exact algorithms agree bit for bit on BASELINE configs[1]
+    (1M points, 2k landmarks, dims <= 2) for several search tunings: sample
+    sizes, and every simplex searched by one warp / by a whole CTA."""
+    X = gen_sphere_torus_mix(1_000_000, seed=0).points
+    tri = delaunay(X[farthest_point_sampling(X, 2000)])
+    algo_switch(0)
+    brute = flood_sq_values(X, tri, 20, True, 2)
+    algo_switch(1, reps, team)
+    search = flood_sq_values(X, tri, 20, True, 2)
+    for k in range(3):
+        assert np.array_equal(brute[k], search[k]), k
+
+
+@pytest.mark.parametrize("algo,reps,team", [(0, 0, 0), (1, 0, 0), (1, 16, 1), (1, 16, 2**30)])
+@pytest.mark.parametrize("name", ["torus10k_m20", "rand3d_m30", "external2d", "circle_m64",
+                                  "dup3d_m5"])
+def test_both_algorithms_golden(algo_switch, algo, reps, team, name):
+    algo_switch(algo, reps, team)
+    z = G.load("flood", name)
+    tri = C.triangulation(z["tri_points"], G.simplices_by_dim(z))
+    subset = str(z["landmark_mode"]) == "subset"
+    sq = flood_sq_values(z["points"], tri, int(z["grid_resolution"]), subset)
+    for k, want in G.values_by_dim(z).items():
+        assert np.array_equal(np.sqrt(sq[k]), want), k
