@@ -123,7 +123,7 @@ int fph_set_tuning(double cell_occupancy, double pairs_per_task);
  * the Lemma-4.2 ball.  Both are exact (identical values).
  * reps_target: candidates per representative (sampling) pass;
  * team_threshold: simplices with more candidates are searched by a whole
- * CTA instead of one warp.  <= 0 keeps the defaults (1024, 32768).
+ * CTA instead of one warp.  <= 0 keeps the defaults (512, 131072).
  */
 int fph_set_search(int32_t algo, int32_t reps_target, int32_t team_threshold);
 

@@ -62,7 +62,7 @@ def load(path: str | None = None):
     global _lib
     if _lib is not None:
         return _lib
-    path = path or LIB_PATH
+    path = path or os.environ.get("FPH_LIB") or LIB_PATH
     if not os.path.exists(path):
         raise RuntimeError(
             f"CUDA library not built ({path}); run `python -m paper_2509_22432_b200._build` "

@@ -16,13 +16,13 @@
 namespace fph {
 
 static thread_local char g_err[1024] = "";
-static double g_occupancy = 8.0;
+static double g_occupancy = 2.0;
 static double g_pairs_per_task = 0.0;
 static bool g_profile = false;
 static int g_algo = 1;
 static double g_probe_cells = 1.0;
-static int g_reps_target = 1024;
-static int g_team_threshold = 32768;
+static int g_reps_target = 512;
+static int g_team_threshold = 131072;
 static thread_local long long g_launches = 0;
 
 void set_error(const char* fmt, ...) {
@@ -181,7 +181,7 @@ int fph_device_count(void) {
 }
 
 int fph_set_tuning(double cell_occupancy, double pairs_per_task) {
-    g_occupancy = cell_occupancy > 0 ? cell_occupancy : 8.0;
+    g_occupancy = cell_occupancy > 0 ? cell_occupancy : 2.0;
     g_pairs_per_task = pairs_per_task > 0 ? pairs_per_task : 0.0;
     return FPH_OK;
 }
@@ -205,8 +205,8 @@ int fph_set_search(int32_t algo, int32_t reps_target, int32_t team_threshold) {
         return FPH_EARG;
     }
     g_algo = algo;
-    g_reps_target = reps_target > 0 ? reps_target : 1024;
-    g_team_threshold = team_threshold > 0 ? team_threshold : 32768;
+    g_reps_target = reps_target > 0 ? reps_target : 512;
+    g_team_threshold = team_threshold > 0 ? team_threshold : 131072;
     return FPH_OK;
 }
 

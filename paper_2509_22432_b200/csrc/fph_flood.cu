@@ -608,7 +608,7 @@ int flood_interior(const Grid& g, const double* d_landmarks3, const int* d_simpl
     a.nblk = search ? (int)blk_off.size() - 1 : 0;
     a.probe = tune.probe_cells * g.h;
     a.reps_target = tune.reps_target > 0 ? tune.reps_target : 384;
-    a.team_threshold = tune.team_threshold > 0 ? tune.team_threshold : 32768;
+    a.team_threshold = tune.team_threshold > 0 ? tune.team_threshold : 131072;
     int* d_blk = nullptr;
 
     uchar4* d_tmpl = nullptr;

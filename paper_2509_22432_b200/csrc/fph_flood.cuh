@@ -45,7 +45,7 @@ struct FloodTuning {
     int algo = 1;                 // 0: brute force over the Lemma-4.2 ball, 1: block search
     double probe_cells = 1.0;     // block search: first-round margin in grid cells
     int reps_target = 384;        // block search: candidates per representative pass
-    int team_threshold = 32768;   // block search: CTA-cooperative simplices above this
+    int team_threshold = 131072;  // bounded search: CTA-cooperative simplices above this
 };
 
 // out[0..5]: work counters (see g_stats), out[6]: pass-kernel ms

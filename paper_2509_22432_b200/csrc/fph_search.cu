@@ -35,7 +35,13 @@ namespace {
 
 constexpr int kSW = 8;          // warps per CTA
 constexpr int kSThreads = 32 * kSW;
-constexpr int kWT = 512;        // candidates per warp tile
+#ifndef FPH_WT
+#define FPH_WT 512
+#endif
+#ifndef FPH_SEARCH_MINB
+#define FPH_SEARCH_MINB 2
+#endif
+constexpr int kWT = FPH_WT;     // candidates per warp tile
 constexpr int kMaxBlk = 160;    // blocks ordered best-first per simplex
 
 struct WarpSmem {
@@ -178,7 +184,17 @@ __device__ __forceinline__ Rows make_rows(const Grid& g, double qx, double qy, d
     return r;
 }
 
-__device__ __forceinline__ int row_batch(const Rows& rw, WarpSmem& W, int rb) {
+// One batch of 32 rows: lane r holds row r's run; the non-empty runs are
+// compacted into shared memory (exclusive offsets and first points) so any
+// flattened candidate position maps to its point index.
+struct Batch {
+    int total;  // candidates in the batch
+    int nne;    // non-empty rows
+    int off;    // this lane's row: exclusive offset
+    int len;    //                  run length
+};
+
+__device__ __forceinline__ Batch row_batch(const Rows& rw, WarpSmem& W, int rb) {
     const int lane = threadIdx.x & 31;
     const int rows = rw.box.rows();
     const int r = rb + lane;
@@ -191,15 +207,38 @@ __device__ __forceinline__ int row_batch(const Rows& rw, WarpSmem& W, int rb) {
         const int t = __shfl_up_sync(0xffffffffu, incl, o);
         if (lane >= o) incl += t;
     }
+    const unsigned ne = __ballot_sync(0xffffffffu, len > 0);
+    const int rank = __popc(ne & ((1u << lane) - 1u));
     __syncwarp();
-    W.row_off[lane] = incl - len;
-    W.row_beg[lane] = run.x;
+    if (len > 0) {
+        W.row_off[rank] = incl - len;
+        W.row_beg[rank] = run.x;
+    }
     __syncwarp();
-    return __shfl_sync(0xffffffffu, incl, 31);
+    Batch b;
+    b.total = __shfl_sync(0xffffffffu, incl, 31);
+    b.nne = __popc(ne);
+    b.off = incl - len;
+    b.len = len;
+    return b;
 }
 
-__device__ __forceinline__ int cand_index(const WarpSmem& W, int nrow, int f) {
-    int lo = 0, hi = nrow;
+// point index of the contiguous position f0 + lane (garbage when past the
+// batch total): the row is the last non-empty row starting at or before it,
+// found from the window's start bitmask instead of a search
+__device__ __forceinline__ int window_index(const WarpSmem& W, const Batch& b, int f0) {
+    const int lane = threadIdx.x & 31;
+    const bool starts = b.len > 0 && b.off >= f0 && b.off < f0 + 32;
+    const unsigned mask = __reduce_or_sync(0xffffffffu, starts ? 1u << (b.off - f0) : 0u);
+    const int before = __popc(__ballot_sync(0xffffffffu, b.len > 0 && b.off < f0));
+    const unsigned upto = lane == 31 ? mask : (mask & ((2u << lane) - 1u));
+    const int k = max(before + __popc(upto) - 1, 0);
+    return W.row_beg[k] + f0 + lane - W.row_off[k];
+}
+
+// point index of an arbitrary position f < total (strided sampling)
+__device__ __forceinline__ int cand_index(const WarpSmem& W, int nne, int f) {
+    int lo = 0, hi = nne;
     while (hi - lo > 1) {
         const int mid = (lo + hi) >> 1;
         if (W.row_off[mid] <= f) lo = mid; else hi = mid;
@@ -252,27 +291,31 @@ __device__ __forceinline__ float tile_min(const WarpSmem& W, int n, const PointF
     const float2 bx = make_float2(q.px2, q.px2), by = make_float2(q.py2, q.py2),
                  bz = make_float2(q.pz2, q.pz2);
     const int np = (n + 1) >> 1;
-    float b0 = best, b1 = INFINITY;
+    float b0 = best, b1 = INFINITY, b2 = INFINITY, b3 = INFINITY;
     int p = 0;
-    for (; p + 1 < np; p += 2) {
-        const float4 A0 = W.tA[p], B0 = W.tB[p], A1 = W.tA[p + 1], B1 = W.tB[p + 1];
-        float2 u = ffma2(bz, make_float2(B0.x, B0.y), make_float2(B0.z, B0.w));
-        float2 v = ffma2(bz, make_float2(B1.x, B1.y), make_float2(B1.z, B1.w));
-        u = ffma2(by, make_float2(A0.z, A0.w), u);
-        v = ffma2(by, make_float2(A1.z, A1.w), v);
-        u = ffma2(bx, make_float2(A0.x, A0.y), u);
-        v = ffma2(bx, make_float2(A1.x, A1.y), v);
-        b0 = fmin3(b0, u.x, u.y);
-        b1 = fmin3(b1, v.x, v.y);
+    // four candidate pairs per iteration: four independent chains
+    for (; p + 3 < np; p += 4) {
+        float2 u[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const float4 A = W.tA[p + i], B = W.tB[p + i];
+            u[i] = ffma2(bz, make_float2(B.x, B.y), make_float2(B.z, B.w));
+            u[i] = ffma2(by, make_float2(A.z, A.w), u[i]);
+            u[i] = ffma2(bx, make_float2(A.x, A.y), u[i]);
+        }
+        b0 = fmin3(b0, u[0].x, u[0].y);
+        b1 = fmin3(b1, u[1].x, u[1].y);
+        b2 = fmin3(b2, u[2].x, u[2].y);
+        b3 = fmin3(b3, u[3].x, u[3].y);
     }
-    if (p < np) {
-        const float4 A0 = W.tA[p], B0 = W.tB[p];
-        float2 u = ffma2(bz, make_float2(B0.x, B0.y), make_float2(B0.z, B0.w));
-        u = ffma2(by, make_float2(A0.z, A0.w), u);
-        u = ffma2(bx, make_float2(A0.x, A0.y), u);
+    for (; p < np; ++p) {
+        const float4 A = W.tA[p], B = W.tB[p];
+        float2 u = ffma2(bz, make_float2(B.x, B.y), make_float2(B.z, B.w));
+        u = ffma2(by, make_float2(A.z, A.w), u);
+        u = ffma2(bx, make_float2(A.x, A.y), u);
         b0 = fmin3(b0, u.x, u.y);
     }
-    return fminf(b0, b1);
+    return fminf(fminf(b0, b1), fminf(b2, b3));
 }
 
 // ------------------------------------------------------------ phase A
@@ -305,15 +348,17 @@ __device__ void reps_pass(const Ctx& c, WarpSmem& W, int stride, float* vals, co
     int tile_n = 0;
     long long fbase = 0;  // this warp's own enumeration: any subset is a valid sample
     for (int rb = tm.rank * 32; rb < rows; rb += tm.size * 32) {
-        const int total = row_batch(rw, W, rb);
-        const int nrow = min(32, rows - rb);
+        const Batch bt = row_batch(rw, W, rb);
+        const int total = bt.total;
         const int first = (int)((stride - fbase % stride) % stride);
         const int nsel = total > first ? (total - first - 1) / stride + 1 : 0;
         for (int i0 = 0; i0 < nsel; i0 += 32) {
+            const int widx = stride == 1 ? window_index(W, bt, i0) : 0;
             bool keep = false;
             float ax = 0.f, ay = 0.f, az = 0.f, aw = 0.f;
             if (i0 + lane < nsel) {
-                load_rel(c, cand_index(W, nrow, first + (i0 + lane) * stride), ax, ay, az, aw);
+                const int idx = stride == 1 ? widx : cand_index(W, bt.nne, first + (i0 + lane) * stride);
+                load_rel(c, idx, ax, ay, az, aw);
                 keep = aw <= c.thr;
             }
             tile_n = tile_push(W, tile_n, keep, ax, ay, az, aw);
@@ -343,13 +388,16 @@ __device__ float point_min32(const Ctx& c, WarpSmem& W, const PointF& q, double 
     const int rows = rw.box.rows();
     float best = INFINITY;
     for (int rb = tm.rank * 32; rb < rows; rb += tm.size * 32) {
-        const int total = row_batch(rw, W, rb);
-        const int nrow = min(32, rows - rb);
-        scanned += total;
-        for (int f = lane; f < total; f += 32) {
-            float ax, ay, az, aw;
-            load_rel(c, cand_index(W, nrow, f), ax, ay, az, aw);
-            if (aw <= c.thr) best = fminf(best, fmaf(q.px2, ax, fmaf(q.py2, ay, fmaf(q.pz2, az, aw))));
+        const Batch bt = row_batch(rw, W, rb);
+        scanned += bt.total;
+        for (int f0 = 0; f0 < bt.total; f0 += 32) {
+            const int idx = window_index(W, bt, f0);
+            if (f0 + lane < bt.total) {
+                float ax, ay, az, aw;
+                load_rel(c, idx, ax, ay, az, aw);
+                if (aw <= c.thr)
+                    best = fminf(best, fmaf(q.px2, ax, fmaf(q.py2, ay, fmaf(q.pz2, az, aw))));
+            }
         }
     }
     return tm.min_f(warp_min_f(best));
@@ -365,12 +413,12 @@ __device__ double point_min64(const Ctx& c, WarpSmem& W, const double p[3], doub
     const Grid& g = c.a->g;
     double best = INFINITY;
     for (int rb = tm.rank * 32; rb < rows; rb += tm.size * 32) {
-        const int total = row_batch(rw, W, rb);
-        const int nrow = min(32, rows - rb);
-        scanned += total;
-        for (int f = lane; f < total; f += 32) {
-            const int idx = cand_index(W, nrow, f);
-            best = fmin(best, sq64(g.x[idx], g.y[idx], g.z[idx], p[0], p[1], p[2]));
+        const Batch bt = row_batch(rw, W, rb);
+        scanned += bt.total;
+        for (int f0 = 0; f0 < bt.total; f0 += 32) {
+            const int idx = window_index(W, bt, f0);
+            if (f0 + lane < bt.total)
+                best = fmin(best, sq64(g.x[idx], g.y[idx], g.z[idx], p[0], p[1], p[2]));
         }
     }
     return tm.min_d(warp_min_d(best));
@@ -426,7 +474,7 @@ __device__ void search_block(const Ctx& c, WarpSmem& W, int blk, float* vals, fl
         if (pass == 0) {
             // count the region; a large one is sampled first to tighten U
             long long cnt = 0;
-            for (int rb = tm.rank * 32; rb < rows; rb += tm.size * 32) cnt += row_batch(rw, W, rb);
+            for (int rb = tm.rank * 32; rb < rows; rb += tm.size * 32) cnt += row_batch(rw, W, rb).total;
             cnt = tm.sum(cnt);
             if (cnt > 4ll * a.reps_target) stride = (int)((cnt + a.reps_target - 1) / a.reps_target);
         }
@@ -434,26 +482,48 @@ __device__ void search_block(const Ctx& c, WarpSmem& W, int blk, float* vals, fl
             int tile_n = 0;
             long long fbase = 0;
             unsigned long long stg = 0;
+            auto take = [&](bool keep, float ax, float ay, float az, float aw) {
+                tile_n = tile_push(W, tile_n, keep, ax, ay, az, aw);
+                if (tile_n > kWT - 32) {
+                    tile_pad(W, tile_n);
+                    best = tile_min(W, tile_n, q, best);
+                    stg += tile_n;
+                    tile_n = 0;
+                    __syncwarp();
+                }
+            };
+            auto accept = [&](float ax, float ay, float az, float aw) {
+                const float dx = ax - cbx, dy = ay - cby, dz = az - cbz;
+                return fmaf(dz, dz, fmaf(dy, dy, dx * dx)) <= rout2 && aw <= c.thr;
+            };
             for (int rb = tm.rank * 32; rb < rows; rb += tm.size * 32) {
-                const int total = row_batch(rw, W, rb);
-                const int nrow = min(32, rows - rb);
-                const int first = (int)((stride - fbase % stride) % stride);
-                const int nsel = total > first ? (total - first - 1) / stride + 1 : 0;
-                for (int i0 = 0; i0 < nsel; i0 += 32) {
-                    bool keep = false;
-                    float ax = 0.f, ay = 0.f, az = 0.f, aw = 0.f;
-                    if (i0 + lane < nsel) {
-                        load_rel(c, cand_index(W, nrow, first + (i0 + lane) * stride), ax, ay, az, aw);
-                        const float dx = ax - cbx, dy = ay - cby, dz = az - cbz;
-                        keep = fmaf(dz, dz, fmaf(dy, dy, dx * dx)) <= rout2 && aw <= c.thr;
+                const Batch bt = row_batch(rw, W, rb);
+                const int total = bt.total;
+                if (stride == 1) {
+                    // two windows in flight: both loads issue before either is used
+                    for (int f0 = 0; f0 < total; f0 += 64) {
+                        const int i0 = window_index(W, bt, f0);
+                        const int i1 = window_index(W, bt, f0 + 32);
+                        const bool v0 = f0 + lane < total, v1 = f0 + 32 + lane < total;
+                        float x0 = 0.f, y0 = 0.f, z0 = 0.f, w0 = 0.f, x1 = 0.f, y1 = 0.f, z1 = 0.f,
+                              w1 = 0.f;
+                        if (v0) load_rel(c, i0, x0, y0, z0, w0);
+                        if (v1) load_rel(c, i1, x1, y1, z1, w1);
+                        take(v0 && accept(x0, y0, z0, w0), x0, y0, z0, w0);
+                        if (f0 + 32 < total) take(v1 && accept(x1, y1, z1, w1), x1, y1, z1, w1);
                     }
-                    tile_n = tile_push(W, tile_n, keep, ax, ay, az, aw);
-                    if (tile_n > kWT - 32) {
-                        tile_pad(W, tile_n);
-                        best = tile_min(W, tile_n, q, best);
-                        stg += tile_n;
-                        tile_n = 0;
-                        __syncwarp();
+                } else {
+                    const int first = (int)((stride - fbase % stride) % stride);
+                    const int nsel = total > first ? (total - first - 1) / stride + 1 : 0;
+                    for (int i0 = 0; i0 < nsel; i0 += 32) {
+                        bool keep = false;
+                        float ax = 0.f, ay = 0.f, az = 0.f, aw = 0.f;
+                        if (i0 + lane < nsel) {
+                            load_rel(c, cand_index(W, bt.nne, first + (i0 + lane) * stride), ax, ay,
+                                     az, aw);
+                            keep = accept(ax, ay, az, aw);
+                        }
+                        take(keep, ax, ay, az, aw);
                     }
                 }
                 fbase += total;
@@ -649,7 +719,7 @@ __device__ void run_simplex(const Ctx& c, WarpSmem& W, const Team& tm) {
     tm.sync();
 }
 
-__global__ void __launch_bounds__(kSThreads, 2)
+__global__ void __launch_bounds__(kSThreads, FPH_SEARCH_MINB)
     search_kernel(const __grid_constant__ FloodArgs a, const SimplexGeom* __restrict__ geom,
                   const int* __restrict__ order, int* counter) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
