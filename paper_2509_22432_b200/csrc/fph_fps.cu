@@ -18,6 +18,15 @@
 // iteration arrived, then the CTA reads every slot in one coalesced pass.
 // All CTAs reduce the same slots in the same order, so they agree on the
 // next landmark without a second broadcast.
+//
+// Clouds too large for shared memory use the tiled variant: points are
+// Morton-sorted into 256-point tiles with float64 bounding boxes, and an
+// iteration only touches the tiles that contain the new landmark or whose
+// box is closer to it than the tile's current largest running minimum --
+// any other tile provably keeps every value (and its cached argmax).  Late
+// iterations touch a few tiles instead of streaming the whole cloud.
+#include <cub/cub.cuh>
+
 #include "fph_common.cuh"
 
 namespace fph {
@@ -163,6 +172,258 @@ __global__ void __launch_bounds__(kFpsThreads, 1)
     }
 }
 
+
+// ------------------------------------------------------------ tiled variant
+constexpr int kTileP = 256;  // points per tile
+
+// winner of this iteration across the grid (identical in every CTA)
+__device__ __forceinline__ int grid_argmax(double bv, int bi, int it, Slot* slots,
+                                           unsigned long long* arrived, double* red_v,
+                                           int* red_i) {
+    block_argmax(bv, bi, red_v, red_i);
+    const int G = gridDim.x;
+    Slot* buf = slots + (it & 1) * G;
+    if (threadIdx.x == 0) {
+        buf[blockIdx.x].val = bv;
+        buf[blockIdx.x].idx = bi;
+        __threadfence();
+        atomicAdd(arrived, 1ull);
+        const unsigned long long target = (unsigned long long)G * it;
+        while (ld_acquire(arrived) < target) {
+        }
+    }
+    __syncthreads();
+    double v = -INFINITY;
+    int i = 0x7fffffff;
+    for (int b = threadIdx.x; b < G; b += blockDim.x) better(v, i, __ldcg(&buf[b].val), __ldcg(&buf[b].idx));
+    block_argmax(v, i, red_v, red_i);
+    return i;
+}
+
+__global__ void __launch_bounds__(kFpsThreads, 1)
+    fps_tiled_kernel(const double* __restrict__ px, const double* __restrict__ py,
+                     const double* __restrict__ pz, const double* __restrict__ sx,
+                     const double* __restrict__ sy, const double* __restrict__ sz,
+                     const int* __restrict__ sidx, const int* __restrict__ spos,
+                     const double* __restrict__ tbox, int n, int k, int start, int per_cta,
+                     int ntiles, double* __restrict__ md, Slot* slots, unsigned long long* arrived,
+                     long long* __restrict__ out) {
+    extern __shared__ double sm[];
+    __shared__ double red_v[32];
+    __shared__ int red_i[32];
+    // tiles are dealt round-robin (tile = blockIdx.x + t * G): the few tiles
+    // near a new landmark are Morton neighbours, so they land on different
+    // CTAs instead of piling onto one
+    const int G = gridDim.x;
+    const int nt = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / G + 1 : 0;
+    double* box = sm;                   // nt x 6
+    double* tmax = sm + 6 * per_cta;    // nt
+    int* targ = reinterpret_cast<int*>(tmax + per_cta);
+    for (int t = threadIdx.x; t < nt; t += blockDim.x) {
+        for (int c = 0; c < 6; ++c) box[t * 6 + c] = tbox[(size_t)(blockIdx.x + t * G) * 6 + c];
+        tmax[t] = INFINITY;
+        targ[t] = 0x7fffffff;
+    }
+    for (int t = 0; t < nt; ++t) {
+        const long long base = (long long)(blockIdx.x + t * G) * kTileP;
+        for (int j = threadIdx.x; j < kTileP; j += blockDim.x)
+            if (base + j < n) md[base + j] = INFINITY;
+    }
+    __syncthreads();
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    int cur = start;
+    if (blockIdx.x == 0 && threadIdx.x == 0) out[0] = start;
+    for (int it = 1; it < k; ++it) {
+        const double qx = px[cur], qy = py[cur], qz = pz[cur];
+        const int ctile = spos[cur] / kTileP;
+        for (int t = w; t < nt; t += kFpsThreads / 32) {
+            const int tile = blockIdx.x + t * G;
+            const double* b = box + t * 6;
+            const double dx = fmax(0.0, fmax(b[0] - qx, qx - b[3]));
+            const double dy = fmax(0.0, fmax(b[1] - qy, qy - b[4]));
+            const double dz = fmax(0.0, fmax(b[2] - qz, qz - b[5]));
+            // a safe lower bound on sq64(x, q) for every x in the box
+            const double lb = (dx * dx + dy * dy + dz * dz) * (1.0 - 1e-12);
+            if (tile != ctile && !(lb < tmax[t])) continue;  // nothing in it can change
+            double v = -INFINITY;
+            int i = 0x7fffffff;
+            const long long base = (long long)tile * kTileP;
+            for (int j = l; j < kTileP; j += 32) {
+                const long long pp = base + j;
+                if (pp < n) {
+                    const int oi = sidx[pp];
+                    const double d = sq64(sx[pp], sy[pp], sz[pp], qx, qy, qz);
+                    const double m = oi == cur ? -1.0 : fmin(md[pp], d);
+                    md[pp] = m;
+                    better(v, i, m, oi);
+                }
+            }
+            warp_argmax(v, i);
+            if (l == 0) {
+                tmax[t] = v;
+                targ[t] = i;
+            }
+        }
+        __syncthreads();
+        double v = -INFINITY;
+        int i = 0x7fffffff;
+        for (int t = threadIdx.x; t < nt; t += blockDim.x) better(v, i, tmax[t], targ[t]);
+        cur = grid_argmax(v, i, it, slots, arrived, red_v, red_i);
+        if (blockIdx.x == 0 && threadIdx.x == 0) out[it] = cur;
+    }
+}
+
+__global__ void morton_kernel(const double* __restrict__ x, const double* __restrict__ y,
+                              const double* __restrict__ z, int n, double lox, double loy,
+                              double loz, double inv, unsigned* __restrict__ code,
+                              int* __restrict__ idx) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    auto q = [&](double v, double lo) {
+        return (unsigned)fmin(1023.0, fmax(0.0, floor((v - lo) * inv)));
+    };
+    auto spread = [](unsigned v) {
+        v = (v | (v << 16)) & 0x030000FFu;
+        v = (v | (v << 8)) & 0x0300F00Fu;
+        v = (v | (v << 4)) & 0x030C30C3u;
+        v = (v | (v << 2)) & 0x09249249u;
+        return v;
+    };
+    code[i] = spread(q(x[i], lox)) | (spread(q(y[i], loy)) << 1) | (spread(q(z[i], loz)) << 2);
+    idx[i] = i;
+}
+
+__global__ void gather_sorted_kernel(const double* __restrict__ x, const double* __restrict__ y,
+                                     const double* __restrict__ z, const int* __restrict__ sidx,
+                                     int n, double* __restrict__ sx, double* __restrict__ sy,
+                                     double* __restrict__ sz, int* __restrict__ spos) {
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= n) return;
+    const int i = sidx[p];
+    sx[p] = x[i];
+    sy[p] = y[i];
+    sz[p] = z[i];
+    spos[i] = p;
+}
+
+// one warp per tile: float64 bounding box
+__global__ void tile_box_kernel(const double* __restrict__ sx, const double* __restrict__ sy,
+                                const double* __restrict__ sz, int n, int ntiles,
+                                double* __restrict__ tbox) {
+    const int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, l = threadIdx.x & 31;
+    if (t >= ntiles) return;
+    double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+    for (int j = l; j < kTileP; j += 32) {
+        const long long p = (long long)t * kTileP + j;
+        if (p < n) {
+            const double v[3] = {sx[p], sy[p], sz[p]};
+            for (int c = 0; c < 3; ++c) {
+                lo[c] = fmin(lo[c], v[c]);
+                hi[c] = fmax(hi[c], v[c]);
+            }
+        }
+    }
+    for (int c = 0; c < 3; ++c) {
+        lo[c] = warp_min_d(lo[c]);
+        for (int o = 16; o > 0; o >>= 1) hi[c] = fmax(hi[c], __shfl_xor_sync(0xffffffffu, hi[c], o));
+    }
+    if (l == 0)
+        for (int c = 0; c < 3; ++c) {
+            tbox[(size_t)t * 6 + c] = lo[c];
+            tbox[(size_t)t * 6 + 3 + c] = hi[c];
+        }
+}
+
+__global__ void minmax_kernel(const double* __restrict__ v, int n, double* __restrict__ out2) {
+    double lo = INFINITY, hi = -INFINITY;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        lo = fmin(lo, v[i]);
+        hi = fmax(hi, v[i]);
+    }
+    lo = warp_min_d(lo);
+    for (int o = 16; o > 0; o >>= 1) hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    if ((threadIdx.x & 31) == 0) {
+        // non-negative reinterpretation trick is not needed: use CAS loops
+        unsigned long long* a = reinterpret_cast<unsigned long long*>(out2);
+        unsigned long long old = a[0], assumed;
+        do {
+            assumed = old;
+            if (__longlong_as_double((long long)assumed) <= lo) break;
+            old = atomicCAS(a, assumed, (unsigned long long)__double_as_longlong(lo));
+        } while (old != assumed);
+        old = a[1];
+        do {
+            assumed = old;
+            if (__longlong_as_double((long long)assumed) >= hi) break;
+            old = atomicCAS(a + 1, assumed, (unsigned long long)__double_as_longlong(hi));
+        } while (old != assumed);
+    }
+}
+
+int fps_tiled(const double* d_x, const double* d_y, const double* d_z, int n, int k, int start,
+              long long* d_out, int G, cudaStream_t stream) {
+    // bounding box (for the Morton quantisation only: any box works)
+    double* mm = nullptr;
+    FPH_CUDA_TRY(cudaMallocAsync(&mm, sizeof(double) * 6, stream));
+    const double init[6] = {INFINITY, -INFINITY, INFINITY, -INFINITY, INFINITY, -INFINITY};
+    FPH_CUDA_TRY(cudaMemcpyAsync(mm, init, sizeof(init), cudaMemcpyHostToDevice, stream));
+    minmax_kernel<<<1024, 256, 0, stream>>>(d_x, n, mm);
+    minmax_kernel<<<1024, 256, 0, stream>>>(d_y, n, mm + 2);
+    minmax_kernel<<<1024, 256, 0, stream>>>(d_z, n, mm + 4);
+    double h[6];
+    FPH_CUDA_TRY(cudaMemcpyAsync(h, mm, sizeof(h), cudaMemcpyDeviceToHost, stream));
+    FPH_CUDA_TRY(cudaStreamSynchronize(stream));
+    const double ext = fmax(fmax(h[1] - h[0], h[3] - h[2]), fmax(h[5] - h[4], 1e-300));
+    const double inv = 1024.0 / ext;
+    unsigned *code = nullptr, *code2 = nullptr;
+    int *idx = nullptr, *sidx = nullptr, *spos = nullptr;
+    double *sx = nullptr, *sy = nullptr, *sz = nullptr, *md = nullptr, *tbox = nullptr;
+    const int ntiles = (n + kTileP - 1) / kTileP;
+    FPH_CUDA_TRY(cudaMallocAsync(&code, sizeof(unsigned) * n, stream));
+    FPH_CUDA_TRY(cudaMallocAsync(&code2, sizeof(unsigned) * n, stream));
+    FPH_CUDA_TRY(cudaMallocAsync(&idx, sizeof(int) * n, stream));
+    FPH_CUDA_TRY(cudaMallocAsync(&sidx, sizeof(int) * n, stream));
+    FPH_CUDA_TRY(cudaMallocAsync(&spos, sizeof(int) * n, stream));
+    FPH_CUDA_TRY(cudaMallocAsync(&sx, sizeof(double) * n, stream));
+    FPH_CUDA_TRY(cudaMallocAsync(&sy, sizeof(double) * n, stream));
+    FPH_CUDA_TRY(cudaMallocAsync(&sz, sizeof(double) * n, stream));
+    FPH_CUDA_TRY(cudaMallocAsync(&md, sizeof(double) * n, stream));
+    FPH_CUDA_TRY(cudaMallocAsync(&tbox, sizeof(double) * 6 * (size_t)ntiles, stream));
+    morton_kernel<<<(n + 255) / 256, 256, 0, stream>>>(d_x, d_y, d_z, n, h[0], h[2], h[4], inv, code,
+                                                       idx);
+    size_t tmp_bytes = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, code, code2, idx, sidx, n, 0, 30, stream);
+    void* tmp = nullptr;
+    FPH_CUDA_TRY(cudaMallocAsync(&tmp, tmp_bytes, stream));
+    FPH_CUDA_TRY(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, code, code2, idx, sidx, n, 0, 30,
+                                                 stream));
+    gather_sorted_kernel<<<(n + 255) / 256, 256, 0, stream>>>(d_x, d_y, d_z, sidx, n, sx, sy, sz,
+                                                              spos);
+    tile_box_kernel<<<(ntiles * 32 + 255) / 256, 256, 0, stream>>>(sx, sy, sz, n, ntiles, tbox);
+    const int per_cta = (ntiles + G - 1) / G;
+    const size_t smem = sizeof(double) * 7 * per_cta + sizeof(int) * per_cta + 16;
+    Slot* slots = nullptr;
+    unsigned long long* arrived = nullptr;
+    FPH_CUDA_TRY(cudaMallocAsync(&slots, sizeof(Slot) * 2 * G, stream));
+    FPH_CUDA_TRY(cudaMallocAsync(&arrived, sizeof(unsigned long long), stream));
+    FPH_CUDA_TRY(cudaMemsetAsync(arrived, 0, sizeof(unsigned long long), stream));
+    FPH_CUDA_TRY(cudaFuncSetAttribute(fps_tiled_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)smem));
+    int ntl = ntiles;
+    void* args[] = {(void*)&d_x,  (void*)&d_y,  (void*)&d_z,   (void*)&sx,      (void*)&sy,
+                    (void*)&sz,   (void*)&sidx, (void*)&spos,  (void*)&tbox,    (void*)&n,
+                    (void*)&k,    (void*)&start, (void*)&per_cta, (void*)&ntl,  (void*)&md,
+                    (void*)&slots, (void*)&arrived, (void*)&d_out};
+    FPH_CUDA_TRY(cudaLaunchCooperativeKernel((void*)fps_tiled_kernel, dim3(G), dim3(kFpsThreads),
+                                             args, smem, stream));
+    FPH_CUDA_TRY(cudaGetLastError());
+    for (void* q : {(void*)mm, (void*)code, (void*)code2, (void*)idx, (void*)sidx, (void*)spos,
+                    (void*)sx, (void*)sy, (void*)sz, (void*)md, (void*)tbox, tmp, (void*)slots,
+                    (void*)arrived})
+        FPH_CUDA_TRY(cudaFreeAsync(q, stream));
+    return FPH_OK;
+}
+
 }  // namespace
 
 int fps_run(const double* d_x, const double* d_y, const double* d_z, int n, int k, int start,
@@ -187,6 +448,7 @@ int fps_run(const double* d_x, const double* d_y, const double* d_z, int n, int 
         smem = (size_t)chunk * 3 * sizeof(double);
         use_smem = true;
     }
+    if (!use_smem && k > 1) return fps_tiled(d_x, d_y, d_z, n, k, start, d_out, G, stream);
     Slot* slots = nullptr;
     double* mind = nullptr;
     unsigned long long* arrived = nullptr;

@@ -32,6 +32,20 @@ def test_fps_matches_oracle(n, dim, k, start):
     np.testing.assert_array_equal(got, oracle.fps(pts, k, start))
 
 
+@pytest.mark.parametrize("n,dim,k,start", [(2_000_000, 3, 300, 5), (1_400_000, 2, 200, 0)])
+def test_fps_tiled_matches_oracle(n, dim, k, start):
+    """Clouds beyond shared-memory residency take the Morton-tiled kernel."""
+    pts = np.random.default_rng(n + 1).normal(size=(n, dim))
+    got = farthest_point_sampling(pts, k, start)
+    np.testing.assert_array_equal(got, oracle.fps(pts, k, start))
+
+
+def test_fps_tiled_lattice_ties():
+    g = np.stack(np.meshgrid(np.arange(120.0), np.arange(120.0), np.arange(100.0)), -1).reshape(-1, 3)
+    got = farthest_point_sampling(g, 150, 17)
+    np.testing.assert_array_equal(got, oracle.fps(g, 150, 17))
+
+
 def test_fps_ties_uniform_grid():
     # a lattice is full of exact ties: lowest index must win every time
     g = np.stack(np.meshgrid(np.arange(40.0), np.arange(40.0), np.arange(5.0)), -1).reshape(-1, 3)
