@@ -282,11 +282,53 @@ int fph_farthest_point_sampling_batched(const double* points, int64_t batch, int
         set_error("batch must be nonnegative");
         return FPH_EARG;
     }
-    for (int64_t b = 0; b < batch; ++b) {
-        FPH_TRY(fph_farthest_point_sampling(points + b * n * dim, n, dim, k, start,
-                                            out_indices + b * k, memory, stream));
+    if (batch == 0) return FPH_OK;
+    FPH_TRY(check_cloud(points, n, dim));
+    if (k < 1 || k > n) {
+        set_error("k must be in [1, %lld], got %lld", (long long)n, (long long)k);
+        return FPH_EARG;
     }
-    return FPH_OK;
+    if (start < 0 || start >= n) {
+        set_error("start must be in [0, %lld), got %lld", (long long)n, (long long)start);
+        return FPH_EARG;
+    }
+    if (batch * n > 0x7fffffffLL) {
+        set_error("batch x n above 2^31 points is not supported");
+        return FPH_EARG;
+    }
+    FPH_TRY(ensure_device());
+    HostCtx hc;
+    FPH_TRY(hc.init(memory, stream));
+    int rc = FPH_OK;
+    {
+        Scratch sc(hc.stream);
+        const long long total = batch * n;
+        const double* d_pts = nullptr;
+        FPH_TRY(stage_in(sc, points, (size_t)total * dim, memory, &d_pts));
+        double *x, *y, *z;
+        FPH_TRY(sc.alloc(&x, total));
+        FPH_TRY(sc.alloc(&y, total));
+        FPH_TRY(sc.alloc(&z, total));
+        soa_kernel<<<blocks_for(total), 256, 0, hc.stream>>>(d_pts, total, dim, x, y, z);
+        count_launches(1);
+        long long* d_out = reinterpret_cast<long long*>(out_indices);
+        if (memory == FPH_MEM_HOST) FPH_TRY(sc.alloc(&d_out, (size_t)batch * k));
+        rc = fps_batched(x, y, z, (int)batch, (int)n, (int)k, (int)start, d_out, hc.stream);
+        count_launches(1);
+        if (rc == FPH_EARG) {  // clouds too large to group: one at a time
+            rc = FPH_OK;
+            for (int64_t b = 0; b < batch && rc == FPH_OK; ++b) {
+                rc = fps_run(x + b * n, y + b * n, z + b * n, (int)n, (int)k, (int)start,
+                             d_out + b * k, hc.stream);
+                count_launches(1);
+            }
+        }
+        if (rc == FPH_OK && memory == FPH_MEM_HOST)
+            FPH_CUDA_TRY(cudaMemcpyAsync(out_indices, d_out, sizeof(long long) * batch * k,
+                                         cudaMemcpyDeviceToHost, hc.stream));
+    }
+    if (memory == FPH_MEM_HOST) FPH_CUDA_TRY(cudaStreamSynchronize(hc.stream));
+    return rc;
 }
 
 int fph_flood_interior(const double* points, int64_t n_points, int32_t dim,

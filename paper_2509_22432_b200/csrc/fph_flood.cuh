@@ -68,4 +68,9 @@ int flood_complete(const double* d_interior, const int* d_facets, int n, int k,
 int fps_run(const double* d_x, const double* d_y, const double* d_z, int n, int k, int start,
             long long* d_out, cudaStream_t stream);
 
+// `batch` equal clouds (SoA, cloud-major); FPH_EARG if one cloud needs more
+// CTAs than there are SMs (the caller then runs fps_run per cloud)
+int fps_batched(const double* d_x, const double* d_y, const double* d_z, int batch, int n, int k,
+                int start, long long* d_out, cudaStream_t stream);
+
 }  // namespace fph

@@ -424,6 +424,81 @@ int fps_tiled(const double* d_x, const double* d_y, const double* d_z, int n, in
     return FPH_OK;
 }
 
+// ----------------------------------------------------------- batched clouds
+// Many equal-size clouds (configs[3]): CTA groups of `cpg` CTAs each run one
+// cloud at a time, exchanging through their own slots and counter, so
+// ngroups = gridDim / cpg clouds advance concurrently instead of every cloud
+// using (and waiting on) the whole GPU.
+__global__ void __launch_bounds__(kFpsThreads, 1)
+    fps_batched_kernel(const double* __restrict__ px, const double* __restrict__ py,
+                       const double* __restrict__ pz, int batch, int n, int k, int start, int cpg,
+                       int chunk, Slot* slots, unsigned long long* arrived,
+                       long long* __restrict__ out) {
+    extern __shared__ double sm[];
+    __shared__ double red_v[32];
+    __shared__ int red_i[32];
+    const int ngroups = gridDim.x / cpg;
+    const int g = blockIdx.x / cpg, r = blockIdx.x % cpg;
+    if (g >= ngroups) return;
+    double* sx = sm;
+    double* sy = sm + chunk;
+    double* sz = sm + 2 * chunk;
+    Slot* gslots = slots + (size_t)g * 2 * cpg;
+    int seq = 0;
+    for (int c = g; c < batch; c += ngroups, ++seq) {
+        const long long cb = (long long)c * n;
+        const int beg = r * chunk, cnt = max(0, min(n, beg + chunk) - beg);
+        __syncthreads();
+        for (int j = threadIdx.x; j < cnt; j += blockDim.x) {
+            sx[j] = px[cb + beg + j];
+            sy[j] = py[cb + beg + j];
+            sz[j] = pz[cb + beg + j];
+        }
+        double md[kFpsMaxPT];
+#pragma unroll
+        for (int t = 0; t < kFpsMaxPT; ++t) md[t] = INFINITY;
+        __syncthreads();
+        int cur = start;
+        if (r == 0 && threadIdx.x == 0) out[(long long)c * k] = start;
+        for (int it = 1; it < k; ++it) {
+            const double qx = px[cb + cur], qy = py[cb + cur], qz = pz[cb + cur];
+            double bv = -INFINITY;
+            int bi = 0x7fffffff;
+#pragma unroll
+            for (int t = 0; t < kFpsMaxPT; ++t) {
+                const int j = threadIdx.x + t * kFpsThreads;
+                if (j < cnt) {
+                    const int gi = beg + j;
+                    const double d = sq64(sx[j], sy[j], sz[j], qx, qy, qz);
+                    const double m = gi == cur ? -1.0 : fmin(md[t], d);
+                    md[t] = m;
+                    better(bv, bi, m, gi);
+                }
+            }
+            block_argmax(bv, bi, red_v, red_i);
+            const long long tag = (long long)seq * (k - 1) + it;  // group-wide iteration
+            Slot* buf = gslots + (tag & 1) * cpg;
+            if (threadIdx.x == 0) {
+                buf[r].val = bv;
+                buf[r].idx = bi;
+                __threadfence();
+                atomicAdd(arrived + g, 1ull);
+                const unsigned long long target = (unsigned long long)cpg * (unsigned long long)tag;
+                while (ld_acquire(arrived + g) < target) {
+                }
+            }
+            __syncthreads();
+            double v = -INFINITY;
+            int i = 0x7fffffff;
+            for (int b = threadIdx.x; b < cpg; b += blockDim.x)
+                better(v, i, __ldcg(&buf[b].val), __ldcg(&buf[b].idx));
+            block_argmax(v, i, red_v, red_i);
+            cur = i;
+            if (r == 0 && threadIdx.x == 0) out[(long long)c * k + it] = cur;
+        }
+    }
+}
+
 }  // namespace
 
 int fps_run(const double* d_x, const double* d_y, const double* d_z, int n, int k, int start,
@@ -473,6 +548,46 @@ int fps_run(const double* d_x, const double* d_y, const double* d_z, int n, int 
     FPH_CUDA_TRY(cudaFreeAsync(slots, stream));
     FPH_CUDA_TRY(cudaFreeAsync(arrived, stream));
     if (mind) FPH_CUDA_TRY(cudaFreeAsync(mind, stream));
+    return FPH_OK;
+}
+
+}  // namespace fph
+
+namespace fph {
+
+int fps_batched(const double* d_x, const double* d_y, const double* d_z, int batch, int n, int k,
+                int start, long long* d_out, cudaStream_t stream) {
+    if (k < 1 || k > n || start < 0 || start >= n || batch < 0) {
+        set_error("farthest point sampling: need 1 <= k <= n and 0 <= start < n");
+        return FPH_EARG;
+    }
+    if (batch == 0) return FPH_OK;
+    int dev = 0, sms = 0, max_smem = 0;
+    FPH_CUDA_TRY(cudaGetDevice(&dev));
+    FPH_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    FPH_CUDA_TRY(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    const int cap = min(kFpsThreads * kFpsMaxPT, (max_smem - 1024) / (3 * (int)sizeof(double)));
+    const int cpg = (n + cap - 1) / cap;
+    if (cpg > sms) return FPH_EARG;  // caller falls back to one cloud at a time
+    const int ngroups = min(sms / cpg, batch);
+    const int chunk = (n + cpg - 1) / cpg;
+    const size_t smem = (size_t)chunk * 3 * sizeof(double);
+    Slot* slots = nullptr;
+    unsigned long long* arrived = nullptr;
+    FPH_CUDA_TRY(cudaMallocAsync(&slots, sizeof(Slot) * 2 * cpg * ngroups, stream));
+    FPH_CUDA_TRY(cudaMallocAsync(&arrived, sizeof(unsigned long long) * ngroups, stream));
+    FPH_CUDA_TRY(cudaMemsetAsync(arrived, 0, sizeof(unsigned long long) * ngroups, stream));
+    FPH_CUDA_TRY(cudaFuncSetAttribute(fps_batched_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)smem));
+    int grid = ngroups * cpg;
+    int b = batch, nn = n, kk = k, st = start, c = cpg, ch = chunk;
+    void* args[] = {(void*)&d_x, (void*)&d_y, (void*)&d_z, (void*)&b,     (void*)&nn,      (void*)&kk,
+                    (void*)&st,  (void*)&c,   (void*)&ch,  (void*)&slots, (void*)&arrived, (void*)&d_out};
+    FPH_CUDA_TRY(cudaLaunchCooperativeKernel((void*)fps_batched_kernel, dim3(grid),
+                                             dim3(kFpsThreads), args, smem, stream));
+    FPH_CUDA_TRY(cudaGetLastError());
+    FPH_CUDA_TRY(cudaFreeAsync(slots, stream));
+    FPH_CUDA_TRY(cudaFreeAsync(arrived, stream));
     return FPH_OK;
 }
 

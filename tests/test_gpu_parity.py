@@ -46,6 +46,16 @@ def test_fps_tiled_lattice_ties():
     np.testing.assert_array_equal(got, oracle.fps(g, 150, 17))
 
 
+@pytest.mark.parametrize("batch,n,k", [(20, 100_000, 64), (7, 3_000, 200), (3, 200_000, 16)])
+def test_fps_batched_matches_oracle(batch, n, k):
+    from paper_2509_22432_b200 import farthest_point_sampling_batched
+
+    clouds = np.random.default_rng(batch * n).random((batch, n, 3))
+    got = farthest_point_sampling_batched(clouds, k, 3)
+    for b in range(batch):
+        np.testing.assert_array_equal(got[b], oracle.fps(clouds[b], k, 3))
+
+
 def test_fps_ties_uniform_grid():
     # a lattice is full of exact ties: lowest index must win every time
     g = np.stack(np.meshgrid(np.arange(40.0), np.arange(40.0), np.arange(5.0)), -1).reshape(-1, 3)
