@@ -84,6 +84,19 @@ int fph_flood_interior(const double* points, int64_t n_points, int32_t dim,
                        int32_t subset_mode, double* out_sq, int32_t memory, void* stream);
 
 /*
+ * Squared flood value of k-simplices over EXPLICIT sample points: out_sq[i]
+ * = max over the n_samples rows samples[i][*] (n_simplices x n_samples x
+ * dim float64, inside conv(simplex i)) of min over cloud points of the
+ * squared distance.  The device half of the reference's uniform-random
+ * sampler (floodph/filtration.py:303 _random_sampler_values: per simplex,
+ * its vertices plus Dirichlet samples, valued by exact nearest neighbours).
+ */
+int fph_flood_samples(const double* points, int64_t n_points, int32_t dim,
+                      const double* landmarks, int64_t n_landmarks, const int32_t* simplices,
+                      int64_t n_simplices, int32_t k, const double* samples, int32_t n_samples,
+                      int32_t subset_mode, double* out_sq, int32_t memory, void* stream);
+
+/*
  * Squared flood values of a whole Delaunay complex.
  * Replaces the msq_by_dim produced by floodph/filtration.py:233
  * _grid_values_masked (and :274 _grid_values_kdtree for external landmarks)

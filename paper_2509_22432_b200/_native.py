@@ -40,6 +40,9 @@ SIGNATURES = {
                                           ctypes.c_int64, _vp, ctypes.c_int64, ctypes.c_int32,
                                           ctypes.c_int32, ctypes.c_int32, _vp, ctypes.c_int32,
                                           _vp]),
+    "fph_flood_samples": (ctypes.c_int, [_vp, ctypes.c_int64, ctypes.c_int32, _vp, ctypes.c_int64,
+                                         _vp, ctypes.c_int64, ctypes.c_int32, _vp, ctypes.c_int32,
+                                         ctypes.c_int32, _vp, ctypes.c_int32, _vp]),
     "fph_flood_filtration": (ctypes.c_int, [_vp, ctypes.c_int64, ctypes.c_int32, _vp,
                                             ctypes.c_int64, ctypes.c_int32, _vp, _vp, _vp,
                                             ctypes.c_int32, ctypes.c_int32, _vp, ctypes.c_int32,

@@ -383,6 +383,61 @@ int fph_flood_interior(const double* points, int64_t n_points, int32_t dim,
     return rc;
 }
 
+int fph_flood_samples(const double* points, int64_t n_points, int32_t dim,
+                      const double* landmarks, int64_t n_landmarks, const int32_t* simplices,
+                      int64_t n_simplices, int32_t k, const double* samples, int32_t n_samples,
+                      int32_t subset_mode, double* out_sq, int32_t memory, void* stream) {
+    g_err[0] = 0;
+    FPH_TRY(check_cloud(points, n_points, dim));
+    if (k < 0 || k > 3 || n_samples < 1 || n_landmarks < 1) {
+        set_error("need 0 <= k <= 3, n_samples >= 1 and landmarks");
+        return FPH_EARG;
+    }
+    if (n_simplices == 0) return FPH_OK;
+    FPH_TRY(ensure_device());
+    HostCtx hc;
+    FPH_TRY(hc.init(memory, stream));
+    int rc = FPH_OK;
+    {
+        Scratch sc(hc.stream);
+        const double *d_pts, *d_lm, *d_smp;
+        const int32_t* d_s;
+        FPH_TRY(stage_in(sc, points, (size_t)n_points * dim, memory, &d_pts));
+        FPH_TRY(stage_in(sc, landmarks, (size_t)n_landmarks * dim, memory, &d_lm));
+        FPH_TRY(stage_in(sc, simplices, (size_t)n_simplices * 4, memory, &d_s));
+        const long long nrow = (long long)n_simplices * n_samples;
+        FPH_TRY(stage_in(sc, samples, (size_t)nrow * dim, memory, &d_smp));
+        double *lm3, *smp3;
+        FPH_TRY(sc.alloc(&lm3, (size_t)n_landmarks * 3));
+        FPH_TRY(sc.alloc(&smp3, (size_t)nrow * 3));
+        pad3_kernel<<<blocks_for(n_landmarks), 256, 0, hc.stream>>>(d_lm, n_landmarks, dim, lm3);
+        pad3_kernel<<<blocks_for(nrow), 256, 0, hc.stream>>>(d_smp, nrow, dim, smp3);
+        count_launches(2);
+        GridStore gs;
+        rc = grid_build(d_pts, (int)n_points, dim, 0.0, g_occupancy, hc.stream, &gs);
+        count_launches(4);
+        if (rc == FPH_OK) {
+            double* d_out = out_sq;
+            if (memory == FPH_MEM_HOST) FPH_TRY(sc.alloc(&d_out, n_simplices));
+            FloodTuning tune;
+            tune.pairs_per_task = g_pairs_per_task;
+            tune.profile = g_profile;
+            tune.algo = g_algo;
+            tune.reps_target = g_reps_target;
+            tune.team_threshold = g_team_threshold;
+            rc = flood_interior(gs.grid, lm3, d_s, (int)n_simplices, k, 1, subset_mode, d_out, tune,
+                                hc.stream, smp3, n_samples);
+            count_launches(4);
+            if (rc == FPH_OK && memory == FPH_MEM_HOST)
+                FPH_CUDA_TRY(cudaMemcpyAsync(out_sq, d_out, sizeof(double) * n_simplices,
+                                             cudaMemcpyDeviceToHost, hc.stream));
+        }
+        gs.free_all(hc.stream);
+    }
+    if (memory == FPH_MEM_HOST) FPH_CUDA_TRY(cudaStreamSynchronize(hc.stream));
+    return rc;
+}
+
 int fph_flood_filtration(const double* points, int64_t n_points, int32_t dim,
                          const double* landmarks, int64_t n_landmarks, int32_t max_dim,
                          const int64_t* counts, const int32_t* const* simplices,

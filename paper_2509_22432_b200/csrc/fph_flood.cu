@@ -233,9 +233,10 @@ __device__ __noinline__ double refine_point(const FloodArgs& a, SmemPass& S, con
 }
 
 // |b| (fp32) of point j, recomputed: the Ritter center is per simplex
-__device__ __forceinline__ float point_b(const FloodArgs& a, const Verts& V, const SimplexGeom& G, int j) {
+__device__ __forceinline__ float point_b(const FloodArgs& a, const Verts& V, const SimplexGeom& G,
+                                         int s, int j) {
     double p[3];
-    embed_row(V, a.k, a.tmpl[j], (double)a.m, p);
+    sample_row(a, V, s, j, nullptr, p);
     float fx = __double2float_rn(__dsub_rn(p[0], G.cx));
     float fy = __double2float_rn(__dsub_rn(p[1], G.cy));
     float fz = __double2float_rn(__dsub_rn(p[2], G.cz));
@@ -253,7 +254,7 @@ __device__ __noinline__ double finalize(const FloodArgs& a, SmemPass& S, int s, 
     int jmax = 0x7fffffff;
     for (int j = threadIdx.x; j < a.P; j += kThreads) {
         float v = __ldcg(m32 + j);
-        float B = point_b(a, V, G, j);
+        float B = point_b(a, V, G, s, j);
         float sv = sqrtf(fmaxf(v, 0.f)) + B;
         float E = (float)(40.0 * kU32 * 1.01) * sv * sv;
         lmax = fmax(lmax, (double)v - (double)E);
@@ -282,7 +283,7 @@ __device__ __noinline__ double finalize(const FloodArgs& a, SmemPass& S, int s, 
             float v = 0.f, E = 0.f;
             if ((pass == 0 && threadIdx.x == 0) || (pass == 1 && j < a.P && j != jm)) {
                 v = __ldcg(m32 + j);
-                float B = point_b(a, V, G, j);
+                float B = point_b(a, V, G, s, j);
                 float sv = sqrtf(fmaxf(v, 0.f)) + B;
                 E = (float)(40.0 * kU32 * 1.01) * sv * sv;
                 want = (double)v + (double)E >= (double)L && (double)v + (double)E > M;
@@ -294,12 +295,12 @@ __device__ __noinline__ double finalize(const FloodArgs& a, SmemPass& S, int s, 
             for (int t = 0; t < tot; ++t) {
                 int jj = S.list[t];
                 float vv = __ldcg(m32 + jj);
-                float B = point_b(a, V, G, jj);
+                float B = point_b(a, V, G, s, jj);
                 float sv = sqrtf(fmaxf(vv, 0.f)) + B;
                 float EE = (float)(40.0 * kU32 * 1.01) * sv * sv;
                 if ((double)vv + (double)EE <= M) continue;  // uniform across the CTA
                 double p[3];
-                embed_row(V, a.k, a.tmpl[jj], (double)a.m, p);
+                sample_row(a, V, s, jj, nullptr, p);
                 double R2 = fmax((double)vv + 2.0 * (double)EE, 0.0);
                 double R = sqrt(R2) * (1.0 + 1e-6) + 1e-300;
                 double m64 = refine_point(a, S, p, R);
@@ -350,7 +351,7 @@ __global__ void __launch_bounds__(kThreads, 2) pass_kernel(FloodArgs a, const Si
         for (int i = 0; i < PPT; ++i) {
             int jl = min(slot * PPT + i, Pc - 1);
             double p[3];
-            embed_row(V, a.k, a.tmpl[pbase + jl], (double)a.m, p);
+            sample_row(a, V, s, pbase + jl, nullptr, p);
             float fx = __double2float_rn(__dsub_rn(p[0], G.cx));
             float fy = __double2float_rn(__dsub_rn(p[1], G.cy));
             float fz = __double2float_rn(__dsub_rn(p[2], G.cz));
@@ -521,8 +522,12 @@ int flood_stats(double* out, int reset) {
 
 int flood_interior(const Grid& g, const double* d_landmarks3, const int* d_simplices, int n,
                    int k, int m, int subset, double* d_out_sq, const FloodTuning& tune,
-                   cudaStream_t stream) {
+                   cudaStream_t stream, const double* d_explicit, int explicit_rows) {
     if (n == 0) return FPH_OK;
+    if (d_explicit && explicit_rows < 1) {
+        set_error("flood_interior: explicit samples need at least one row per simplex");
+        return FPH_EARG;
+    }
     if (k < 0 || k > 3 || m < 1 || m > 255) {
         set_error("flood_interior: need 0 <= k <= 3 and 1 <= m <= 255");
         return FPH_EARG;
@@ -582,9 +587,21 @@ int flood_interior(const Grid& g, const double* d_landmarks3, const int* d_simpl
     std::vector<int> blk_off;
     for (const Blk& b : blks) {
         blk_off.push_back((int)tmpl.size());
+    if (d_explicit) {  // explicit rows: blocks of 32 consecutive samples
+        tmpl.assign(explicit_rows, make_uchar4(0, 0, 0, 0));
+        blk_off.clear();
+        for (int b = 0; b < explicit_rows; b += 32) blk_off.push_back(b);
+        blk_off.push_back(explicit_rows);
+    }
         for (int i = b.beg; i < b.end; ++i) tmpl.push_back(rows[keyed[i].second]);
     }
     blk_off.push_back((int)tmpl.size());
+    if (d_explicit) {  // explicit rows: blocks of 32 consecutive samples
+        tmpl.assign(explicit_rows, make_uchar4(0, 0, 0, 0));
+        blk_off.clear();
+        for (int b = 0; b < explicit_rows; b += 32) blk_off.push_back(b);
+        blk_off.push_back(explicit_rows);
+    }
     const int P = (int)tmpl.size();
     if (P == 0) {
         no_interior_kernel<<<(n + 255) / 256, 256, 0, stream>>>(d_out_sq, n);
@@ -604,6 +621,7 @@ int flood_interior(const Grid& g, const double* d_landmarks3, const int* d_simpl
     a.chunk_pts = kThreads * ppt;
     a.pairs_per_task = tune.pairs_per_task > 0 ? tune.pairs_per_task : (double)(1 << 21);
     a.out_sq = d_out_sq;
+    a.explicit_pts = d_explicit;
     const bool search = tune.algo == 1;
     a.nblk = search ? (int)blk_off.size() - 1 : 0;
     a.probe = tune.probe_cells * g.h;

@@ -33,6 +33,7 @@ struct FloodArgs {
     int* cand_count;          // per simplex: candidates in the Lemma-4.2 ball rows
     unsigned long long* stats;  // work counters (fph_flood_stats)
     int team_threshold;       // candidates above which a whole CTA takes the simplex
+    const double* explicit_pts;  // n x P x 3 sample rows (uniform-random sampler), or null
 };
 
 // algorithm 1 (fph_search.cu): warp-per-simplex bounded search
@@ -59,7 +60,7 @@ int choose_ppt(int P);
 // simplex (k = 0: the vertex itself), exactly as the reference computes it.
 int flood_interior(const Grid& g, const double* d_landmarks3, const int* d_simplices, int n,
                    int k, int m, int subset, double* d_out_sq, const FloodTuning& tune,
-                   cudaStream_t stream);
+                   cudaStream_t stream, const double* d_explicit = nullptr, int explicit_rows = 0);
 
 // out[i] = max(interior[i], lower[facets[i][j]] for j <= k)
 int flood_complete(const double* d_interior, const int* d_facets, int n, int k,

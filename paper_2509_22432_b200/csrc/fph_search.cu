@@ -123,7 +123,7 @@ struct PointF {
 };
 
 __device__ __forceinline__ PointF point_at(const Ctx& c, int j, double p64[3]) {
-    embed_w(c.V, c.a->k, c.a->tmpl[j], c.wt, p64);
+    sample_row(*c.a, c.V, c.s, j, c.wt, p64);
     PointF q;
     q.bx = __double2float_rn(__dsub_rn(p64[0], c.G.cx));
     q.by = __double2float_rn(__dsub_rn(p64[1], c.G.cy));

@@ -15,6 +15,8 @@ reference's outputs:
                     flood value of every simplex per dim
                     (reference: floodph/filtration.py:348 build_flood_filtration,
                      masked-batch path filtration.py:233, kdtree path :274)
+  sampler_<name>.npz  the same under the uniform-random sampler
+                    (reference: floodph/filtration.py:303 _random_sampler_values)
 
 The fixtures pin the CPU oracle (oracle/) and, through it, the CUDA path.
 """
@@ -82,6 +84,14 @@ def flood_cases():
     yield "torus10k_m20", gen_torus(10000, seed=0).points, 500, 20
 
 
+def sampler_cases():
+    rng = np.random.default_rng
+    yield "rand2d_c30", rng(13).random((400, 2)), 15, 30, 5
+    yield "rand3d_c50", rng(14).random((600, 3)), 20, 50, 1
+    ext_x = rng(15).random((300, 2))
+    yield "external2d_c20", ext_x, rng(16).random((12, 2)) * 0.8 + 0.1, 20, 2
+
+
 def main() -> None:
     _ref()
     from floodph._kernels import warm_up
@@ -97,6 +107,24 @@ def main() -> None:
             points=pts, k=k, start=start, indices=idx, ref_digest=digest,
         )
         print(f"fps_{name}: n={len(pts)} k={k}")
+    for name, pts, L, count, seed in sampler_cases():
+        cfg = FloodConfig(sampler="uniform-random", sampler_count=count, sampler_seed=seed,
+                          threads=os.cpu_count())
+        fc = build_flood_filtration(pts, L, cfg)
+        tri = fc.meta["triangulation"]
+        vm = fc.value_map()
+        payload = dict(points=pts, sampler_count=count, sampler_seed=seed, tri_points=tri.points,
+                       dim=tri.dim, landmark_mode=fc.meta["landmark_mode"], ref_digest=digest)
+        if isinstance(L, (int, np.integer)):
+            payload["n_landmarks"] = int(L)
+        else:
+            payload["landmarks"] = np.asarray(L, dtype=np.float64)
+        for d in range(tri.dim + 1):
+            rows = tri.simplices_by_dim[d]
+            payload[f"simplices_{d}"] = rows
+            payload[f"values_{d}"] = np.array([vm[tuple(int(v) for v in r)] for r in rows])
+        np.savez_compressed(os.path.join(OUT, f"sampler_{name}.npz"), **payload)
+        print(f"sampler_{name}: {tri.counts()}")
     for name, pts, L, m in flood_cases():
         t0 = time.time()
         cfg = FloodConfig(grid_resolution=m, threads=os.cpu_count())

@@ -183,3 +183,20 @@ def test_both_algorithms_golden(algo_switch, algo, reps, team, name):
     sq = flood_sq_values(z["points"], tri, int(z["grid_resolution"]), subset)
     for k, want in G.values_by_dim(z).items():
         assert np.array_equal(np.sqrt(sq[k]), want), k
+
+
+@pytest.mark.parametrize("name", G.cases("sampler"))
+def test_uniform_random_sampler_golden(name):
+    """Reference uniform-random sampler (filtration.py:303): same Philox draws
+    on the host, nearest neighbours on the GPU; values within 1e-12 relative
+    (the reference takes cKDTree's neighbour, exact up to distance ties)."""
+    z = G.load("sampler", name)
+    L = int(z["n_landmarks"]) if "n_landmarks" in z.files else z["landmarks"]
+    cfg = FloodConfig(sampler="uniform-random", sampler_count=int(z["sampler_count"]),
+                      sampler_seed=int(z["sampler_seed"]))
+    fc = build_flood_filtration(z["points"], L, cfg)
+    vm = fc.value_map()
+    assert fc.meta["landmark_mode"] == str(z["landmark_mode"])
+    for k in range(int(z["dim"]) + 1):
+        got = np.array([vm[tuple(int(v) for v in r)] for r in z[f"simplices_{k}"]])
+        np.testing.assert_allclose(got, z[f"values_{k}"], rtol=1e-12, atol=0)
