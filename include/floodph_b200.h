@@ -124,6 +124,22 @@ int fph_flood_complete(const double* interior_sq, const int32_t* facets, int64_t
                        const double* lower_sq, double* out_sq, void* stream);
 
 /*
+ * Persistence pairs of a filtered complex (host computation, no GPU needed):
+ * Z/2 column reduction with the twist / clearing optimisation.  Replaces
+ * floodph/persistence.py:89 _run_reduction (pairing as :118 reduce_and_extract).
+ *   counts[k], facets[k]  as in fph_flood_filtration (k = 0..max_dim)
+ *   order[i]               rank of simplex i, simplices concatenated by
+ *                          dimension (FilteredComplex.order)
+ *   out_pairs              (birth rank, death rank) pairs, room for
+ *                          sum(counts) pairs; n_pairs receives their number
+ * Unpaired ranks are the essential classes.  FPH_EINTEGRITY if a facet does
+ * not precede its coface.
+ */
+int fph_persistence_pairs(int32_t max_dim, const int64_t* counts, const int32_t* const* facets,
+                          const int64_t* order, int32_t clearing, int64_t* out_pairs,
+                          int64_t* n_pairs);
+
+/*
  * Tuning knobs (<= 0 keeps the default): target points per grid cell if the
  * cloud filled its bounding box, and fp32 pairs per flood task.
  */

@@ -15,7 +15,7 @@ CSRC = os.path.join(HERE, "csrc")
 LIB_DIR = os.path.join(HERE, "_lib")
 LIB_PATH = os.path.join(LIB_DIR, "libfloodph_b200.so")
 SOURCES = ["fph_api.cu", "fph_flood.cu", "fph_search.cu", "fph_fps.cu", "fph_grid.cu",
-           "fph_diag.cu"]
+           "fph_diag.cu", "fph_persistence.cpp"]
 HEADERS = ["fph_common.cuh", "fph_dev.cuh", "fph_flood.cuh", "fph_grid.cuh"]
 
 NVCC_FLAGS = [

@@ -49,6 +49,8 @@ SIGNATURES = {
                                             _vp]),
     "fph_flood_complete": (ctypes.c_int, [_vp, _vp, ctypes.c_int64, ctypes.c_int32, _vp, _vp,
                                           _vp]),
+    "fph_persistence_pairs": (ctypes.c_int, [ctypes.c_int32, _vp, _vp, _vp, ctypes.c_int32, _vp,
+                                             _vp]),
     "fph_set_tuning": (ctypes.c_int, [ctypes.c_double, ctypes.c_double]),
     "fph_set_search": (ctypes.c_int, [ctypes.c_int32, ctypes.c_int32, ctypes.c_int32]),
     "fph_set_profiling": (ctypes.c_int, [ctypes.c_int32]),

@@ -1,0 +1,96 @@
+"""Host-side pieces of the path (no GPU): Delaunay policy against the
+reference's complexes, the native persistence reduction against the Python
+one, filtration order, config validation."""
+
+import math
+
+import numpy as np
+import pytest
+
+from paper_2509_22432_b200.delaunay import circumsphere_check, delaunay
+from paper_2509_22432_b200.filtration import FilteredComplex, FloodConfig, filtration_order
+from paper_2509_22432_b200.persistence import (
+    BoundaryMatrix,
+    _pairs,
+    betti_at,
+    boundary_matrix,
+    reduce_and_extract,
+)
+from tests import _complex as C
+from tests import _golden as G
+
+
+@pytest.mark.parametrize("name", G.cases("flood"))
+def test_delaunay_matches_reference_complex(name):
+    z = G.load("flood", name)
+    if "landmark_indices" in z.files:
+        lm = z["points"][z["landmark_indices"]]
+    else:
+        lm = z["landmarks"]
+    tri = delaunay(lm)
+    np.testing.assert_array_equal(tri.points, z["tri_points"])
+    for k in range(int(z["dim"]) + 1):
+        np.testing.assert_array_equal(tri.simplices_by_dim[k], z[f"simplices_{k}"])
+
+
+def test_delaunay_square_needs_jitter():
+    tri = delaunay(np.array([[0.0, 0.0], [1.0, 0.0], [1.0, 1.0], [0.0, 1.0]]))
+    assert tri.counts() == {0: 4, 1: 5, 2: 2}
+    assert tri.jitter_applied
+    assert circumsphere_check(tri) == []
+
+
+def _flood_complex(name):
+    """A FilteredComplex of a golden case with its reference values."""
+    z = G.load("flood", name)
+    by_dim = G.simplices_by_dim(z)
+    tri = C.triangulation(z["tri_points"], by_dim)
+    values = G.values_by_dim(z)
+    simplices = [(tuple(int(v) for v in r), k, float(values[k][i]))
+                 for k in range(len(by_dim)) for i, r in enumerate(by_dim[k])]
+    order = filtration_order(values, by_dim)
+    return FilteredComplex(simplices=simplices, order=order, meta={"triangulation": tri})
+
+
+@pytest.mark.parametrize("name", ["rand2d_m6", "rand3d_m4", "circle_m64", "torus10k_m20"])
+@pytest.mark.parametrize("clearing", [True, False])
+def test_native_persistence_equals_python_reduction(name, clearing):
+    fc = _flood_complex(name)
+    bm = boundary_matrix(fc)
+    assert bm.native is not None
+    native = reduce_and_extract(bm, fc, clearing=clearing)
+    plain = FilteredComplex(fc.simplices, fc.order, meta={})
+    py = reduce_and_extract(boundary_matrix(plain), plain, clearing=clearing)
+    assert native.bars == py.bars
+
+
+def test_filtration_order_matches_reference_sort():
+    fc = _flood_complex("rand3d_m4")
+    keys = [(v, d, verts) for verts, d, v in fc.simplices]
+    ranks = sorted(range(len(keys)), key=lambda i: keys[i])
+    want = np.empty(len(keys), dtype=np.int64)
+    want[ranks] = np.arange(len(keys))
+    np.testing.assert_array_equal(fc.order, want)
+
+
+def test_reduction_hand_example():
+    # triangle boundary, vertices at 0, edges at 1, 2, 3 (reference persistence tests)
+    simplices = [((0,), 0, 0.0), ((1,), 0, 0.0), ((2,), 0, 0.0),
+                 ((0, 1), 1, 1.0), ((0, 2), 1, 2.0), ((1, 2), 1, 3.0)]
+    keys = [(v, d, s) for s, d, v in simplices]
+    ranks = sorted(range(6), key=lambda i: keys[i])
+    order = np.empty(6, dtype=np.int64)
+    order[ranks] = np.arange(6)
+    fc = FilteredComplex(simplices, order, meta={})
+    dgm = reduce_and_extract(boundary_matrix(fc), fc)
+    assert dgm.in_dim(0) == [(0.0, 1.0), (0.0, 2.0), (0.0, math.inf)]
+    assert dgm.in_dim(1) == [(3.0, math.inf)]
+    assert betti_at(dgm, 3.5, 1) == 1
+
+
+def test_config_validation():
+    for bad in (dict(grid_resolution=0), dict(batch_size=0), dict(sampler="sobol"),
+                dict(backend="gpu"), dict(threads=0), dict(max_dim=4), dict(grid_resolution=256)):
+        with pytest.raises(ValueError):
+            FloodConfig(**bad).validate()
+    FloodConfig(backend="kdtree").validate()
