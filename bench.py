@@ -151,17 +151,14 @@ class DeviceComplex:
         self.dev = torch.device(f"cuda:{device}")
         self.lm = torch.from_numpy(np.ascontiguousarray(tri.points)).to(self.dev)
         self.counts_full = [int(tri.simplices_by_dim[k].shape[0]) for k in range(self.top + 1)]
-        self.simp4 = {}
         self.facets = {}
         for k in range(1, self.top + 1):
-            s = tri.simplices_by_dim[k]
-            pad = np.full((s.shape[0], 4), -1, dtype=np.int32)
-            pad[:, : k + 1] = s
-            self.simp4[k] = torch.from_numpy(pad[rank::world].copy()).to(self.dev)
-            self.facets[k] = torch.from_numpy(np.ascontiguousarray(tri.facet_links[k], dtype=np.int32)).to(self.dev)
+            self.facets[k] = torch.from_numpy(
+                np.ascontiguousarray(tri.facet_links[k], dtype=np.int32)).to(self.dev)
         self.full_simp = {k: torch.from_numpy(np.ascontiguousarray(tri.simplices_by_dim[k], dtype=np.int32)).to(self.dev)
                           for k in range(1, self.top + 1)}
         self.counts = torch.tensor(self.counts_full, dtype=torch.int64)
+        self.vert_ids = torch.arange(self.counts_full[0], dtype=torch.int32, device=self.dev)
         self.out = [torch.empty(max(c, 1), dtype=torch.float64, device=self.dev) for c in self.counts_full]
         self.world, self.rank = world, rank
 
@@ -177,28 +174,17 @@ def step_single(lib, native, w, dc, stream):
 
 
 def step_sharded(lib, native, w, dc, stream):
-    """N > 1: interior values of this rank's interleaved shard, NCCL
-    all-gather, then facet completion (identical on every rank)."""
-    import torch
+    """N > 1: this rank's interleaved share of every dimension in one
+    fph_flood_shard call (grid built once), NCCL all-gather back into row
+    order, then facet completion on every rank."""
     import torch.distributed as dist
 
-    from paper_2509_22432_b200.parallel import gather_interleaved
+    from paper_2509_22432_b200.parallel import flood_sq_values_sharded
 
-    interiors = {}
-    for k in range(1, dc.top + 1):
-        mine = torch.empty(max(dc.simp4[k].shape[0], 1), dtype=torch.float64, device=dc.dev)
-        if dc.simp4[k].shape[0]:
-            native.check(lib.fph_flood_interior(
-                w["Xd"].data_ptr(), w["n"], w["X"].shape[1], dc.lm.data_ptr(), dc.lm.shape[0],
-                dc.simp4[k].data_ptr(), dc.simp4[k].shape[0], k, w["m"], 1, mine.data_ptr(),
-                native.FPH_MEM_DEVICE, stream))
-        interiors[k] = gather_interleaved(mine[: dc.simp4[k].shape[0]], dc.counts_full[k],
-                                          dc.world, dist)
-    dc.out[0].zero_()
-    for k in range(1, dc.top + 1):
-        native.check(lib.fph_flood_complete(
-            interiors[k].data_ptr(), dc.facets[k].data_ptr(), dc.counts_full[k], k,
-            dc.out[k - 1].data_ptr(), dc.out[k].data_ptr(), stream))
+    by_dim = {0: dc.vert_ids, **dc.full_simp}
+    vals = flood_sq_values_sharded(w["Xd"], dc.lm, by_dim, dc.facets, dc.top, w["m"], dist)
+    for k in range(dc.top + 1):
+        dc.out[k][: vals[k].shape[0]] = vals[k]
 
 
 def run_ours(args):

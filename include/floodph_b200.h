@@ -115,6 +115,20 @@ int fph_flood_filtration(const double* points, int64_t n_points, int32_t dim,
                          void* stream);
 
 /*
+ * One rank's share of a sharded fph_flood_filtration: builds the grid once
+ * and values the interior term of rows rank, rank + world, ... of every
+ * dimension 1..max_dim; out_interior[k] receives ceil((counts[k] - rank) /
+ * world) squared values in that order.  After an all-gather back into row
+ * order, fph_flood_complete folds in the facets (vertices: 0 in subset
+ * mode).  counts / simplices / out_interior tables are host arrays.
+ */
+int fph_flood_shard(const double* points, int64_t n_points, int32_t dim,
+                    const double* landmarks, int64_t n_landmarks, int32_t max_dim,
+                    const int64_t* counts, const int32_t* const* simplices, int32_t rank,
+                    int32_t world, int32_t grid_resolution, int32_t subset_mode,
+                    double* const* out_interior, int32_t memory, void* stream);
+
+/*
  * Facet completion for sharded runs (device memory only): out[i] =
  * max(interior_sq[i], lower_sq[facets[i][j]] for j <= k).  This is the
  * face-nesting identity that replaces the reference's per-cell face

@@ -47,6 +47,9 @@ SIGNATURES = {
                                             ctypes.c_int64, ctypes.c_int32, _vp, _vp, _vp,
                                             ctypes.c_int32, ctypes.c_int32, _vp, ctypes.c_int32,
                                             _vp]),
+    "fph_flood_shard": (ctypes.c_int, [_vp, ctypes.c_int64, ctypes.c_int32, _vp, ctypes.c_int64,
+                                       ctypes.c_int32, _vp, _vp, ctypes.c_int32, ctypes.c_int32,
+                                       ctypes.c_int32, ctypes.c_int32, _vp, ctypes.c_int32, _vp]),
     "fph_flood_complete": (ctypes.c_int, [_vp, _vp, ctypes.c_int64, ctypes.c_int32, _vp, _vp,
                                           _vp]),
     "fph_persistence_pairs": (ctypes.c_int, [ctypes.c_int32, _vp, _vp, _vp, ctypes.c_int32, _vp,

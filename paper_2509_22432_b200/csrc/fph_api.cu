@@ -61,6 +61,15 @@ __global__ void pad4_kernel(const int* __restrict__ s, long long n, int k, int* 
     for (int j = 0; j < 4; ++j) out[i * 4 + j] = j <= k ? s[i * (k + 1) + j] : -1;
 }
 
+// rows rank, rank + world, ... of an n x (k+1) table, padded to 4 ids
+__global__ void pad4_shard_kernel(const int* __restrict__ s, long long n_out, int k, int rank,
+                                  int world, int* __restrict__ out) {
+    long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (i >= n_out) return;
+    const long long row = rank + i * world;
+    for (int j = 0; j < 4; ++j) out[i * 4 + j] = j <= k ? s[row * (k + 1) + j] : -1;
+}
+
 __global__ void fill_kernel(double* out, long long n, double v) {
     long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     if (i < n) out[i] = v;
@@ -430,6 +439,65 @@ int fph_flood_samples(const double* points, int64_t n_points, int32_t dim,
             count_launches(4);
             if (rc == FPH_OK && memory == FPH_MEM_HOST)
                 FPH_CUDA_TRY(cudaMemcpyAsync(out_sq, d_out, sizeof(double) * n_simplices,
+                                             cudaMemcpyDeviceToHost, hc.stream));
+        }
+        gs.free_all(hc.stream);
+    }
+    if (memory == FPH_MEM_HOST) FPH_CUDA_TRY(cudaStreamSynchronize(hc.stream));
+    return rc;
+}
+
+int fph_flood_shard(const double* points, int64_t n_points, int32_t dim,
+                    const double* landmarks, int64_t n_landmarks, int32_t max_dim,
+                    const int64_t* counts, const int32_t* const* simplices, int32_t rank,
+                    int32_t world, int32_t grid_resolution, int32_t subset_mode,
+                    double* const* out_interior, int32_t memory, void* stream) {
+    g_err[0] = 0;
+    FPH_TRY(check_cloud(points, n_points, dim));
+    if (max_dim < 1 || max_dim > 3 || grid_resolution < 1 || grid_resolution > 255 ||
+        n_landmarks < 1 || !counts || world < 1 || rank < 0 || rank >= world) {
+        set_error("need 1 <= max_dim <= 3, 1 <= grid_resolution <= 255, 0 <= rank < world");
+        return FPH_EARG;
+    }
+    FPH_TRY(ensure_device());
+    HostCtx hc;
+    FPH_TRY(hc.init(memory, stream));
+    int rc = FPH_OK;
+    {
+        Scratch sc(hc.stream);
+        const double *d_pts, *d_lm;
+        FPH_TRY(stage_in(sc, points, (size_t)n_points * dim, memory, &d_pts));
+        FPH_TRY(stage_in(sc, landmarks, (size_t)n_landmarks * dim, memory, &d_lm));
+        double* lm3;
+        FPH_TRY(sc.alloc(&lm3, (size_t)n_landmarks * 3));
+        pad3_kernel<<<blocks_for(n_landmarks), 256, 0, hc.stream>>>(d_lm, n_landmarks, dim, lm3);
+        count_launches(1);
+        GridStore gs;
+        rc = grid_build(d_pts, (int)n_points, dim, 0.0, g_occupancy, hc.stream, &gs);
+        count_launches(4);
+        FloodTuning tune;
+        tune.pairs_per_task = g_pairs_per_task;
+        tune.profile = g_profile;
+        tune.algo = g_algo;
+        tune.reps_target = g_reps_target;
+        tune.team_threshold = g_team_threshold;
+        for (int k = 1; k <= max_dim && rc == FPH_OK; ++k) {
+            const long long nk = counts[k];
+            const long long mine = nk > rank ? (nk - 1 - rank) / world + 1 : 0;
+            if (mine == 0) continue;
+            const int32_t* d_s;
+            FPH_TRY(stage_in(sc, simplices[k], (size_t)nk * (k + 1), memory, &d_s));
+            int* s4;
+            FPH_TRY(sc.alloc(&s4, (size_t)mine * 4));
+            pad4_shard_kernel<<<blocks_for(mine), 256, 0, hc.stream>>>(d_s, mine, k, rank, world, s4);
+            count_launches(1);
+            double* d_out = out_interior[k];
+            if (memory == FPH_MEM_HOST) FPH_TRY(sc.alloc(&d_out, (size_t)mine));
+            rc = flood_interior(gs.grid, lm3, s4, (int)mine, k, grid_resolution, subset_mode, d_out,
+                                tune, hc.stream);
+            count_launches(4);
+            if (rc == FPH_OK && memory == FPH_MEM_HOST)
+                FPH_CUDA_TRY(cudaMemcpyAsync(out_interior[k], d_out, sizeof(double) * mine,
                                              cudaMemcpyDeviceToHost, hc.stream));
         }
         gs.free_all(hc.stream);

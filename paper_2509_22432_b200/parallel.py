@@ -42,3 +42,60 @@ def gather_interleaved(mine, n_total: int, world: int, dist):
 def shard_clouds(batch: int, world: int, rank: int) -> np.ndarray:
     """Cloud ids of a batch owned by `rank` (whole clouds, round-robin)."""
     return shard_rows(batch, world, rank)
+
+
+def shard_interior(pts, lms, by_dim, top: int, m: int, subset: bool, rank: int, world: int,
+                   stream=None):
+    """This rank's interior squared values {k: tensor} (fph_flood_shard).
+
+    pts, lms: float64 CUDA tensors (n x d, n_L x d); by_dim[k]: int32 CUDA
+    tensors (n_k x (k+1)).  Row i of the result for dim k is simplex
+    rank + i * world.
+    """
+    import torch
+
+    from . import _native
+
+    lib = _native.require_gpu()
+    dev = pts.device
+    counts = torch.tensor([by_dim[k].shape[0] for k in range(top + 1)], dtype=torch.int64)
+    outs = [None] + [torch.empty(max(len(shard_rows(int(counts[k]), world, rank)), 1),
+                                 dtype=torch.float64, device=dev) for k in range(1, top + 1)]
+    simp = [None] + [by_dim[k] for k in range(1, top + 1)]
+    s = stream if stream is not None else torch.cuda.current_stream(dev).cuda_stream
+    _native.check(lib.fph_flood_shard(
+        pts.data_ptr(), pts.shape[0], pts.shape[1], lms.data_ptr(), lms.shape[0], top,
+        counts.data_ptr(), _native.ptr_array(simp, None), rank, world, m, 1 if subset else 0,
+        _native.ptr_array(outs, None), _native.FPH_MEM_DEVICE, s))
+    return {k: outs[k][: len(shard_rows(int(counts[k]), world, rank))] for k in range(1, top + 1)}
+
+
+def complete(interior: dict, facets: dict, n0: int, top: int, subset: bool, stream=None):
+    """Facet completion on the device: {k: squared values} from the gathered
+    interior terms (vertices 0 in subset mode)."""
+    import torch
+
+    from . import _native
+
+    lib = _native.require_gpu()
+    dev = interior[1].device
+    s = stream if stream is not None else torch.cuda.current_stream(dev).cuda_stream
+    if not subset:
+        raise ValueError("sharded runs need landmarks that are cloud points")
+    out = {0: torch.zeros(n0, dtype=torch.float64, device=dev)}
+    for k in range(1, top + 1):
+        out[k] = torch.empty_like(interior[k])
+        _native.check(lib.fph_flood_complete(
+            interior[k].data_ptr(), facets[k].data_ptr(), interior[k].shape[0], k,
+            out[k - 1].data_ptr(), out[k].data_ptr(), s))
+    return out
+
+
+def flood_sq_values_sharded(pts, lms, by_dim, facets, top: int, m: int, dist, subset=True):
+    """Multi-GPU flood values: shard, all-gather (NCCL), complete on every rank."""
+    world = dist.get_world_size() if dist is not None and dist.is_initialized() else 1
+    rank = dist.get_rank() if world > 1 else 0
+    mine = shard_interior(pts, lms, by_dim, top, m, subset, rank, world)
+    interior = {k: gather_interleaved(mine[k], by_dim[k].shape[0], world, dist)
+                for k in range(1, top + 1)}
+    return complete(interior, facets, by_dim[0].shape[0], top, subset)

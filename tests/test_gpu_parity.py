@@ -200,3 +200,33 @@ def test_uniform_random_sampler_golden(name):
     for k in range(int(z["dim"]) + 1):
         got = np.array([vm[tuple(int(v) for v in r)] for r in z[f"simplices_{k}"]])
         np.testing.assert_allclose(got, z[f"values_{k}"], rtol=1e-12, atol=0)
+
+
+@pytest.mark.parametrize("world", [2, 3, 8])
+def test_sharded_values_equal_single_gpu(world):
+    """Every rank's share (computed here one rank after another on one GPU,
+    no collective) reassembled and completed equals the single-call values."""
+    import torch
+
+    from paper_2509_22432_b200.parallel import complete, shard_interior
+
+    X = gen_sphere_torus_mix(200_000, seed=3).points
+    tri = delaunay(X[farthest_point_sampling(X, 500)])
+    want = flood_sq_values(X, tri, 12, True, 3)
+    dev = torch.device("cuda:0")
+    Xd = torch.from_numpy(X).to(dev)
+    lm = torch.from_numpy(np.ascontiguousarray(tri.points)).to(dev)
+    by_dim = {k: torch.from_numpy(np.ascontiguousarray(tri.simplices_by_dim[k], dtype=np.int32)).to(dev)
+              for k in range(4)}
+    fac = {k: torch.from_numpy(np.ascontiguousarray(tri.facet_links[k], dtype=np.int32)).to(dev)
+           for k in range(1, 4)}
+    shares = [shard_interior(Xd, lm, by_dim, 3, 12, True, r, world) for r in range(world)]
+    interior = {}
+    for k in range(1, 4):
+        full = torch.empty(by_dim[k].shape[0], dtype=torch.float64, device=dev)
+        for r in range(world):
+            full[r::world] = shares[r][k]
+        interior[k] = full
+    got = complete(interior, fac, by_dim[0].shape[0], 3, True)
+    for k in range(4):
+        assert np.array_equal(got[k].cpu().numpy(), want[k]), k
