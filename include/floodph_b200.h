@@ -180,8 +180,9 @@ int fph_set_profiling(int32_t on);
  * (with profiling on); block search: [7] blocks, [8] blocks pruned whole,
  * [9] points certified in round 1, [10] points still needed after round 1,
  * [11] representative passes, [12] round-2 passes, [13..15] candidates
- * scanned in round 1 / representative / round 2, [16..18] staged likewise.
- * out must hold 24 doubles.
+ * scanned in round 1 / representative / round 2, [16..18] staged likewise,
+ * [19..22] warp-cycles spent in the bounded search's phases A, B, C and
+ * finalize.  out must hold 24 doubles.
  */
 int fph_flood_stats(double* out, int32_t reset);
 

@@ -180,4 +180,45 @@ __device__ __forceinline__ int2 row_run(const Grid& g, const Box& b, int r, doub
     return make_int2(g.cell_start[base + x0], g.cell_start[base + x1 + 1]);
 }
 
+// fp32 version for the search kernel: the same superset contract, with the
+// ball center given relative to the grid origin (one float64 subtraction per
+// region, not per row) and an absolute slack that dominates every fp32
+// rounding of the chord arithmetic.
+struct RowClipF {
+    float cx, cy, cz;  // center - grid origin
+    float R, slack;
+};
+
+__device__ __forceinline__ RowClipF make_clip_f(const Grid& g, double cx, double cy, double cz,
+                                                double R) {
+    RowClipF c;
+    const double rx = cx - g.lox, ry = cy - g.loy, rz = cz - g.loz;
+    c.cx = (float)rx;
+    c.cy = (float)ry;
+    c.cz = (float)rz;
+    c.R = (float)R;
+    c.slack = (float)(2e-5 * (fabs(rx) + fabs(ry) + fabs(rz) + R + g.h) + 1e-3 * g.h + g.margin);
+    return c;
+}
+
+__device__ __forceinline__ int2 row_run_f(const Grid& g, const Box& b, int r, const RowClipF& c) {
+    const int ny_b = b.ny_b();
+    const int iy = b.y0 + r % ny_b;
+    const int iz = b.z0 + r / ny_b;
+    const float h = (float)g.h, ih = (float)g.inv_h;
+    const float ylo = iy * h - c.slack, yhi = (iy + 1) * h + c.slack;
+    const float zlo = iz * h - c.slack, zhi = (iz + 1) * h + c.slack;
+    const float dy = fmaxf(0.f, fmaxf(ylo - c.cy, c.cy - yhi));
+    const float dz = fmaxf(0.f, fmaxf(zlo - c.cz, c.cz - zhi));
+    const float Rs = c.R + c.slack;
+    const float rem = Rs * Rs - dy * dy - dz * dz;
+    if (rem < 0.f) return make_int2(0, 0);
+    const float half = sqrtf(rem) * 1.0001f + c.slack;
+    const int x0 = max(b.x0, (int)floorf((c.cx - half) * ih));
+    const int x1 = min(b.x1, (int)floorf((c.cx + half) * ih));
+    if (x1 < x0) return make_int2(0, 0);
+    const int base = (iz * g.ny + iy) * g.nx;
+    return make_int2(g.cell_start[base + x0], g.cell_start[base + x1 + 1]);
+}
+
 }  // namespace fph

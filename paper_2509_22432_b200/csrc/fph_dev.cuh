@@ -112,6 +112,20 @@ __device__ __forceinline__ void sample_row(const FloodArgs& a, const Verts& V, i
     }
 }
 
+// sample_row for kernels that always hold the weight table (no division
+// code is emitted)
+__device__ __forceinline__ void sample_row_w(const FloodArgs& a, const Verts& V, int s, int j,
+                                             const double* wt, double p[3]) {
+    if (a.explicit_pts) {
+        const double* q = a.explicit_pts + ((size_t)s * a.P + j) * 3;
+        p[0] = q[0];
+        p[1] = q[1];
+        p[2] = q[2];
+    } else {
+        embed_w(V, a.k, a.tmpl[j], wt, p);
+    }
+}
+
 // Rigorous bound on |m32 - d^2| for the expanded fp32 distance
 // |a|^2 - 2 a.b + |b|^2 with a, b rounded once from float64 offsets to the
 // simplex center: <= 16 u (|b| + d)^2, taken with a 2.5x margin.

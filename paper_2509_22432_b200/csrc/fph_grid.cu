@@ -29,9 +29,11 @@ __host__ __device__ inline double ord2d(unsigned long long u) {
     return d;
 }
 
-// bbox[0..2] = ordered mins, bbox[3..5] = ordered maxes
+// bbox[0..2] = ordered mins, bbox[3..5] = ordered maxes (block reduction,
+// then one atomic per block and value)
 __global__ void bbox_kernel(const double* __restrict__ pts, int n, int dim,
                             unsigned long long* bbox) {
+    __shared__ double smn[3][32], smx[3][32];
     double mn[3] = {INFINITY, INFINITY, INFINITY};
     double mx[3] = {-INFINITY, -INFINITY, -INFINITY};
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
@@ -41,15 +43,27 @@ __global__ void bbox_kernel(const double* __restrict__ pts, int n, int dim,
             mx[a] = fmax(mx[a], v);
         }
     }
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31, nw = blockDim.x >> 5;
     for (int a = 0; a < dim; ++a) {
         for (int o = 16; o > 0; o >>= 1) {
             mn[a] = fmin(mn[a], __shfl_xor_sync(0xffffffffu, mn[a], o));
             mx[a] = fmax(mx[a], __shfl_xor_sync(0xffffffffu, mx[a], o));
         }
-        if ((threadIdx.x & 31) == 0) {
-            atomicMin(&bbox[a], d2ord(mn[a]));
-            atomicMax(&bbox[3 + a], d2ord(mx[a]));
+        if (l == 0) {
+            smn[a][w] = mn[a];
+            smx[a][w] = mx[a];
         }
+    }
+    __syncthreads();
+    if (threadIdx.x < dim) {
+        const int a = threadIdx.x;
+        double lo = smn[a][0], hi = smx[a][0];
+        for (int i = 1; i < nw; ++i) {
+            lo = fmin(lo, smn[a][i]);
+            hi = fmax(hi, smx[a][i]);
+        }
+        atomicMin(&bbox[a], d2ord(lo));
+        atomicMax(&bbox[3 + a], d2ord(hi));
     }
 }
 
@@ -118,7 +132,7 @@ int grid_build(const double* d_pts, int n, int dim, double cell_size, double occ
     }
     FPH_CUDA_TRY(cudaMemcpyAsync(d_bbox, init, sizeof(init), cudaMemcpyHostToDevice, stream));
     int blocks = (n + 255) / 256;
-    if (blocks > 4096) blocks = 4096;
+    if (blocks > 592) blocks = 592;
     bbox_kernel<<<blocks, 256, 0, stream>>>(d_pts, n, dim, d_bbox);
     unsigned long long hb[6];
     FPH_CUDA_TRY(cudaMemcpyAsync(hb, d_bbox, sizeof(hb), cudaMemcpyDeviceToHost, stream));

@@ -41,6 +41,12 @@ constexpr int kSThreads = 32 * kSW;
 #ifndef FPH_SEARCH_MINB
 #define FPH_SEARCH_MINB 2
 #endif
+#ifndef FPH_ROWCLIP_F32
+#define FPH_ROWCLIP_F32 1
+#endif
+#ifndef FPH_COUNT_SKIP
+#define FPH_COUNT_SKIP 0
+#endif
 constexpr int kWT = FPH_WT;     // candidates per warp tile
 constexpr int kMaxBlk = 160;    // blocks ordered best-first per simplex
 
@@ -50,6 +56,8 @@ struct WarpSmem {
     int row_off[32];
     int row_beg[32];
     float key[kMaxBlk];
+    Verts V;             // the current simplex (kept out of registers)
+    SimplexGeom G;
 };
 
 // cross-warp scratch of a CTA working on one simplex together
@@ -78,41 +86,51 @@ struct Team {
     }
     // per-lane minimum across the team's warps
     __device__ __forceinline__ float lane_min(float v) const {
-        if (size == 1) return v;
+        return size == 1 ? v : team_lane_min(ts, rank, v);
+    }
+    __device__ __forceinline__ double min_d(double v) const {  // warp-uniform v
+        return size == 1 ? v : team_min_d(ts, rank, v);
+    }
+    __device__ __forceinline__ float min_f(float v) const { return (float)min_d((double)v); }
+    __device__ __forceinline__ float max_f(float v) const { return -(float)min_d(-(double)v); }
+    __device__ __forceinline__ long long sum(long long v) const {  // warp-uniform v
+        return size == 1 ? v : team_sum(ts, rank, v);
+    }
+    // out of line: one copy each (the kernel's instruction footprint matters)
+    static __device__ __noinline__ float team_lane_min(TeamSmem* ts, int rank, float v) {
         const int lane = threadIdx.x & 31;
         __syncthreads();
         ts->f[rank][lane] = v;
         __syncthreads();
         float r = ts->f[0][lane];
-        for (int i = 1; i < size; ++i) r = fminf(r, ts->f[i][lane]);
+#pragma unroll
+        for (int i = 1; i < kSW; ++i) r = fminf(r, ts->f[i][lane]);
         return r;
     }
-    __device__ __forceinline__ double min_d(double v) const {  // warp-uniform v
-        if (size == 1) return v;
+    static __device__ __noinline__ double team_min_d(TeamSmem* ts, int rank, double v) {
         __syncthreads();
         if ((threadIdx.x & 31) == 0) ts->d[rank] = v;
         __syncthreads();
         double r = ts->d[0];
-        for (int i = 1; i < size; ++i) r = fmin(r, ts->d[i]);
+#pragma unroll
+        for (int i = 1; i < kSW; ++i) r = fmin(r, ts->d[i]);
         return r;
     }
-    __device__ __forceinline__ float min_f(float v) const { return (float)min_d((double)v); }
-    __device__ __forceinline__ float max_f(float v) const { return -(float)min_d(-(double)v); }
-    __device__ __forceinline__ long long sum(long long v) const {  // warp-uniform v
-        if (size == 1) return v;
+    static __device__ __noinline__ long long team_sum(TeamSmem* ts, int rank, long long v) {
         __syncthreads();
         if ((threadIdx.x & 31) == 0) ts->ll[rank] = v;
         __syncthreads();
         long long r = 0;
-        for (int i = 0; i < size; ++i) r += ts->ll[i];
+#pragma unroll
+        for (int i = 0; i < kSW; ++i) r += ts->ll[i];
         return r;
     }
 };
 
 struct Ctx {
     const FloodArgs* a;
-    SimplexGeom G;
-    Verts V;
+    const SimplexGeom& G;
+    const Verts& V;
     const double* wt;
     float thr;  // simplex ball (Lemma 4.2) on |a|^2; +inf when unpruned
     int s;
@@ -123,7 +141,7 @@ struct PointF {
 };
 
 __device__ __forceinline__ PointF point_at(const Ctx& c, int j, double p64[3]) {
-    sample_row(*c.a, c.V, c.s, j, c.wt, p64);
+    sample_row_w(*c.a, c.V, c.s, j, c.wt, p64);
     PointF q;
     q.bx = __double2float_rn(__dsub_rn(p64[0], c.G.cx));
     q.by = __double2float_rn(__dsub_rn(p64[1], c.G.cy));
@@ -167,7 +185,11 @@ __device__ __forceinline__ float vertex_bound(const Ctx& c, const PointF& q) {
 struct Rows {
     const Grid* g;
     Box box;
+#if FPH_ROWCLIP_F32
+    RowClipF cf;
+#else
     double qx, qy, qz, R;
+#endif
     bool clip;
 };
 
@@ -175,12 +197,16 @@ __device__ __forceinline__ Rows make_rows(const Grid& g, double qx, double qy, d
                                           double R) {
     Rows r;
     r.g = &g;
+    r.clip = R < 1e300;
+    r.box = r.clip ? ball_box(g, qx, qy, qz, R) : full_box(g);
+#if FPH_ROWCLIP_F32
+    if (r.clip) r.cf = make_clip_f(g, qx, qy, qz, R);
+#else
     r.qx = qx;
     r.qy = qy;
     r.qz = qz;
     r.R = R;
-    r.clip = R < 1e300;
-    r.box = r.clip ? ball_box(g, qx, qy, qz, R) : full_box(g);
+#endif
     return r;
 }
 
@@ -198,8 +224,20 @@ __device__ __forceinline__ Batch row_batch(const Rows& rw, WarpSmem& W, int rb) 
     const int lane = threadIdx.x & 31;
     const int rows = rw.box.rows();
     const int r = rb + lane;
-    const int2 run = r < rows ? row_run(*rw.g, rw.box, r, rw.qx, rw.qy, rw.qz, rw.R, rw.clip)
-                              : make_int2(0, 0);
+    int2 run = make_int2(0, 0);
+    if (r < rows) {
+        if (rw.clip) {
+#if FPH_ROWCLIP_F32
+            run = row_run_f(*rw.g, rw.box, r, rw.cf);
+#else
+            run = row_run(*rw.g, rw.box, r, rw.qx, rw.qy, rw.qz, rw.R, true);
+#endif
+        } else {
+            const int base = ((rw.box.z0 + r / rw.box.ny_b()) * rw.g->ny + rw.box.y0 +
+                              r % rw.box.ny_b()) * rw.g->nx;
+            run = make_int2(rw.g->cell_start[base + rw.box.x0], rw.g->cell_start[base + rw.box.x1 + 1]);
+        }
+    }
     const int len = run.y - run.x;
     int incl = len;
 #pragma unroll
@@ -471,7 +509,13 @@ __device__ void search_block(const Ctx& c, WarpSmem& W, int blk, float* vals, fl
         const Rows rw = make_rows(a.g, qx, qy, qz, Rrow);
         const int rows = rw.box.rows();
         int stride = 1;
-        if (pass == 0) {
+        // a region expected to hold few candidates (the simplex's count
+        // scaled by the area ratio, an over-estimate for volume data) skips
+        // the counting pass
+        const double frac = c.G.rho > 0.0 ? fmin(1.0, (R * R) / (c.G.rho * c.G.rho)) : 1.0;
+        const bool small = FPH_COUNT_SKIP && a.subset &&
+                           (double)a.cand_count[c.s] * frac <= 2.0 * a.reps_target;
+        if (pass == 0 && !small) {
             // count the region; a large one is sampled first to tighten U
             long long cnt = 0;
             for (int rb = tm.rank * 32; rb < rows; rb += tm.size * 32) cnt += row_batch(rw, W, rb).total;
@@ -614,6 +658,8 @@ __device__ void run_simplex(const Ctx& c, WarpSmem& W, const Team& tm) {
     float* vals = a.perpoint + (size_t)c.s * a.P;
     unsigned long long pairs = 0, staged = 0, st[3] = {0, 0, 0}, refined = 0, scanned = 0,
                        blocks = 0, pruned = 0;
+    long long clk[5];
+    clk[0] = clock64();
     // ---- A
     for (int j = tm.rank * 32 + lane; j < a.P; j += tm.size * 32)
         vals[j] = tm.size == 1 ? INFINITY : __uint_as_float(f2ord(INFINITY));
@@ -628,6 +674,9 @@ __device__ void run_simplex(const Ctx& c, WarpSmem& W, const Team& tm) {
             vals[j] = ord2f(__float_as_uint(vals[j]));
         tm.sync();
     }
+    clk[1] = clock64();
+    clk[2] = clk[1];
+    clk[3] = clk[1];
     if (stride > 1) {
         // ---- B: upper bounds; exact search of the top point
         float umax = -INFINITY;
@@ -653,6 +702,7 @@ __device__ void run_simplex(const Ctx& c, WarpSmem& W, const Team& tm) {
             const float m = point_min32(c, W, q, R, tm, scanned) + q.bb;
             L = m - err_bound(m, q.B);
         }
+        clk[2] = clock64();
         // ---- C: blocks best-first
         const int nblk = a.nblk;
         float* key = tm.size == 1 ? W.key : tm.ts->key;
@@ -698,7 +748,9 @@ __device__ void run_simplex(const Ctx& c, WarpSmem& W, const Team& tm) {
         }
     }
     tm.sync();
+    if (stride > 1) clk[3] = clock64();
     const double M = finalize_team(c, W, vals, tm, refined, scanned);
+    clk[4] = clock64();
     unsigned long long* stats = a.stats;
     if (lane == 0) {
         if (tm.rank == 0) {
@@ -715,6 +767,8 @@ __device__ void run_simplex(const Ctx& c, WarpSmem& W, const Team& tm) {
         atomicAdd(&stats[16], staged);
         atomicAdd(&stats[17], st[0]);
         atomicAdd(&stats[18], st[1]);
+        // warp-cycles per phase (A, B, C, finalize)
+        for (int i = 0; i < 4; ++i) atomicAdd(&stats[19 + i], (unsigned long long)(clk[i + 1] - clk[i]));
     }
     tm.sync();
 }
@@ -727,9 +781,6 @@ __global__ void __launch_bounds__(kSThreads, FPH_SEARCH_MINB)
     for (int i = threadIdx.x; i <= a.m; i += blockDim.x) S.wt[i] = __ddiv_rn((double)i, (double)a.m);
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     WarpSmem& W = S.w[w];
-    Ctx c;
-    c.a = &a;
-    c.wt = S.wt;
     // team mode: the whole CTA per simplex while the queue (sorted by
     // candidate count, largest first) holds big simplices
     int pending = -1;
@@ -744,10 +795,12 @@ __global__ void __launch_bounds__(kSThreads, FPH_SEARCH_MINB)
             pending = t;  // first small simplex: handed to warp 0
             break;
         }
-        c.s = s;
-        c.G = geom[s];
-        c.thr = a.subset ? (float)(c.G.rho * c.G.rho * (1.0 + 1e-5)) : INFINITY;
-        load_verts(a, s, c.V);
+        __syncwarp();
+        if (lane == 0) W.G = geom[s];
+        if (lane == 0) load_verts(a, s, W.V);
+        __syncwarp();
+        const Ctx c{&a, W.G, W.V, S.wt,
+                    a.subset ? (float)(W.G.rho * W.G.rho * (1.0 + 1e-5)) : INFINITY, s};
         const Team tm{w, kSW, &S.team};
         run_simplex(c, W, tm);
     }
@@ -763,10 +816,13 @@ __global__ void __launch_bounds__(kSThreads, FPH_SEARCH_MINB)
             t = __shfl_sync(0xffffffffu, t, 0);
         }
         if (t >= a.n) return;
-        c.s = order[t];
-        c.G = geom[c.s];
-        c.thr = a.subset ? (float)(c.G.rho * c.G.rho * (1.0 + 1e-5)) : INFINITY;
-        load_verts(a, c.s, c.V);
+        const int s = order[t];
+        __syncwarp();
+        if (lane == 0) W.G = geom[s];
+        if (lane == 0) load_verts(a, s, W.V);
+        __syncwarp();
+        const Ctx c{&a, W.G, W.V, S.wt,
+                    a.subset ? (float)(W.G.rho * W.G.rho * (1.0 + 1e-5)) : INFINITY, s};
         run_simplex(c, W, tm);
     }
 }

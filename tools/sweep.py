@@ -59,7 +59,8 @@ def main():
                           "ms": round(min(times), 3), "pass_ms": round(s[6], 3), "pairs": s[0],
                           "staged": s[1], "refined": s[3], "blocks": s[7], "pruned_blocks": s[8],
                           "team_simplices": s[9], "st_A": s[16], "st_Csample": s[17],
-                          "st_Cfull": s[18], "same": same}),
+                          "st_Cfull": s[18], "cyc_A": s[19], "cyc_B": s[20], "cyc_C": s[21],
+                          "cyc_F": s[22], "same": same}),
               flush=True)
 
 
