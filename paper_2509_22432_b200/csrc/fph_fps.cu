@@ -42,6 +42,12 @@ struct __align__(16) Slot {
     int pad;
 };
 
+// release-ordered arrival: the slot stores before it are visible to any
+// thread that acquires the counter value it produces (no full SC fence)
+__device__ __forceinline__ void arrive_release(unsigned long long* p) {
+    asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(p) : "memory");
+}
+
 __device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long* p) {
     unsigned long long v;
     asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
@@ -151,8 +157,7 @@ __global__ void __launch_bounds__(kFpsThreads, 1)
         if (threadIdx.x == 0) {
             buf[blockIdx.x].val = bv;
             buf[blockIdx.x].idx = bi;
-            __threadfence();
-            atomicAdd(arrived, 1ull);
+            arrive_release(arrived);
             const unsigned long long target = (unsigned long long)G * it;
             while (ld_acquire(arrived) < target) {
             }
@@ -186,8 +191,7 @@ __device__ __forceinline__ int grid_argmax(double bv, int bi, int it, Slot* slot
     if (threadIdx.x == 0) {
         buf[blockIdx.x].val = bv;
         buf[blockIdx.x].idx = bi;
-        __threadfence();
-        atomicAdd(arrived, 1ull);
+        arrive_release(arrived);
         const unsigned long long target = (unsigned long long)G * it;
         while (ld_acquire(arrived) < target) {
         }
@@ -481,8 +485,7 @@ __global__ void __launch_bounds__(kFpsThreads, 1)
             if (threadIdx.x == 0) {
                 buf[r].val = bv;
                 buf[r].idx = bi;
-                __threadfence();
-                atomicAdd(arrived + g, 1ull);
+                arrive_release(arrived + g);
                 const unsigned long long target = (unsigned long long)cpg * (unsigned long long)tag;
                 while (ld_acquire(arrived + g) < target) {
                 }
