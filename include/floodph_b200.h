@@ -170,6 +170,12 @@ int fph_set_tuning(double cell_occupancy, double pairs_per_task);
  */
 int fph_set_search(int32_t algo, int32_t reps_target, int32_t team_threshold);
 
+/*
+ * Bounded search: a simplex whose rows x candidates <= pairs is finished by
+ * one exact pass (phase A unsampled) instead of the bounded search.
+ */
+int fph_set_exact_pairs(double pairs);
+
 /* Time every flooding-kernel launch with CUDA events (profiling aid). */
 int fph_set_profiling(int32_t on);
 
@@ -185,6 +191,14 @@ int fph_set_profiling(int32_t on);
  * finalize.  out must hold 24 doubles.
  */
 int fph_flood_stats(double* out, int32_t reset);
+
+/*
+ * Profiling aid: enable (1) / disable (0) per-simplex capture in the
+ * bounded search; out (cap int64s) receives the last flood_interior call's
+ * 8 values per simplex (cycles of phases A, B, C, finalize; blocks
+ * searched; blocks pruned; candidates staged; team size), n their count.
+ */
+int fph_debug_simplex_cycles(int32_t enable, int64_t* out, int64_t cap, int64_t* n);
 
 /* Measured FP32 (FFMA2) throughput of the current device, TFLOP/s. */
 double fph_fp32_peak_tflops(void);

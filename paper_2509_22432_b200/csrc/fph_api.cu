@@ -23,6 +23,7 @@ static int g_algo = 1;
 static double g_probe_cells = 1.0;
 static int g_reps_target = 512;
 static int g_team_threshold = 131072;
+static double g_exact_pairs = 0.0;
 static thread_local long long g_launches = 0;
 
 void set_error(const char* fmt, ...) {
@@ -219,6 +220,11 @@ int fph_set_search(int32_t algo, int32_t reps_target, int32_t team_threshold) {
     return FPH_OK;
 }
 
+int fph_set_exact_pairs(double pairs) {
+    g_exact_pairs = pairs > 0 ? pairs : 0.0;
+    return FPH_OK;
+}
+
 int fph_set_profiling(int32_t on) {
     g_profile = on != 0;
     return FPH_OK;
@@ -235,6 +241,16 @@ double fph_fp32_peak_tflops(void) {
     int dev = 0;
     cudaGetDevice(&dev);
     return ffma2_peak_tflops(dev);
+}
+
+int fph_debug_simplex_cycles(int32_t enable, int64_t* out, int64_t cap, int64_t* n) {
+    debug_enable(enable != 0);
+    if (out && n) {
+        long long nn = 0;
+        debug_fetch(reinterpret_cast<long long*>(out), cap, &nn);
+        *n = nn;
+    }
+    return FPH_OK;
 }
 
 int64_t fph_launch_count(int32_t reset) {
@@ -379,6 +395,7 @@ int fph_flood_interior(const double* points, int64_t n_points, int32_t dim,
             tune.probe_cells = g_probe_cells;
             tune.reps_target = g_reps_target;
             tune.team_threshold = g_team_threshold;
+            tune.exact_pairs = g_exact_pairs;
             rc = flood_interior(gs.grid, lm3, d_s, (int)n_simplices, k, grid_resolution,
                                 subset_mode, d_out, tune, hc.stream);
             count_launches(4);
@@ -434,6 +451,7 @@ int fph_flood_samples(const double* points, int64_t n_points, int32_t dim,
             tune.algo = g_algo;
             tune.reps_target = g_reps_target;
             tune.team_threshold = g_team_threshold;
+            tune.exact_pairs = g_exact_pairs;
             rc = flood_interior(gs.grid, lm3, d_s, (int)n_simplices, k, 1, subset_mode, d_out, tune,
                                 hc.stream, smp3, n_samples);
             count_launches(4);
@@ -481,6 +499,7 @@ int fph_flood_shard(const double* points, int64_t n_points, int32_t dim,
         tune.algo = g_algo;
         tune.reps_target = g_reps_target;
         tune.team_threshold = g_team_threshold;
+            tune.exact_pairs = g_exact_pairs;
         for (int k = 1; k <= max_dim && rc == FPH_OK; ++k) {
             const long long nk = counts[k];
             const long long mine = nk > rank ? (nk - 1 - rank) / world + 1 : 0;
@@ -542,6 +561,7 @@ int fph_flood_filtration(const double* points, int64_t n_points, int32_t dim,
         tune.probe_cells = g_probe_cells;
         tune.reps_target = g_reps_target;
         tune.team_threshold = g_team_threshold;
+            tune.exact_pairs = g_exact_pairs;
         double* d_vals[4] = {nullptr, nullptr, nullptr, nullptr};
         for (int k = 0; k <= max_dim && rc == FPH_OK; ++k) {
             const long long nk = counts[k];

@@ -520,6 +520,15 @@ int flood_stats(double* out, int reset) {
     return FPH_OK;
 }
 
+static bool g_debug = false;
+static std::vector<long long> g_debug_buf;
+void debug_enable(bool on) { g_debug = on; }
+int debug_fetch(long long* out, long long cap, long long* n) {
+    *n = (long long)g_debug_buf.size();
+    std::copy(g_debug_buf.begin(), g_debug_buf.begin() + std::min<long long>(cap, *n), out);
+    return FPH_OK;
+}
+
 int flood_interior(const Grid& g, const double* d_landmarks3, const int* d_simplices, int n,
                    int k, int m, int subset, double* d_out_sq, const FloodTuning& tune,
                    cudaStream_t stream, const double* d_explicit, int explicit_rows) {
@@ -627,6 +636,7 @@ int flood_interior(const Grid& g, const double* d_landmarks3, const int* d_simpl
     a.probe = tune.probe_cells * g.h;
     a.reps_target = tune.reps_target > 0 ? tune.reps_target : 384;
     a.team_threshold = tune.team_threshold > 0 ? tune.team_threshold : 131072;
+    a.exact_pairs = tune.exact_pairs;
     int* d_blk = nullptr;
 
     uchar4* d_tmpl = nullptr;
@@ -676,8 +686,21 @@ int flood_interior(const Grid& g, const double* d_landmarks3, const int* d_simpl
     }
     FPH_CUDA_TRY(cudaGetDevice(&dev));
     FPH_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    long long* d_dbg = nullptr;
+    if (search && g_debug) {
+        FPH_CUDA_TRY(cudaMallocAsync(&d_dbg, sizeof(long long) * 8 * n, stream));
+        FPH_CUDA_TRY(cudaMemsetAsync(d_dbg, 0, sizeof(long long) * 8 * n, stream));
+    }
+    a.dbg = d_dbg;
     if (search) {
         FPH_TRY(launch_search(a, d_geom, a.cand_count, stream));
+        if (d_dbg) {
+            g_debug_buf.assign((size_t)8 * n, 0);
+            FPH_CUDA_TRY(cudaMemcpyAsync(g_debug_buf.data(), d_dbg, sizeof(long long) * 8 * n,
+                                         cudaMemcpyDeviceToHost, stream));
+            FPH_CUDA_TRY(cudaStreamSynchronize(stream));
+            FPH_CUDA_TRY(cudaFreeAsync(d_dbg, stream));
+        }
     } else switch (ppt) {
 #define FPH_LAUNCH(PPTV)                                                                     \
     case PPTV:                                                                               \

@@ -34,7 +34,13 @@ struct FloodArgs {
     unsigned long long* stats;  // work counters (fph_flood_stats)
     int team_threshold;       // candidates above which a whole CTA takes the simplex
     const double* explicit_pts;  // n x P x 3 sample rows (uniform-random sampler), or null
+    long long* dbg;           // optional: per simplex 8 values (phase cycles, counters)
+    double exact_pairs;       // bounded search: one exact pass when rows x candidates <= this
 };
+
+// debug capture of the last flood_interior call (per-simplex phase cycles)
+void debug_enable(bool on);
+int debug_fetch(long long* out, long long cap, long long* n);
 
 // algorithm 1 (fph_search.cu): warp-per-simplex bounded search
 int launch_search(const FloodArgs& a, const SimplexGeom* d_geom, const int* d_cand,
@@ -47,6 +53,7 @@ struct FloodTuning {
     double probe_cells = 1.0;     // block search: first-round margin in grid cells
     int reps_target = 384;        // block search: candidates per representative pass
     int team_threshold = 131072;  // bounded search: CTA-cooperative simplices above this
+    double exact_pairs = 0.0;     // bounded search: exact pass below this many pairs
 };
 
 // out[0..5]: work counters (see g_stats), out[6]: pass-kernel ms

@@ -665,7 +665,10 @@ __device__ void run_simplex(const Ctx& c, WarpSmem& W, const Team& tm) {
         vals[j] = tm.size == 1 ? INFINITY : __uint_as_float(f2ord(INFINITY));
     tm.sync();
     const long long C = a.cand_count[c.s];
-    const int stride = (int)max(1ll, (C + a.reps_target - 1) / a.reps_target);
+    // small enough for one exact pass (every row x every candidate), else a
+    // sample of ~reps_target candidates
+    const bool exact = (double)C * (double)a.P <= a.exact_pairs;
+    const int stride = exact ? 1 : (int)max(1ll, (C + a.reps_target - 1) / a.reps_target);
     reps_pass(c, W, stride, vals, tm, pairs, staged);
     tm.sync();
     if (tm.size > 1) {  // decode the ordered minima
@@ -769,6 +772,14 @@ __device__ void run_simplex(const Ctx& c, WarpSmem& W, const Team& tm) {
         atomicAdd(&stats[18], st[1]);
         // warp-cycles per phase (A, B, C, finalize)
         for (int i = 0; i < 4; ++i) atomicAdd(&stats[19 + i], (unsigned long long)(clk[i + 1] - clk[i]));
+        if (a.dbg && tm.rank == 0) {
+            long long* d = a.dbg + (size_t)c.s * 8;
+            for (int i = 0; i < 4; ++i) d[i] = clk[i + 1] - clk[i];
+            d[4] = (long long)blocks;
+            d[5] = (long long)pruned;
+            d[6] = (long long)(staged + st[0] + st[1]);
+            d[7] = tm.size;
+        }
     }
     tm.sync();
 }

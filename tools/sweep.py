@@ -31,8 +31,11 @@ def main():
     stream = torch.cuda.current_stream().cuda_stream
     ref = None
     stats = np.zeros(24)
-    for algo, reps, team, occ in settings:
+    for st in settings:
+        algo, reps, team, occ = st[:4]
+        exact = st[4] if len(st) > 4 else 0
         _native.check(lib.fph_set_search(algo, reps, team))
+        lib.fph_set_exact_pairs(float(exact))
         lib.fph_set_tuning(occ, 0.0)
         step_single(lib, _native, w, dc, stream)
         torch.cuda.synchronize()
@@ -55,7 +58,7 @@ def main():
         else:
             same = all(np.array_equal(a, b) for a, b in zip(ref, vals))
         s = stats / 3
-        print(json.dumps({"algo": algo, "reps": reps, "team": team, "occ": occ,
+        print(json.dumps({"algo": algo, "reps": reps, "team": team, "occ": occ, "exact": exact,
                           "ms": round(min(times), 3), "pass_ms": round(s[6], 3), "pairs": s[0],
                           "staged": s[1], "refined": s[3], "blocks": s[7], "pruned_blocks": s[8],
                           "team_simplices": s[9], "st_A": s[16], "st_Csample": s[17],
