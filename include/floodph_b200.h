@@ -163,7 +163,9 @@ int fph_set_tuning(double cell_occupancy, double pairs_per_task);
  * Flooding algorithm: 1 (default) bounded search -- per simplex, sampled
  * upper bounds, an exact lower bound, and exact search of only the point
  * blocks that can still hold the maximum; 0 brute force over every point of
- * the Lemma-4.2 ball.  Both are exact (identical values).
+ * the Lemma-4.2 ball; 2 bounded search with its sampling pass run by the
+ * brute-force CTA kernel (measured slower on configs[1]; kept for study).
+ * All are exact (identical values).
  * reps_target: candidates per representative (sampling) pass;
  * team_threshold: simplices with more candidates are searched by a whole
  * CTA instead of one warp.  <= 0 keeps the defaults (512, 131072).
@@ -172,7 +174,8 @@ int fph_set_search(int32_t algo, int32_t reps_target, int32_t team_threshold);
 
 /*
  * Bounded search: a simplex whose rows x candidates <= pairs is finished by
- * one exact pass (phase A unsampled) instead of the bounded search.
+ * one exact pass (phase A unsampled) instead of the bounded search
+ * (default 262144; negative restores the default).
  */
 int fph_set_exact_pairs(double pairs);
 

@@ -23,7 +23,7 @@ static int g_algo = 1;
 static double g_probe_cells = 1.0;
 static int g_reps_target = 512;
 static int g_team_threshold = 131072;
-static double g_exact_pairs = 0.0;
+static double g_exact_pairs = 262144.0;
 static thread_local long long g_launches = 0;
 
 void set_error(const char* fmt, ...) {
@@ -210,8 +210,8 @@ int fph_flood_complete(const double* interior_sq, const int32_t* facets, int64_t
 }
 
 int fph_set_search(int32_t algo, int32_t reps_target, int32_t team_threshold) {
-    if (algo != 0 && algo != 1) {
-        set_error("algo must be 0 (brute force) or 1 (bounded search)");
+    if (algo < 0 || algo > 2) {
+        set_error("algo must be 0 (brute force), 1 (bounded search) or 2 (split bounded search)");
         return FPH_EARG;
     }
     g_algo = algo;
@@ -221,7 +221,7 @@ int fph_set_search(int32_t algo, int32_t reps_target, int32_t team_threshold) {
 }
 
 int fph_set_exact_pairs(double pairs) {
-    g_exact_pairs = pairs > 0 ? pairs : 0.0;
+    g_exact_pairs = pairs >= 0 ? pairs : 262144.0;
     return FPH_OK;
 }
 

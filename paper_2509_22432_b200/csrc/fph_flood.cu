@@ -137,7 +137,13 @@ __global__ void setup_kernel(FloodArgs a, SimplexGeom* __restrict__ geom,
     for (int o = 16; o > 0; o >>= 1) cand += __shfl_xor_sync(0xffffffffu, cand, o);
     int npc = (a.P + a.chunk_pts - 1) / a.chunk_pts;
     int pc = min(a.P, a.chunk_pts);
-    double pairs = (double)pc * (double)cand;
+    // bounded search (split): simplices small enough are valued exactly by
+    // the pass kernel; the others get a stride-s sample of ~reps_target
+    int stride = 1;
+    if (a.split && (double)cand * (double)a.P > a.exact_pairs)
+        stride = (int)max(1ll, (cand + a.reps_target - 1) / a.reps_target);
+    G.stride = stride;
+    double pairs = (double)pc * (double)((cand + stride - 1) / stride);
     int nrp = (int)fmin(fmax(1.0, ceil(pairs / a.pairs_per_task)), (double)max(rows, 1));
     G.nrp = nrp;
     G.npc = npc;
@@ -363,6 +369,7 @@ __global__ void __launch_bounds__(kThreads, 2) pass_kernel(FloodArgs a, const Si
         }
         const float thr = a.subset ? (float)(G.rho * G.rho * (1.0 + 1e-5)) : INFINITY;
         int tile_n = 0;
+        long long fbase = 0;
         unsigned long long n_staged = 0, n_scanned = 0;
         for (int rb = row_lo; rb < row_hi; rb += kThreads) {
             int r = rb + threadIdx.x;
@@ -375,11 +382,17 @@ __global__ void __launch_bounds__(kThreads, 2) pass_kernel(FloodArgs a, const Si
             __syncthreads();
             const int nrow = min(kThreads, row_hi - rb);
             n_scanned += total;
-            for (int f0 = 0; f0 < total; f0 += kThreads) {
-                int f = f0 + threadIdx.x;
+            // stride > 1: only every stride-th enumerated candidate (phase A
+            // sample of the bounded search; any subset gives valid bounds)
+            const int stride = G.stride;
+            const int first = (int)((stride - fbase % stride) % stride);
+            const int nsel = total > first ? (total - first - 1) / stride + 1 : 0;
+            fbase += total;
+            for (int f0 = 0; f0 < nsel; f0 += kThreads) {
+                int f = first + (f0 + (int)threadIdx.x) * stride;
                 bool keep = false;
                 float ax = 0.f, ay = 0.f, az = 0.f, aw = 0.f;
-                if (f < total) {
+                if (f0 + (int)threadIdx.x < nsel) {
                     int l = 0, h = nrow;
                     while (h - l > 1) {
                         int mid = (l + h) >> 1;
@@ -447,6 +460,7 @@ __global__ void __launch_bounds__(kThreads, 2) pass_kernel(FloodArgs a, const Si
             __threadfence();
             __syncthreads();
         }
+        if (G.stride > 1) continue;  // bounds only: the search kernel takes it from here
         double M = finalize(a, S, s, V, G);
         if (threadIdx.x == 0) a.out_sq[s] = M;
         __syncthreads();
@@ -631,12 +645,13 @@ int flood_interior(const Grid& g, const double* d_landmarks3, const int* d_simpl
     a.pairs_per_task = tune.pairs_per_task > 0 ? tune.pairs_per_task : (double)(1 << 21);
     a.out_sq = d_out_sq;
     a.explicit_pts = d_explicit;
-    const bool search = tune.algo == 1;
+    const bool search = tune.algo >= 1;
     a.nblk = search ? (int)blk_off.size() - 1 : 0;
     a.probe = tune.probe_cells * g.h;
     a.reps_target = tune.reps_target > 0 ? tune.reps_target : 384;
     a.team_threshold = tune.team_threshold > 0 ? tune.team_threshold : 131072;
     a.exact_pairs = tune.exact_pairs;
+    a.split = tune.algo == 2 ? 1 : 0;
     int* d_blk = nullptr;
 
     uchar4* d_tmpl = nullptr;
@@ -656,7 +671,7 @@ int flood_interior(const Grid& g, const double* d_landmarks3, const int* d_simpl
     FPH_CUDA_TRY(cudaMemsetAsync(d_done, 0, sizeof(int) * n, stream));
     FPH_CUDA_TRY(cudaMemsetAsync(d_ntasks + n, 0, sizeof(int), stream));
     long long npp = (long long)n * P;
-    if (!search)
+    if (!search || a.split)
         init_perpoint_kernel<<<(unsigned)((npp + 255) / 256), 256, 0, stream>>>(
             reinterpret_cast<unsigned*>(d_perpoint), npp);
     FPH_CUDA_TRY(cudaMallocAsync(&d_blk, sizeof(int) * blk_off.size(), stream));
@@ -692,6 +707,25 @@ int flood_interior(const Grid& g, const double* d_landmarks3, const int* d_simpl
         FPH_CUDA_TRY(cudaMemsetAsync(d_dbg, 0, sizeof(long long) * 8 * n, stream));
     }
     a.dbg = d_dbg;
+    if (search && a.split) {
+        // phase A of every simplex (exact ones finished) in the CTA pass
+        // kernel, then phases B, C, F of the sampled ones
+        switch (ppt) {
+#define FPH_LAUNCH_A(PPTV)                                                                   \
+    case PPTV:                                                                               \
+        FPH_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pass_kernel<PPTV>,  \
+                                                                   kThreads, 0));            \
+        pass_kernel<PPTV><<<sms * (occ > 0 ? occ : 1), kThreads, 0, stream>>>(               \
+            a, d_geom, d_task_off, d_counter, d_done);                                       \
+        break;
+            FPH_LAUNCH_A(1)
+            FPH_LAUNCH_A(2)
+            FPH_LAUNCH_A(4)
+            FPH_LAUNCH_A(8)
+#undef FPH_LAUNCH_A
+        }
+        FPH_CUDA_TRY(cudaGetLastError());
+    }
     if (search) {
         FPH_TRY(launch_search(a, d_geom, a.cand_count, stream));
         if (d_dbg) {

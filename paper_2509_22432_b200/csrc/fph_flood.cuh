@@ -12,6 +12,7 @@ struct SimplexGeom {
     Box box;            // candidate cell box
     int npc;            // point chunks
     int nrp;            // row parts (candidate splits)
+    int stride;         // phase A sampling stride (1: exact pass, finalised by pass_kernel)
 };
 
 struct FloodArgs {
@@ -36,6 +37,7 @@ struct FloodArgs {
     const double* explicit_pts;  // n x P x 3 sample rows (uniform-random sampler), or null
     long long* dbg;           // optional: per simplex 8 values (phase cycles, counters)
     double exact_pairs;       // bounded search: one exact pass when rows x candidates <= this
+    int split;                // 1: pass_kernel runs phase A of the bounded search for every simplex
 };
 
 // debug capture of the last flood_interior call (per-simplex phase cycles)

@@ -660,22 +660,25 @@ __device__ void run_simplex(const Ctx& c, WarpSmem& W, const Team& tm) {
                        blocks = 0, pruned = 0;
     long long clk[5];
     clk[0] = clock64();
-    // ---- A
-    for (int j = tm.rank * 32 + lane; j < a.P; j += tm.size * 32)
-        vals[j] = tm.size == 1 ? INFINITY : __uint_as_float(f2ord(INFINITY));
-    tm.sync();
-    const long long C = a.cand_count[c.s];
-    // small enough for one exact pass (every row x every candidate), else a
-    // sample of ~reps_target candidates
-    const bool exact = (double)C * (double)a.P <= a.exact_pairs;
-    const int stride = exact ? 1 : (int)max(1ll, (C + a.reps_target - 1) / a.reps_target);
-    reps_pass(c, W, stride, vals, tm, pairs, staged);
-    tm.sync();
-    if (tm.size > 1) {  // decode the ordered minima
-        __threadfence_block();
+    // ---- A (done by pass_kernel in split mode: vals hold the sample minima)
+    int stride = c.G.stride;
+    if (!a.split) {
         for (int j = tm.rank * 32 + lane; j < a.P; j += tm.size * 32)
-            vals[j] = ord2f(__float_as_uint(vals[j]));
+            vals[j] = tm.size == 1 ? INFINITY : __uint_as_float(f2ord(INFINITY));
         tm.sync();
+        const long long C = a.cand_count[c.s];
+        // small enough for one exact pass (every row x every candidate), else a
+        // sample of ~reps_target candidates
+        const bool exact = (double)C * (double)a.P <= a.exact_pairs;
+        stride = exact ? 1 : (int)max(1ll, (C + a.reps_target - 1) / a.reps_target);
+        reps_pass(c, W, stride, vals, tm, pairs, staged);
+        tm.sync();
+        if (tm.size > 1) {  // decode the ordered minima
+            __threadfence_block();
+            for (int j = tm.rank * 32 + lane; j < a.P; j += tm.size * 32)
+                vals[j] = ord2f(__float_as_uint(vals[j]));
+            tm.sync();
+        }
     }
     clk[1] = clock64();
     clk[2] = clk[1];
@@ -802,6 +805,7 @@ __global__ void __launch_bounds__(kSThreads, FPH_SEARCH_MINB)
         const int t = S.team.t;
         if (t >= a.n) return;
         const int s = order[t];
+        if (a.split && geom[s].stride == 1) continue;  // finished by the pass kernel
         if (a.cand_count[s] <= a.team_threshold) {
             pending = t;  // first small simplex: handed to warp 0
             break;
@@ -828,6 +832,7 @@ __global__ void __launch_bounds__(kSThreads, FPH_SEARCH_MINB)
         }
         if (t >= a.n) return;
         const int s = order[t];
+        if (a.split && geom[s].stride == 1) continue;
         __syncwarp();
         if (lane == 0) W.G = geom[s];
         if (lane == 0) load_verts(a, s, W.V);

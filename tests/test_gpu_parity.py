@@ -172,7 +172,8 @@ def test_block_search_equals_brute_force_full_size(algo_switch, reps, team):
         assert np.array_equal(brute[k], search[k]), k
 
 
-@pytest.mark.parametrize("algo,reps,team", [(0, 0, 0), (1, 0, 0), (1, 16, 1), (1, 16, 2**30)])
+@pytest.mark.parametrize("algo,reps,team", [(0, 0, 0), (1, 0, 0), (1, 16, 1), (1, 16, 2**30),
+                                            (2, 0, 0), (2, 16, 1)])
 @pytest.mark.parametrize("name", ["torus10k_m20", "rand3d_m30", "external2d", "circle_m64",
                                   "dup3d_m5"])
 def test_both_algorithms_golden(algo_switch, algo, reps, team, name):

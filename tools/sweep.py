@@ -33,7 +33,7 @@ def main():
     stats = np.zeros(24)
     for st in settings:
         algo, reps, team, occ = st[:4]
-        exact = st[4] if len(st) > 4 else 0
+        exact = st[4] if len(st) > 4 else -1
         _native.check(lib.fph_set_search(algo, reps, team))
         lib.fph_set_exact_pairs(float(exact))
         lib.fph_set_tuning(occ, 0.0)
