@@ -179,6 +179,9 @@ int fph_set_search(int32_t algo, int32_t reps_target, int32_t team_threshold);
  */
 int fph_set_exact_pairs(double pairs);
 
+/* ... and k-simplices with at most `candidates` candidates (0: off). */
+int fph_set_exact_candidates(int32_t k, int64_t candidates);
+
 /* Time every flooding-kernel launch with CUDA events (profiling aid). */
 int fph_set_profiling(int32_t on);
 

@@ -57,6 +57,7 @@ SIGNATURES = {
     "fph_set_tuning": (ctypes.c_int, [ctypes.c_double, ctypes.c_double]),
     "fph_set_search": (ctypes.c_int, [ctypes.c_int32, ctypes.c_int32, ctypes.c_int32]),
     "fph_set_exact_pairs": (ctypes.c_int, [ctypes.c_double]),
+    "fph_set_exact_candidates": (ctypes.c_int, [ctypes.c_int32, ctypes.c_int64]),
     "fph_set_profiling": (ctypes.c_int, [ctypes.c_int32]),
     "fph_flood_stats": (ctypes.c_int, [_vp, ctypes.c_int32]),
     "fph_debug_simplex_cycles": (ctypes.c_int, [ctypes.c_int32, _vp, ctypes.c_int64, _vp]),

@@ -24,6 +24,7 @@ static double g_probe_cells = 1.0;
 static int g_reps_target = 512;
 static int g_team_threshold = 131072;
 static double g_exact_pairs = 262144.0;
+static long long g_exact_cand[4] = {0, 0, 2500, 0};
 static thread_local long long g_launches = 0;
 
 void set_error(const char* fmt, ...) {
@@ -225,6 +226,15 @@ int fph_set_exact_pairs(double pairs) {
     return FPH_OK;
 }
 
+int fph_set_exact_candidates(int32_t k, int64_t candidates) {
+    if (k < 0 || k > 3) {
+        set_error("k must be in [0, 3]");
+        return FPH_EARG;
+    }
+    g_exact_cand[k] = candidates > 0 ? candidates : 0;
+    return FPH_OK;
+}
+
 int fph_set_profiling(int32_t on) {
     g_profile = on != 0;
     return FPH_OK;
@@ -396,6 +406,7 @@ int fph_flood_interior(const double* points, int64_t n_points, int32_t dim,
             tune.reps_target = g_reps_target;
             tune.team_threshold = g_team_threshold;
             tune.exact_pairs = g_exact_pairs;
+            for (int i = 0; i < 4; ++i) tune.exact_cand[i] = g_exact_cand[i];
             rc = flood_interior(gs.grid, lm3, d_s, (int)n_simplices, k, grid_resolution,
                                 subset_mode, d_out, tune, hc.stream);
             count_launches(4);
@@ -452,6 +463,7 @@ int fph_flood_samples(const double* points, int64_t n_points, int32_t dim,
             tune.reps_target = g_reps_target;
             tune.team_threshold = g_team_threshold;
             tune.exact_pairs = g_exact_pairs;
+            for (int i = 0; i < 4; ++i) tune.exact_cand[i] = g_exact_cand[i];
             rc = flood_interior(gs.grid, lm3, d_s, (int)n_simplices, k, 1, subset_mode, d_out, tune,
                                 hc.stream, smp3, n_samples);
             count_launches(4);
@@ -500,6 +512,7 @@ int fph_flood_shard(const double* points, int64_t n_points, int32_t dim,
         tune.reps_target = g_reps_target;
         tune.team_threshold = g_team_threshold;
             tune.exact_pairs = g_exact_pairs;
+            for (int i = 0; i < 4; ++i) tune.exact_cand[i] = g_exact_cand[i];
         for (int k = 1; k <= max_dim && rc == FPH_OK; ++k) {
             const long long nk = counts[k];
             const long long mine = nk > rank ? (nk - 1 - rank) / world + 1 : 0;
@@ -562,6 +575,7 @@ int fph_flood_filtration(const double* points, int64_t n_points, int32_t dim,
         tune.reps_target = g_reps_target;
         tune.team_threshold = g_team_threshold;
             tune.exact_pairs = g_exact_pairs;
+            for (int i = 0; i < 4; ++i) tune.exact_cand[i] = g_exact_cand[i];
         double* d_vals[4] = {nullptr, nullptr, nullptr, nullptr};
         for (int k = 0; k <= max_dim && rc == FPH_OK; ++k) {
             const long long nk = counts[k];

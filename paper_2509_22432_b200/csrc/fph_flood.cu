@@ -140,7 +140,7 @@ __global__ void setup_kernel(FloodArgs a, SimplexGeom* __restrict__ geom,
     // bounded search (split): simplices small enough are valued exactly by
     // the pass kernel; the others get a stride-s sample of ~reps_target
     int stride = 1;
-    if (a.split && (double)cand * (double)a.P > a.exact_pairs)
+    if (a.split && (double)cand * (double)a.P > a.exact_pairs && cand > a.exact_cand[a.k])
         stride = (int)max(1ll, (cand + a.reps_target - 1) / a.reps_target);
     G.stride = stride;
     double pairs = (double)pc * (double)((cand + stride - 1) / stride);
@@ -651,6 +651,7 @@ int flood_interior(const Grid& g, const double* d_landmarks3, const int* d_simpl
     a.reps_target = tune.reps_target > 0 ? tune.reps_target : 384;
     a.team_threshold = tune.team_threshold > 0 ? tune.team_threshold : 131072;
     a.exact_pairs = tune.exact_pairs;
+    for (int i = 0; i < 4; ++i) a.exact_cand[i] = tune.exact_cand[i];
     a.split = tune.algo == 2 ? 1 : 0;
     int* d_blk = nullptr;
 

@@ -38,6 +38,7 @@ struct FloodArgs {
     long long* dbg;           // optional: per simplex 8 values (phase cycles, counters)
     double exact_pairs;       // bounded search: one exact pass when rows x candidates <= this
     int split;                // 1: pass_kernel runs phase A of the bounded search for every simplex
+    long long exact_cand[4];  // bounded search: exact pass when candidates <= this, per dim
 };
 
 // debug capture of the last flood_interior call (per-simplex phase cycles)
@@ -56,6 +57,7 @@ struct FloodTuning {
     int reps_target = 384;        // block search: candidates per representative pass
     int team_threshold = 131072;  // bounded search: CTA-cooperative simplices above this
     double exact_pairs = 0.0;     // bounded search: exact pass below this many pairs
+    long long exact_cand[4] = {0, 0, 0, 0};  // ... or below this many candidates (per dim)
 };
 
 // out[0..5]: work counters (see g_stats), out[6]: pass-kernel ms

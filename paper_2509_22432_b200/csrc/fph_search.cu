@@ -669,7 +669,7 @@ __device__ void run_simplex(const Ctx& c, WarpSmem& W, const Team& tm) {
         const long long C = a.cand_count[c.s];
         // small enough for one exact pass (every row x every candidate), else a
         // sample of ~reps_target candidates
-        const bool exact = (double)C * (double)a.P <= a.exact_pairs;
+        const bool exact = (double)C * (double)a.P <= a.exact_pairs || C <= a.exact_cand[a.k];
         stride = exact ? 1 : (int)max(1ll, (C + a.reps_target - 1) / a.reps_target);
         reps_pass(c, W, stride, vals, tm, pairs, staged);
         tm.sync();

@@ -34,6 +34,9 @@ def main():
     for st in settings:
         algo, reps, team, occ = st[:4]
         exact = st[4] if len(st) > 4 else -1
+        ecand = st[5] if len(st) > 5 else [0, 0, 0, 0]
+        for kk in range(4):
+            lib.fph_set_exact_candidates(kk, int(ecand[kk]))
         _native.check(lib.fph_set_search(algo, reps, team))
         lib.fph_set_exact_pairs(float(exact))
         lib.fph_set_tuning(occ, 0.0)
@@ -58,7 +61,7 @@ def main():
         else:
             same = all(np.array_equal(a, b) for a, b in zip(ref, vals))
         s = stats / 3
-        print(json.dumps({"algo": algo, "reps": reps, "team": team, "occ": occ, "exact": exact,
+        print(json.dumps({"algo": algo, "reps": reps, "team": team, "occ": occ, "exact": exact, "ecand": ecand,
                           "ms": round(min(times), 3), "pass_ms": round(s[6], 3), "pairs": s[0],
                           "staged": s[1], "refined": s[3], "blocks": s[7], "pruned_blocks": s[8],
                           "team_simplices": s[9], "st_A": s[16], "st_Csample": s[17],
