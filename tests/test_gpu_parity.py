@@ -231,3 +231,82 @@ def test_sharded_values_equal_single_gpu(world):
     got = complete(interior, fac, by_dim[0].shape[0], 3, True)
     for k in range(4):
         assert np.array_equal(got[k].cpu().numpy(), want[k]), k
+
+
+# ------------------------------------------------------------- edge cases
+def test_empty_and_tiny_inputs():
+    from paper_2509_22432_b200 import _native
+
+    lib = _native.require_gpu()
+    X = np.random.default_rng(0).random((50, 3))
+    lm = X[:5].copy()
+    # zero simplices: nothing to do, success
+    out = np.empty(1)
+    _native.check(lib.fph_flood_interior(_native.ptr(X), 50, 3, _native.ptr(lm), 5,
+                                         _native.ptr(np.zeros((1, 4), np.int32)), 0, 2, 8, 1,
+                                         _native.ptr(out), _native.FPH_MEM_HOST, None))
+    # single-point cloud FPS, k = 1
+    np.testing.assert_array_equal(farthest_point_sampling(np.array([[0.5, 0.5]]), 1, 0), [0])
+    with pytest.raises(ValueError):
+        farthest_point_sampling(np.array([[0.5, 0.5]]), 2, 0)
+
+
+@pytest.mark.parametrize("m", [1, 2, 3])
+def test_low_resolution_has_no_interior_rows(m):
+    """m <= k: a k-simplex has no interior rows; its value comes from its
+    facets alone (reference: grid = vertices and edge points only)."""
+    z = G.load("flood", "rand3d_m1") if m == 1 else G.load("flood", "rand3d_m2")
+    X = z["points"]
+    tri = C.triangulation(z["tri_points"], G.simplices_by_dim(z))
+    sq = flood_sq_values(X, tri, m, True)
+    want = oracle.flood_values(X, tri.points, tri.simplices_by_dim, m)
+    for k in range(4):
+        assert np.array_equal(sq[k], want[k])
+
+
+def test_planar_cloud_full_size_sampled_oracle():
+    """2-D cloud (z = 0 internally): 500k noisy circle-annulus points."""
+    rng = np.random.default_rng(3)
+    th = rng.uniform(0, 2 * np.pi, 500_000)
+    r = 1.0 + 0.02 * rng.normal(size=th.size)
+    X = np.c_[r * np.cos(th), r * np.sin(th)]
+    tri = delaunay(X[farthest_point_sampling(X, 300)])
+    sq = flood_sq_values(X, tri, 16, True)
+    rows = np.random.default_rng(1).choice(tri.simplices_by_dim[2].shape[0], 40, replace=False)
+    sub = C.sub_complex(tri.simplices_by_dim, rows, 2)
+    want = oracle.flood_values(X, tri.points, sub, 16, top_dim=2)
+    for k in (1, 2):
+        index = {tuple(rw): i for i, rw in enumerate(tri.simplices_by_dim[k].tolist())}
+        got = np.array([sq[k][index[tuple(rw)]] for rw in sub[k].tolist()])
+        assert np.array_equal(got, want[k])
+
+
+def test_duplicate_points_and_landmarks():
+    """Duplicates in the cloud; FPS beyond the distinct count picks
+    duplicates (value 0 rows); Delaunay drops duplicate landmarks."""
+    rng = np.random.default_rng(5)
+    base = rng.random((200, 3))
+    X = np.vstack([base, base])
+    idx = farthest_point_sampling(X, 300)
+    np.testing.assert_array_equal(idx, oracle.fps(X, 300))
+    fc = build_flood_filtration(X, 250, FloodConfig(grid_resolution=4))
+    tri = fc.meta["triangulation"]
+    assert tri.dedup_dropped.size == 50
+    want = oracle.flood_values(X, tri.points, tri.simplices_by_dim, 4)
+    vm = fc.value_map()
+    for k in range(4):
+        got = np.array([vm[tuple(int(v) for v in r)] for r in tri.simplices_by_dim[k]])
+        assert np.array_equal(got, np.sqrt(want[k]))
+
+
+def test_max_resolution_and_bad_arguments():
+    z = G.load("flood", "rand2d_m6")
+    tri = C.triangulation(z["tri_points"], G.simplices_by_dim(z))
+    sq = flood_sq_values(z["points"], tri, 255, True)
+    want = oracle.flood_values(z["points"], tri.points, tri.simplices_by_dim, 255)
+    for k in range(3):
+        assert np.array_equal(sq[k], want[k])
+    with pytest.raises(ValueError):
+        flood_sq_values(z["points"], tri, 256, True)
+    with pytest.raises(ValueError):
+        flood_sq_values(z["points"], tri, 0, True)
