@@ -130,9 +130,26 @@ __global__ void setup_kernel(FloodArgs a, SimplexGeom* __restrict__ geom,
     G.box = b;
     int rows = b.rows();
     long long cand = 0;
-    for (int rr = lane; rr < rows; rr += 32) {
-        int2 run = row_run(a.g, b, rr, c[0], c[1], c[2], G.rho, a.subset != 0);
-        cand += run.y - run.x;
+    if (a.nblk > 0) {
+        // bounded search: the count only steers sampling and scheduling, so
+        // an estimate suffices -- fp32 row clipping, every `step`-th row
+        const int step = rows > 512 ? 4 : (rows > 128 ? 2 : 1);
+        const RowClipF cf = make_clip_f(a.g, c[0], c[1], c[2], G.rho);
+        for (int rr = lane * step; rr < rows; rr += 32 * step) {
+            int2 run;
+            if (a.subset) {
+                run = row_run_f(a.g, b, rr, cf);
+            } else {
+                const int base = ((b.z0 + rr / b.ny_b()) * a.g.ny + b.y0 + rr % b.ny_b()) * a.g.nx;
+                run = make_int2(a.g.cell_start[base + b.x0], a.g.cell_start[base + b.x1 + 1]);
+            }
+            cand += (long long)(run.y - run.x) * step;
+        }
+    } else {
+        for (int rr = lane; rr < rows; rr += 32) {
+            int2 run = row_run(a.g, b, rr, c[0], c[1], c[2], G.rho, a.subset != 0);
+            cand += run.y - run.x;
+        }
     }
     for (int o = 16; o > 0; o >>= 1) cand += __shfl_xor_sync(0xffffffffu, cand, o);
     int npc = (a.P + a.chunk_pts - 1) / a.chunk_pts;

@@ -6,7 +6,8 @@
 // cloud is binned once into a uniform grid: points are radix-sorted by
 // linear cell id (x fastest) and stored as float64 SoA, so every (y, z) row
 // of a ball's cell box is ONE contiguous run of points -- coalesced loads and
-// a two-lookup range query per row.
+// a two-lookup range query per row.  Binning is a counting sort (histogram,
+// scan, scatter): cell_start is the scan itself.
 #include <cub/cub.cuh>
 
 #include <cmath>
@@ -67,37 +68,35 @@ __global__ void bbox_kernel(const double* __restrict__ pts, int n, int dim,
     }
 }
 
+// cell id per point + histogram (counting sort pass 1)
 __global__ void cell_id_kernel(const double* __restrict__ pts, int n, int dim, Grid g,
-                               int* __restrict__ keys, int* __restrict__ vals) {
+                               int* __restrict__ keys, int* __restrict__ counts) {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const double* p = pts + (size_t)i * dim;
     int ix = cell_coord(p[0], g.lox, g.inv_h, g.nx);
     int iy = cell_coord(p[1], g.loy, g.inv_h, g.ny);
     int iz = dim == 3 ? cell_coord(p[2], g.loz, g.inv_h, g.nz) : 0;
-    keys[i] = (iz * g.ny + iy) * g.nx + ix;
-    vals[i] = i;
+    const int key = (iz * g.ny + iy) * g.nx + ix;
+    keys[i] = key;
+    atomicAdd(counts + key, 1);
 }
 
-__global__ void gather_kernel(const double* __restrict__ pts, int n, int dim,
-                              const int* __restrict__ perm, double* __restrict__ x,
-                              double* __restrict__ y, double* __restrict__ z) {
+// counting sort pass 3: each point to its cell's next free slot.  The order
+// inside a cell is arbitrary -- nothing downstream depends on it (minima are
+// order-free, the float64 refine is exact).
+__global__ void scatter_kernel(const double* __restrict__ pts, int n, int dim,
+                               const int* __restrict__ keys, const int* __restrict__ cell_start,
+                               int* __restrict__ cursor, double* __restrict__ x,
+                               double* __restrict__ y, double* __restrict__ z) {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
-    const double* p = pts + (size_t)perm[i] * dim;
-    x[i] = p[0];
-    y[i] = p[1];
-    z[i] = dim == 3 ? p[2] : 0.0;
-}
-
-// cell_start[c] = first sorted position with key >= c, for c in [0, ncells]
-__global__ void cell_start_kernel(const int* __restrict__ keys, int n, int ncells,
-                                  int* __restrict__ cell_start) {
-    int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i > n) return;
-    int prev = i == 0 ? -1 : keys[i - 1];
-    int cur = i == n ? ncells : keys[i];
-    for (int c = prev + 1; c <= cur; ++c) cell_start[c] = i;
+    const int key = keys[i];
+    const int pos = cell_start[key] + atomicAdd(cursor + key, 1);
+    const double* p = pts + (size_t)i * dim;
+    x[pos] = p[0];
+    y[pos] = p[1];
+    z[pos] = dim == 3 ? p[2] : 0.0;
 }
 
 }  // namespace
@@ -172,33 +171,30 @@ int grid_build(const double* d_pts, int n, int dim, double cell_size, double occ
     long long ncells = (long long)g.nx * g.ny * g.nz;
 
     gs->free_all(stream);
-    int *keys = nullptr, *vals = nullptr, *keys2 = nullptr, *perm = nullptr;
+    int *keys = nullptr, *counts = nullptr, *cursor = nullptr;
     FPH_CUDA_TRY(cudaMallocAsync(&keys, sizeof(int) * n, stream));
-    FPH_CUDA_TRY(cudaMallocAsync(&vals, sizeof(int) * n, stream));
-    FPH_CUDA_TRY(cudaMallocAsync(&keys2, sizeof(int) * n, stream));
-    FPH_CUDA_TRY(cudaMallocAsync(&perm, sizeof(int) * n, stream));
+    FPH_CUDA_TRY(cudaMallocAsync(&counts, sizeof(int) * (ncells + 1), stream));
+    FPH_CUDA_TRY(cudaMallocAsync(&cursor, sizeof(int) * ncells, stream));
     FPH_CUDA_TRY(cudaMallocAsync(&gs->x, sizeof(double) * n, stream));
     FPH_CUDA_TRY(cudaMallocAsync(&gs->y, sizeof(double) * n, stream));
     FPH_CUDA_TRY(cudaMallocAsync(&gs->z, sizeof(double) * n, stream));
     FPH_CUDA_TRY(cudaMallocAsync(&gs->cell_start, sizeof(int) * (ncells + 1), stream));
-    cell_id_kernel<<<(n + 255) / 256, 256, 0, stream>>>(d_pts, n, dim, g, keys, vals);
-    int end_bit = 1;
-    while ((1ll << end_bit) < ncells && end_bit < 31) ++end_bit;
+    FPH_CUDA_TRY(cudaMemsetAsync(counts, 0, sizeof(int) * (ncells + 1), stream));
+    FPH_CUDA_TRY(cudaMemsetAsync(cursor, 0, sizeof(int) * ncells, stream));
+    cell_id_kernel<<<(n + 255) / 256, 256, 0, stream>>>(d_pts, n, dim, g, keys, counts);
     size_t tmp_bytes = 0;
-    cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, keys, keys2, vals, perm, n, 0, end_bit,
-                                    stream);
+    cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, counts, gs->cell_start, ncells + 1, stream);
     void* tmp = nullptr;
     FPH_CUDA_TRY(cudaMallocAsync(&tmp, tmp_bytes, stream));
-    FPH_CUDA_TRY(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, keys, keys2, vals, perm, n, 0,
-                                                 end_bit, stream));
-    gather_kernel<<<(n + 255) / 256, 256, 0, stream>>>(d_pts, n, dim, perm, gs->x, gs->y, gs->z);
-    cell_start_kernel<<<(n + 256) / 256, 256, 0, stream>>>(keys2, n, (int)ncells, gs->cell_start);
+    FPH_CUDA_TRY(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, counts, gs->cell_start, ncells + 1,
+                                               stream));
+    scatter_kernel<<<(n + 255) / 256, 256, 0, stream>>>(d_pts, n, dim, keys, gs->cell_start, cursor,
+                                                        gs->x, gs->y, gs->z);
     FPH_CUDA_TRY(cudaGetLastError());
     FPH_CUDA_TRY(cudaFreeAsync(tmp, stream));
     FPH_CUDA_TRY(cudaFreeAsync(keys, stream));
-    FPH_CUDA_TRY(cudaFreeAsync(vals, stream));
-    FPH_CUDA_TRY(cudaFreeAsync(keys2, stream));
-    FPH_CUDA_TRY(cudaFreeAsync(perm, stream));
+    FPH_CUDA_TRY(cudaFreeAsync(counts, stream));
+    FPH_CUDA_TRY(cudaFreeAsync(cursor, stream));
     g.x = gs->x;
     g.y = gs->y;
     g.z = gs->z;

@@ -863,11 +863,13 @@ int launch_search(const FloodArgs& a, const SimplexGeom* d_geom, const int* d_ca
     FPH_CUDA_TRY(cudaMemsetAsync(d_counter, 0, sizeof(int), stream));
     size_t tmp_bytes = 0;
     cub::DeviceRadixSort::SortPairsDescending(nullptr, tmp_bytes, d_cand, d_keys, d_iota, d_order,
-                                              a.n, 0, 31, stream);
+                                              a.n, 0, 24, stream);
     void* tmp = nullptr;
     FPH_CUDA_TRY(cudaMallocAsync(&tmp, tmp_bytes, stream));
+    // 24 key bits: counts above 2^24 only need to sort among themselves
+    // loosely (scheduling order, not correctness)
     FPH_CUDA_TRY(cub::DeviceRadixSort::SortPairsDescending(tmp, tmp_bytes, d_cand, d_keys, d_iota,
-                                                           d_order, a.n, 0, 31, stream));
+                                                           d_order, a.n, 0, 24, stream));
     int dev = 0, sms = 0, occ = 0;
     FPH_CUDA_TRY(cudaGetDevice(&dev));
     FPH_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
