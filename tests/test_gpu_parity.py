@@ -310,3 +310,51 @@ def test_max_resolution_and_bad_arguments():
         flood_sq_values(z["points"], tri, 256, True)
     with pytest.raises(ValueError):
         flood_sq_values(z["points"], tri, 0, True)
+
+
+# ------------------------------------------------- pipeline acceptance
+def test_circle_golden_diagram():
+    """Reference acceptance criterion 1 (Appendix circle example): 4096
+    uniform-angle circle points, 12 FPS landmarks, m = 64: H0 deaths
+    1 - cos(pi/16) x 8 and 1 - cos(pi/8) x 3 plus one essential bar; one H1
+    bar (1 - cos(pi/8), 1); tolerance 2e-3."""
+    import math
+
+    from paper_2509_22432_b200 import flood_diagram
+    from paper_2509_22432_b200.datagen import gen_circle
+
+    dgm, fc = flood_diagram(gen_circle(4096), 12, FloodConfig(grid_resolution=64))
+    short, long_ = 1 - math.cos(math.pi / 16), 1 - math.cos(math.pi / 8)
+    h0 = dgm.in_dim(0)
+    deaths = [d for _, d in h0]
+    assert len(h0) == 12 and all(b == 0.0 for b, _ in h0)
+    assert sum(abs(d - short) < 2e-3 for d in deaths) == 8
+    assert sum(abs(d - long_) < 2e-3 for d in deaths) == 3
+    assert sum(math.isinf(d) for d in deaths) == 1
+    h1 = dgm.in_dim(1)
+    assert len(h1) == 1 and abs(h1[0][0] - long_) < 2e-3 and abs(h1[0][1] - 1.0) < 2e-3
+
+
+def test_torus_topology_and_reference_diagram():
+    """configs[0] (10k torus points, 500 landmarks, m = 20): the diagram
+    equals the one computed from the reference's own values (golden), and
+    the torus shows Betti (1, 2, 1) at a mid radius."""
+    from paper_2509_22432_b200 import flood_diagram
+    from paper_2509_22432_b200.persistence import betti_at
+
+    z = G.load("flood", "torus10k_m20")
+    dgm, fc = flood_diagram(z["points"], 500, FloodConfig(grid_resolution=20))
+    # rebuild the complex with the reference values: same diagram
+    from paper_2509_22432_b200.filtration import FilteredComplex, filtration_order
+    from paper_2509_22432_b200.persistence import boundary_matrix, reduce_and_extract
+
+    vals = G.values_by_dim(z)
+    by_dim = G.simplices_by_dim(z)
+    simplices = [(tuple(int(v) for v in r), k, float(vals[k][i]))
+                 for k in range(4) for i, r in enumerate(by_dim[k])]
+    ref_fc = FilteredComplex(simplices, filtration_order(vals, by_dim),
+                             meta={"triangulation": fc.meta["triangulation"]})
+    ref_dgm = reduce_and_extract(boundary_matrix(ref_fc), ref_fc)
+    assert dgm.bars == ref_dgm.bars
+    r = 0.3
+    assert (betti_at(dgm, r, 0), betti_at(dgm, r, 1), betti_at(dgm, r, 2)) == (1, 2, 1)
