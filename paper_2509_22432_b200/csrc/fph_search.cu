@@ -364,13 +364,52 @@ __device__ void fold_all(const Ctx& c, WarpSmem& W, int n, float* vals, const Te
     const int lane = threadIdx.x & 31;
     tile_pad(W, n);
     const int P = c.a->P;
-    for (int j0 = 0; j0 < P; j0 += 32) {
-        const int j = j0 + lane;
-        if (j < P) {
-            const PointF q = point_at(c, j);
-            const float v = tile_min(W, n, q, INFINITY) + q.bb;
-            if (tm.size == 1) vals[j] = fminf(vals[j], v);
-            else atomicMin(reinterpret_cast<unsigned*>(vals) + j, f2ord(v));
+    const int np = (n + 1) >> 1;
+    // two points per lane: each tile read serves 64 points
+    for (int j0 = 0; j0 < P; j0 += 64) {
+        const int ja = j0 + lane, jb = j0 + 32 + lane;
+        const PointF qa = point_at(c, min(ja, P - 1));
+        const PointF qb = point_at(c, min(jb, P - 1));
+        float ba0 = INFINITY, ba1 = INFINITY, bb0 = INFINITY, bb1 = INFINITY;
+        int p = 0;
+        for (; p + 1 < np; p += 2) {
+            const float4 A0 = W.tA[p], B0 = W.tB[p], A1 = W.tA[p + 1], B1 = W.tB[p + 1];
+            float2 u0 = ffma2(make_float2(qa.pz2, qa.pz2), make_float2(B0.x, B0.y), make_float2(B0.z, B0.w));
+            float2 v0 = ffma2(make_float2(qb.pz2, qb.pz2), make_float2(B0.x, B0.y), make_float2(B0.z, B0.w));
+            float2 u1 = ffma2(make_float2(qa.pz2, qa.pz2), make_float2(B1.x, B1.y), make_float2(B1.z, B1.w));
+            float2 v1 = ffma2(make_float2(qb.pz2, qb.pz2), make_float2(B1.x, B1.y), make_float2(B1.z, B1.w));
+            u0 = ffma2(make_float2(qa.py2, qa.py2), make_float2(A0.z, A0.w), u0);
+            v0 = ffma2(make_float2(qb.py2, qb.py2), make_float2(A0.z, A0.w), v0);
+            u1 = ffma2(make_float2(qa.py2, qa.py2), make_float2(A1.z, A1.w), u1);
+            v1 = ffma2(make_float2(qb.py2, qb.py2), make_float2(A1.z, A1.w), v1);
+            u0 = ffma2(make_float2(qa.px2, qa.px2), make_float2(A0.x, A0.y), u0);
+            v0 = ffma2(make_float2(qb.px2, qb.px2), make_float2(A0.x, A0.y), v0);
+            u1 = ffma2(make_float2(qa.px2, qa.px2), make_float2(A1.x, A1.y), u1);
+            v1 = ffma2(make_float2(qb.px2, qb.px2), make_float2(A1.x, A1.y), v1);
+            ba0 = fmin3(ba0, u0.x, u0.y);
+            bb0 = fmin3(bb0, v0.x, v0.y);
+            ba1 = fmin3(ba1, u1.x, u1.y);
+            bb1 = fmin3(bb1, v1.x, v1.y);
+        }
+        if (p < np) {
+            const float4 A0 = W.tA[p], B0 = W.tB[p];
+            float2 u0 = ffma2(make_float2(qa.pz2, qa.pz2), make_float2(B0.x, B0.y), make_float2(B0.z, B0.w));
+            float2 v0 = ffma2(make_float2(qb.pz2, qb.pz2), make_float2(B0.x, B0.y), make_float2(B0.z, B0.w));
+            u0 = ffma2(make_float2(qa.py2, qa.py2), make_float2(A0.z, A0.w), u0);
+            v0 = ffma2(make_float2(qb.py2, qb.py2), make_float2(A0.z, A0.w), v0);
+            u0 = ffma2(make_float2(qa.px2, qa.px2), make_float2(A0.x, A0.y), u0);
+            v0 = ffma2(make_float2(qb.px2, qb.px2), make_float2(A0.x, A0.y), v0);
+            ba0 = fmin3(ba0, u0.x, u0.y);
+            bb0 = fmin3(bb0, v0.x, v0.y);
+        }
+        const float va = fminf(ba0, ba1) + qa.bb, vb = fminf(bb0, bb1) + qb.bb;
+        if (ja < P) {
+            if (tm.size == 1) vals[ja] = fminf(vals[ja], va);
+            else atomicMin(reinterpret_cast<unsigned*>(vals) + ja, f2ord(va));
+        }
+        if (jb < P) {
+            if (tm.size == 1) vals[jb] = fminf(vals[jb], vb);
+            else atomicMin(reinterpret_cast<unsigned*>(vals) + jb, f2ord(vb));
         }
     }
     pairs += (unsigned long long)n * P;
