@@ -6,9 +6,12 @@
  *   FPH_MEM_HOST    all array arguments are host pointers; the call copies
  *                   them to the GPU, runs, copies results back and returns
  *                   when they are ready (the drop-in for the CPU reference);
- *   FPH_MEM_DEVICE  all array arguments are device pointers on the current
- *                   CUDA device; work is ordered on `stream` (a cudaStream_t,
- *                   NULL = legacy default stream).
+ *   FPH_MEM_DEVICE  all data arrays (coordinates, simplices, facets, values,
+ *                   indices) are device pointers on the current CUDA device;
+ *                   work is ordered on `stream` (a cudaStream_t, NULL =
+ *                   legacy default stream).  `counts` and the per-dimension
+ *                   pointer tables (simplices[k], facets[k], out_sq[k]) are
+ *                   always host arrays (their entries follow `memory`).
  * Return value: FPH_OK (0) or an FPH_E* code; fph_last_error() describes the
  * most recent failure of the calling thread.  Argument errors (FPH_EARG)
  * correspond to the reference's ValueError, FPH_EINTEGRITY to IntegrityError.
