@@ -358,3 +358,36 @@ def test_torus_topology_and_reference_diagram():
     assert dgm.bars == ref_dgm.bars
     r = 0.3
     assert (betti_at(dgm, r, 0), betti_at(dgm, r, 1), betti_at(dgm, r, 2)) == (1, 2, 1)
+
+
+# ------------------------------------------------- adversarial numerics
+@pytest.mark.parametrize("scale,offset", [(1.0, 1e4), (1e-6, 0.0), (1e6, 3e6), (1.0, -7.5e2)])
+def test_scaled_and_offset_clouds(algo_switch, scale, offset):
+    """The fp32 filter works on float64 offsets to each simplex's center;
+    its error bound must hold at any scale / offset (values stay bitwise
+    the reference's)."""
+    base = gen_sphere_torus_mix(40_000, seed=11).points
+    X = base * scale + offset
+    tri = delaunay(X[farthest_point_sampling(X, 150)])
+    want = oracle.flood_values(X, tri.points, {k: tri.simplices_by_dim[k] for k in range(3)}, 10,
+                               top_dim=2)
+    for algo in (0, 1):
+        algo_switch(algo)
+        got = flood_sq_values(X, tri, 10, True, 2)
+        for k in range(3):
+            assert np.array_equal(got[k], want[k]), (algo, k)
+
+
+def test_near_ties_lattice_cloud(algo_switch):
+    """A jittered lattice: many candidates at nearly equal distances from
+    sample points, where the fp32 minimum and the float64 minimum can pick
+    different points; the refine must still return the float64 value."""
+    g = np.stack(np.meshgrid(np.arange(30.0), np.arange(30.0), np.arange(30.0)), -1).reshape(-1, 3)
+    X = g + np.random.default_rng(2).normal(scale=1e-7, size=g.shape)
+    tri = delaunay(X[farthest_point_sampling(X, 120)])
+    want = oracle.flood_values(X, tri.points, tri.simplices_by_dim, 6)
+    for algo in (0, 1):
+        algo_switch(algo)
+        got = flood_sq_values(X, tri, 6, True)
+        for k in range(4):
+            assert np.array_equal(got[k], want[k]), (algo, k)
