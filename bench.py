@@ -311,7 +311,9 @@ def roofline(lib, stats, step_ms, steps, clocks, brute_pairs=None):
     achieved = 6.0 * pairs / sec / 1e12 if pass_ms > 0 else 0.0
     peak = float(lib.fph_fp32_peak_tflops())
     out = {"bound": "fp32", "kernel": "search_kernel", "achieved": achieved, "peak": peak,
-           "unit": "TFLOP/s", "frac": achieved / peak if peak else None, "traffic": None,
+           "unit": "TFLOP/s", "frac": achieved / peak if peak else None, "traffic": _traffic(),
+           "traffic_note": "dram__bytes_read.sum + dram__bytes_write.sum per step over the flooding "
+                           "kernel's launches, from profiles/r01/ncu_search_full_final.json",
            "peak_source": "measured FFMA2 microbenchmark on this GPU (fph_fp32_peak_tflops); "
                           "MEASURED_PEAKS.json has no FP32 figure",
            "kernel_ms_per_step": pass_ms / steps, "kernel_share_of_step": pass_ms / steps / step_ms}
@@ -319,6 +321,19 @@ def roofline(lib, stats, step_ms, steps, clocks, brute_pairs=None):
         out["reference_algorithm_pairs_per_step"] = brute_pairs
         out["effective_tflops_vs_reference_algorithm"] = 6.0 * brute_pairs / (sec / steps) / 1e12
     return out
+
+
+def _traffic():
+    """DRAM bytes (read + write) per step of the flooding kernel's launches,
+    from the committed `ncu --set full` capture of this bench command
+    (profiles/r01/ncu_search_full_final.json); None if it is absent."""
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01",
+                        "ncu_search_full_final.json")
+    try:
+        with open(path) as fh:
+            return float(json.load(fh)["dram_bytes_per_step"])
+    except (OSError, KeyError, ValueError):
+        return None
 
 
 def brute_pairs(lib, native, w, dc, stream):
