@@ -565,6 +565,7 @@ __device__ void search_block(const Ctx& c, WarpSmem& W, int blk, float* vals, fl
             int tile_n = 0;
             long long fbase = 0;
             unsigned long long stg = 0;
+            const unsigned act = __ballot_sync(0xffffffffu, active);
             auto take = [&](bool keep, float ax, float ay, float az, float aw) {
                 tile_n = tile_push(W, tile_n, keep, ax, ay, az, aw);
                 if (tile_n > kWT - 32) {
@@ -619,6 +620,8 @@ __device__ void search_block(const Ctx& c, WarpSmem& W, int blk, float* vals, fl
             }
             st[pass] += stg;
             st[2] += stg * (unsigned long long)nb;
+            st[3 + 2 * pass] += stg * (unsigned long long)__popc(act);
+            st[4 + 2 * pass] += stg * (unsigned long long)nb;
             best = tm.lane_min(best);
         }
         if (pass == 0) {
@@ -695,7 +698,7 @@ __device__ void run_simplex(const Ctx& c, WarpSmem& W, const Team& tm) {
     const int lane = threadIdx.x & 31;
     const FloodArgs& a = *c.a;
     float* vals = a.perpoint + (size_t)c.s * a.P;
-    unsigned long long pairs = 0, staged = 0, st[3] = {0, 0, 0}, refined = 0, scanned = 0,
+    unsigned long long pairs = 0, staged = 0, st[7] = {0, 0, 0, 0, 0, 0, 0}, refined = 0, scanned = 0,
                        blocks = 0, pruned = 0;
     long long clk[5];
     clk[0] = clock64();
@@ -748,33 +751,42 @@ __device__ void run_simplex(const Ctx& c, WarpSmem& W, const Team& tm) {
             L = m - err_bound(m, q.B);
         }
         clk[2] = clock64();
-        // ---- C: blocks best-first
+        // ---- C: blocks best-first (in order when there are too many to rank);
+        // one call site, so search_block is inlined once
         const int nblk = a.nblk;
+        const bool ranked = nblk <= kMaxBlk;
         float* key = tm.size == 1 ? W.key : tm.ts->key;
-        if (nblk <= kMaxBlk) {
+        if (ranked) {
             for (int b = tm.rank * 32 + lane; b < nblk; b += tm.size * 32) {
                 float k2 = -INFINITY;
                 for (int i = a.blk_off[b]; i < a.blk_off[b + 1]; ++i) k2 = fmaxf(k2, vals[i]);
                 key[b] = k2;
             }
             tm.sync();
-            for (;;) {
+        }
+        for (int seq = 0;; ++seq) {
+            int b = seq;
+            if (ranked) {
                 float kb = -INFINITY;
                 int bb = 0x7fffffff;
-                for (int b = lane; b < nblk; b += 32)
-                    if (key[b] > kb) {
-                        kb = key[b];
-                        bb = b;
+                for (int i = lane; i < nblk; i += 32)
+                    if (key[i] > kb) {
+                        kb = key[i];
+                        bb = i;
                     }
                 const float km = warp_max(kb);
                 if (!(km >= L)) break;  // every remaining block is below L
-                const int b = __reduce_min_sync(0xffffffffu, kb == km ? bb : 0x7fffffff);
+                b = __reduce_min_sync(0xffffffffu, kb == km ? bb : 0x7fffffff);
                 tm.sync();
                 if (tm.rank == 0 && lane == 0) key[b] = -INFINITY;
                 tm.sync();
-                search_block(c, W, b, vals, L, tm, st);
-                ++blocks;
+            } else if (seq >= nblk) {
+                break;
             }
+            search_block(c, W, b, vals, L, tm, st);
+            ++blocks;
+        }
+        if (ranked) {
             // blocks never searched cannot reach L
             for (int b = 0; b < nblk; ++b) {
                 if (key[b] > -INFINITY) {
@@ -785,11 +797,6 @@ __device__ void run_simplex(const Ctx& c, WarpSmem& W, const Team& tm) {
                 }
             }
             tm.sync();
-        } else {
-            for (int b = 0; b < nblk; ++b) {
-                search_block(c, W, b, vals, L, tm, st);
-                ++blocks;
-            }
         }
     }
     tm.sync();
@@ -812,6 +819,9 @@ __device__ void run_simplex(const Ctx& c, WarpSmem& W, const Team& tm) {
         atomicAdd(&stats[16], staged);
         atomicAdd(&stats[17], st[0]);
         atomicAdd(&stats[18], st[1]);
+        // useful (active-lane) vs executed pairs per phase-C pass; phase-A pairs
+        for (int i = 0; i < 4; ++i) atomicAdd(&stats[10 + i], st[3 + i]);
+        atomicAdd(&stats[14], pairs);
         // warp-cycles per phase (A, B, C, finalize)
         for (int i = 0; i < 4; ++i) atomicAdd(&stats[19 + i], (unsigned long long)(clk[i + 1] - clk[i]));
         if (a.dbg && tm.rank == 0) {
@@ -835,34 +845,24 @@ __global__ void __launch_bounds__(kSThreads, FPH_SEARCH_MINB)
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     WarpSmem& W = S.w[w];
     // team mode: the whole CTA per simplex while the queue (sorted by
-    // candidate count, largest first) holds big simplices
+    // candidate count, largest first) holds big simplices; then warp mode.
+    // One call site of run_simplex: the kernel body is inlined once.
     int pending = -1;
+    bool team = true;
     for (;;) {
-        __syncthreads();
-        if (threadIdx.x == 0) S.team.t = atomicAdd(counter, 1);
-        __syncthreads();
-        const int t = S.team.t;
-        if (t >= a.n) return;
-        const int s = order[t];
-        if (a.split && geom[s].stride == 1) continue;  // finished by the pass kernel
-        if (a.cand_count[s] <= a.team_threshold) {
-            pending = t;  // first small simplex: handed to warp 0
-            break;
-        }
-        __syncwarp();
-        if (lane == 0) W.G = geom[s];
-        if (lane == 0) load_verts(a, s, W.V);
-        __syncwarp();
-        const Ctx c{&a, W.G, W.V, S.wt,
-                    a.subset ? (float)(W.G.rho * W.G.rho * (1.0 + 1e-5)) : INFINITY, s};
-        const Team tm{w, kSW, &S.team};
-        run_simplex(c, W, tm);
-    }
-    // warp mode
-    const Team tm{0, 1, nullptr};
-    for (;;) {
-        int t = 0;
-        if (w == 0 && pending >= 0) {
+        int t;
+        if (team) {
+            __syncthreads();
+            if (threadIdx.x == 0) S.team.t = atomicAdd(counter, 1);
+            __syncthreads();
+            t = S.team.t;
+            if (t >= a.n) return;
+            if (a.cand_count[order[t]] <= a.team_threshold) {
+                team = false;
+                pending = t;  // first small simplex: handed to warp 0
+                continue;
+            }
+        } else if (w == 0 && pending >= 0) {
             t = pending;
             pending = -1;
         } else {
@@ -871,13 +871,14 @@ __global__ void __launch_bounds__(kSThreads, FPH_SEARCH_MINB)
         }
         if (t >= a.n) return;
         const int s = order[t];
-        if (a.split && geom[s].stride == 1) continue;
+        if (a.split && geom[s].stride == 1) continue;  // finished by the pass kernel
         __syncwarp();
         if (lane == 0) W.G = geom[s];
         if (lane == 0) load_verts(a, s, W.V);
         __syncwarp();
         const Ctx c{&a, W.G, W.V, S.wt,
                     a.subset ? (float)(W.G.rho * W.G.rho * (1.0 + 1e-5)) : INFINITY, s};
+        const Team tm = team ? Team{w, kSW, &S.team} : Team{0, 1, nullptr};
         run_simplex(c, W, tm);
     }
 }
