@@ -15,9 +15,9 @@
 // through L2/HBM.  Per iteration each CTA publishes its (value, index) to a
 // double-buffered slot array and bumps one monotone arrival counter; one
 // thread per CTA polls the counter (ld.acquire) until all CTAs of this
-// iteration arrived, then the CTA reads every slot in one coalesced pass.
-// All CTAs reduce the same slots in the same order, so they agree on the
-// next landmark without a second broadcast.
+// iteration arrived, then its warp reads every slot and reduces them.  All
+// CTAs reduce the same slots in the same order, so they agree on the next
+// landmark without a second broadcast; two CTA barriers per iteration.
 //
 // Clouds too large for shared memory use the tiled variant: points are
 // Morton-sorted into 256-point tiles with float64 bounding boxes, and an
@@ -70,29 +70,44 @@ __device__ __forceinline__ void warp_argmax(double& v, int& i) {
     }
 }
 
-// Block-wide argmax; result valid in every thread.
-__device__ __forceinline__ void block_argmax(double& v, int& i, double* sv, int* si) {
-    warp_argmax(v, i);
-    int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-    __syncthreads();
+// One iteration's exchange with two CTA barriers (a block-wide argmax on
+// each side took seven): warps leave their argmax in shared memory; warp 0
+// folds them, publishes the CTA's candidate, polls the arrival counter,
+// reads all G slots and reduces them (same slots, same order in every CTA ->
+// the same winner) and leaves the winner in red_i[32].
+// `buf` holds this iteration's G slots; `target` is the arrival count that
+// completes it.
+__device__ __forceinline__ int exchange_argmax(double bv, int bi, Slot* buf, int G, int slot,
+                                               unsigned long long* arrived,
+                                               unsigned long long target, double* red_v,
+                                               int* red_i) {
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    warp_argmax(bv, bi);
     if (l == 0) {
-        sv[w] = v;
-        si[w] = i;
+        red_v[w] = bv;
+        red_i[w] = bi;
     }
     __syncthreads();
-    int nw = blockDim.x >> 5;
     if (w == 0) {
-        v = l < nw ? sv[l] : -INFINITY;
-        i = l < nw ? si[l] : 0x7fffffff;
+        double v = l < (int)(blockDim.x >> 5) ? red_v[l] : -INFINITY;
+        int i = l < (int)(blockDim.x >> 5) ? red_i[l] : 0x7fffffff;
         warp_argmax(v, i);
         if (l == 0) {
-            sv[0] = v;
-            si[0] = i;
+            buf[slot].val = v;
+            buf[slot].idx = i;
+            arrive_release(arrived);
+            while (ld_acquire(arrived) < target) {
+            }
         }
+        __syncwarp();
+        v = -INFINITY;
+        i = 0x7fffffff;
+        for (int b = l; b < G; b += 32) better(v, i, __ldcg(&buf[b].val), __ldcg(&buf[b].idx));
+        warp_argmax(v, i);
+        if (l == 0) red_i[32] = i;
     }
     __syncthreads();
-    v = sv[0];
-    i = si[0];
+    return red_i[32];
 }
 
 template <bool kSmem>
@@ -103,8 +118,7 @@ __global__ void __launch_bounds__(kFpsThreads, 1)
                long long* __restrict__ out) {
     extern __shared__ double sm[];
     __shared__ double red_v[32];
-    __shared__ int red_i[32];
-    const int G = gridDim.x;
+    __shared__ int red_i[33];
     const int beg = blockIdx.x * chunk;
     const int end = min(n, beg + chunk);
     const int cnt = max(0, end - beg);
@@ -152,26 +166,9 @@ __global__ void __launch_bounds__(kFpsThreads, 1)
             }
         }
         if (it == k) break;
-        block_argmax(bv, bi, red_v, red_i);
-        Slot* buf = slots + (it & 1) * G;
-        if (threadIdx.x == 0) {
-            buf[blockIdx.x].val = bv;
-            buf[blockIdx.x].idx = bi;
-            arrive_release(arrived);
-            const unsigned long long target = (unsigned long long)G * it;
-            while (ld_acquire(arrived) < target) {
-            }
-        }
-        __syncthreads();
-        // every CTA has published this iteration's candidate
-        double v = -INFINITY;
-        int i = 0x7fffffff;
-        for (int b = threadIdx.x; b < G; b += blockDim.x) {
-            double sv = __ldcg(&buf[b].val);
-            int si = __ldcg(&buf[b].idx);
-            better(v, i, sv, si);
-        }
-        block_argmax(v, i, red_v, red_i);
+        const int G = gridDim.x;
+        const int i = exchange_argmax(bv, bi, slots + (it & 1) * G, G, blockIdx.x, arrived,
+                                      (unsigned long long)G * it, red_v, red_i);
         cur = i;
         if (blockIdx.x == 0 && threadIdx.x == 0) out[it] = cur;
     }
@@ -180,29 +177,6 @@ __global__ void __launch_bounds__(kFpsThreads, 1)
 
 // ------------------------------------------------------------ tiled variant
 constexpr int kTileP = 256;  // points per tile
-
-// winner of this iteration across the grid (identical in every CTA)
-__device__ __forceinline__ int grid_argmax(double bv, int bi, int it, Slot* slots,
-                                           unsigned long long* arrived, double* red_v,
-                                           int* red_i) {
-    block_argmax(bv, bi, red_v, red_i);
-    const int G = gridDim.x;
-    Slot* buf = slots + (it & 1) * G;
-    if (threadIdx.x == 0) {
-        buf[blockIdx.x].val = bv;
-        buf[blockIdx.x].idx = bi;
-        arrive_release(arrived);
-        const unsigned long long target = (unsigned long long)G * it;
-        while (ld_acquire(arrived) < target) {
-        }
-    }
-    __syncthreads();
-    double v = -INFINITY;
-    int i = 0x7fffffff;
-    for (int b = threadIdx.x; b < G; b += blockDim.x) better(v, i, __ldcg(&buf[b].val), __ldcg(&buf[b].idx));
-    block_argmax(v, i, red_v, red_i);
-    return i;
-}
 
 __global__ void __launch_bounds__(kFpsThreads, 1)
     fps_tiled_kernel(const double* __restrict__ px, const double* __restrict__ py,
@@ -214,7 +188,7 @@ __global__ void __launch_bounds__(kFpsThreads, 1)
                      long long* __restrict__ out) {
     extern __shared__ double sm[];
     __shared__ double red_v[32];
-    __shared__ int red_i[32];
+    __shared__ int red_i[33];
     // tiles are dealt round-robin (tile = blockIdx.x + t * G): the few tiles
     // near a new landmark are Morton neighbours, so they land on different
     // CTAs instead of piling onto one
@@ -272,7 +246,8 @@ __global__ void __launch_bounds__(kFpsThreads, 1)
         double v = -INFINITY;
         int i = 0x7fffffff;
         for (int t = threadIdx.x; t < nt; t += blockDim.x) better(v, i, tmax[t], targ[t]);
-        cur = grid_argmax(v, i, it, slots, arrived, red_v, red_i);
+        cur = exchange_argmax(v, i, slots + (it & 1) * G, G, blockIdx.x, arrived,
+                              (unsigned long long)G * it, red_v, red_i);
         if (blockIdx.x == 0 && threadIdx.x == 0) out[it] = cur;
     }
 }
@@ -440,7 +415,7 @@ __global__ void __launch_bounds__(kFpsThreads, 1)
                        long long* __restrict__ out) {
     extern __shared__ double sm[];
     __shared__ double red_v[32];
-    __shared__ int red_i[32];
+    __shared__ int red_i[33];
     const int ngroups = gridDim.x / cpg;
     const int g = blockIdx.x / cpg, r = blockIdx.x % cpg;
     if (g >= ngroups) return;
@@ -479,23 +454,10 @@ __global__ void __launch_bounds__(kFpsThreads, 1)
                     better(bv, bi, m, gi);
                 }
             }
-            block_argmax(bv, bi, red_v, red_i);
             const long long tag = (long long)seq * (k - 1) + it;  // group-wide iteration
-            Slot* buf = gslots + (tag & 1) * cpg;
-            if (threadIdx.x == 0) {
-                buf[r].val = bv;
-                buf[r].idx = bi;
-                arrive_release(arrived + g);
-                const unsigned long long target = (unsigned long long)cpg * (unsigned long long)tag;
-                while (ld_acquire(arrived + g) < target) {
-                }
-            }
-            __syncthreads();
-            double v = -INFINITY;
-            int i = 0x7fffffff;
-            for (int b = threadIdx.x; b < cpg; b += blockDim.x)
-                better(v, i, __ldcg(&buf[b].val), __ldcg(&buf[b].idx));
-            block_argmax(v, i, red_v, red_i);
+            const int i = exchange_argmax(bv, bi, gslots + (tag & 1) * cpg, cpg, r, arrived + g,
+                                          (unsigned long long)cpg * (unsigned long long)tag, red_v,
+                                          red_i);
             cur = i;
             if (r == 0 && threadIdx.x == 0) out[(long long)c * k + it] = cur;
         }
