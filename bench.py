@@ -283,6 +283,7 @@ def run_ours(args):
                                    "f64_refine_distances": stats[4] / args.steps,
                                    "tasks": stats[5] / args.steps,
                                    "search": {"blocks_searched": stats[7] / args.steps,
+                                              "block_searches": stats[15] / args.steps,
                                               "blocks_pruned": stats[8] / args.steps,
                                               "cta_team_simplices": stats[9] / args.steps,
                                               "staged_phase_a": stats[16] / args.steps,
