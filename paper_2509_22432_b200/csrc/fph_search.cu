@@ -45,7 +45,7 @@ constexpr int kSThreads = 32 * kSW;
 #define FPH_ROWCLIP_F32 1
 #endif
 #ifndef FPH_COUNT_SKIP
-#define FPH_COUNT_SKIP 0
+#define FPH_COUNT_SKIP 1
 #endif
 constexpr int kWT = FPH_WT;     // candidates per warp tile
 constexpr int kMaxBlk = 160;    // blocks ordered best-first per simplex
