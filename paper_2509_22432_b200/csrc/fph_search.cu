@@ -76,6 +76,15 @@ struct SearchSmem {
     TeamSmem team;
 };
 
+// Per-row values of the current simplex (U bounds, then certified minima)
+// live in shared memory after SearchSmem when the template has at most
+// kValsCap rows: every phase reads and writes them, and an L2 round trip per
+// access was a large part of a block search's latency.  A team uses warp
+// 0's array.  Larger templates use the global scratch (a.perpoint).
+constexpr int kValsCap = 1024;
+constexpr size_t kSmemVals = sizeof(SearchSmem) + sizeof(float) * kSW * kValsCap;
+static_assert(kSmemVals + 1024 <= 233472 / 2, "two search CTAs per SM");
+
 // A team is one warp (size 1) or all warps of the CTA (size kSW) working on
 // one simplex: row batches are dealt round-robin to the team's warps and the
 // partial results combined through shared memory.
@@ -705,10 +714,9 @@ __device__ double finalize_team(const Ctx& c, WarpSmem& W, float* vals, const Te
 }
 
 // ------------------------------------------------------- one simplex
-__device__ void run_simplex(const Ctx& c, WarpSmem& W, const Team& tm) {
+__device__ void run_simplex(const Ctx& c, WarpSmem& W, const Team& tm, float* vals) {
     const int lane = threadIdx.x & 31;
     const FloodArgs& a = *c.a;
-    float* vals = a.perpoint + (size_t)c.s * a.P;
     unsigned long long pairs = 0, staged = 0, st[7] = {0, 0, 0, 0, 0, 0, 0}, refined = 0, scanned = 0,
                        blocks = 0, pruned = 0, searches = 0;
     long long clk[5];
@@ -875,6 +883,7 @@ __device__ void run_simplex(const Ctx& c, WarpSmem& W, const Team& tm) {
     tm.sync();
 }
 
+template <bool kSV>
 __global__ void __launch_bounds__(kSThreads, FPH_SEARCH_MINB)
     search_kernel(const __grid_constant__ FloodArgs a, const SimplexGeom* __restrict__ geom,
                   const int* __restrict__ order, int* counter) {
@@ -918,7 +927,17 @@ __global__ void __launch_bounds__(kSThreads, FPH_SEARCH_MINB)
         const Ctx c{&a, W.G, W.V, S.wt,
                     a.subset ? (float)(W.G.rho * W.G.rho * (1.0 + 1e-5)) : INFINITY, s};
         const Team tm = team ? Team{w, kSW, &S.team} : Team{0, 1, nullptr};
-        run_simplex(c, W, tm);
+        float* vals = a.perpoint + (size_t)s * a.P;
+        if (kSV) {
+            float* sv = reinterpret_cast<float*>(smem_raw + sizeof(SearchSmem)) +
+                        (team ? 0 : w) * kValsCap;
+            if (a.split) {  // phase A ran in the pass kernel: its minima seed the rows
+                for (int j = tm.rank * 32 + lane; j < a.P; j += tm.size * 32) sv[j] = vals[j];
+                tm.sync();
+            }
+            vals = sv;
+        }
+        run_simplex(c, W, tm, vals);
     }
 }
 
@@ -952,13 +971,15 @@ int launch_search(const FloodArgs& a, const SimplexGeom* d_geom, const int* d_ca
     int dev = 0, sms = 0, occ = 0;
     FPH_CUDA_TRY(cudaGetDevice(&dev));
     FPH_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    const int smem = (int)sizeof(SearchSmem);
-    FPH_CUDA_TRY(cudaFuncSetAttribute(search_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    FPH_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, search_kernel, kSThreads, smem));
+    const bool sv = a.P <= kValsCap;
+    auto kern = sv ? search_kernel<true> : search_kernel<false>;
+    const int smem = (int)(sv ? kSmemVals : sizeof(SearchSmem));
+    FPH_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    FPH_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kSThreads, smem));
     const int warps_needed = a.n;
     int blocks = sms * (occ > 0 ? occ : 1);
     blocks = blocks < (warps_needed + kSW - 1) / kSW ? blocks : (warps_needed + kSW - 1) / kSW;
-    search_kernel<<<blocks, kSThreads, smem, stream>>>(a, d_geom, d_order, d_counter);
+    kern<<<blocks, kSThreads, smem, stream>>>(a, d_geom, d_order, d_counter);
     FPH_CUDA_TRY(cudaGetLastError());
     for (void* p : {(void*)d_keys, (void*)d_order, (void*)d_iota, (void*)d_counter, tmp})
         FPH_CUDA_TRY(cudaFreeAsync(p, stream));
