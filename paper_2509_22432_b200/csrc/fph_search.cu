@@ -44,6 +44,12 @@ constexpr int kSThreads = 32 * kSW;
 #ifndef FPH_ROWCLIP_F32
 #define FPH_ROWCLIP_F32 1
 #endif
+#ifndef FPH_FOLD_GROUPS
+#define FPH_FOLD_GROUPS 1
+#endif
+#ifndef FPH_TWO_KERNELS
+#define FPH_TWO_KERNELS 1
+#endif
 #ifndef FPH_COUNT_SKIP
 #define FPH_COUNT_SKIP 1
 #endif
@@ -369,12 +375,68 @@ __device__ __forceinline__ float tile_min(const WarpSmem& W, int n, const PointF
 // ------------------------------------------------------------ phase A
 // fold a full tile into the running minima of ALL sample points; a team
 // folds with atomicMin on order-preserving uints (vals_ord)
+__device__ __forceinline__ void lds128(unsigned addr, float4& v) {
+    asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                 : "r"(addr));
+}
+
 __device__ void fold_all(const Ctx& c, WarpSmem& W, int n, float* vals, const Team& tm,
-                         unsigned long long& pairs) {
+                            unsigned long long& pairs) {
     const int lane = threadIdx.x & 31;
     tile_pad(W, n);
     const int P = c.a->P;
     const int np = (n + 1) >> 1;
+    const unsigned sA = (unsigned)__cvta_generic_to_shared(W.tA), sB = (unsigned)__cvta_generic_to_shared(W.tB);
+#if FPH_FOLD_GROUPS
+    const int half = (P + 1) >> 1;
+    if (P <= 32 && half <= 16) {
+        // few rows (edges): G groups of `half` lanes, two rows per lane, each
+        // group folds every G-th candidate pair; group minima meet in group 0
+        const int G = 32 / half;
+        const int g = lane / half, i = lane - g * half;
+        const int ja = i, jb = i + half;
+        const PointF qa = point_at(c, min(ja, P - 1));
+        const PointF qb = point_at(c, min(jb, P - 1));
+        const float2 ax = make_float2(qa.px2, qa.px2), ay = make_float2(qa.py2, qa.py2),
+                     az = make_float2(qa.pz2, qa.pz2);
+        const float2 bx = make_float2(qb.px2, qb.px2), by = make_float2(qb.py2, qb.py2),
+                     bz = make_float2(qb.pz2, qb.pz2);
+        float ba = INFINITY, bb = INFINITY;
+        for (int p = g < G ? g : np; p < np; p += G) {
+            float4 A, B;
+            lds128(sA + 16u * p, A);
+            lds128(sB + 16u * p, B);
+            float2 u = ffma2(az, make_float2(B.x, B.y), make_float2(B.z, B.w));
+            float2 v = ffma2(bz, make_float2(B.x, B.y), make_float2(B.z, B.w));
+            u = ffma2(ay, make_float2(A.z, A.w), u);
+            v = ffma2(by, make_float2(A.z, A.w), v);
+            u = ffma2(ax, make_float2(A.x, A.y), u);
+            v = ffma2(bx, make_float2(A.x, A.y), v);
+            ba = fmin3(ba, u.x, u.y);
+            bb = fmin3(bb, v.x, v.y);
+        }
+        for (int gg = 1; gg < G; ++gg) {
+            const int src = min(i + gg * half, 31);
+            ba = fminf(ba, __shfl_sync(0xffffffffu, ba, src));
+            bb = fminf(bb, __shfl_sync(0xffffffffu, bb, src));
+        }
+        if (g == 0) {
+            const float va = ba + qa.bb, vb = bb + qb.bb;
+            if (ja < P) {
+                if (tm.size == 1) vals[ja] = fminf(vals[ja], va);
+                else atomicMin(reinterpret_cast<unsigned*>(vals) + ja, f2ord(va));
+            }
+            if (jb < P) {
+                if (tm.size == 1) vals[jb] = fminf(vals[jb], vb);
+                else atomicMin(reinterpret_cast<unsigned*>(vals) + jb, f2ord(vb));
+            }
+        }
+        pairs += (unsigned long long)n * P;
+        __syncwarp();
+        return;
+    }
+#endif
     // two points per lane: each tile read serves 64 points
     for (int j0 = 0; j0 < P; j0 += 64) {
         const int ja = j0 + lane, jb = j0 + 32 + lane;
@@ -383,7 +445,11 @@ __device__ void fold_all(const Ctx& c, WarpSmem& W, int n, float* vals, const Te
         float ba0 = INFINITY, ba1 = INFINITY, bb0 = INFINITY, bb1 = INFINITY;
         int p = 0;
         for (; p + 1 < np; p += 2) {
-            const float4 A0 = W.tA[p], B0 = W.tB[p], A1 = W.tA[p + 1], B1 = W.tB[p + 1];
+            float4 A0, B0, A1, B1;
+            lds128(sA + 16u * p, A0);
+            lds128(sB + 16u * p, B0);
+            lds128(sA + 16u * (p + 1), A1);
+            lds128(sB + 16u * (p + 1), B1);
             float2 u0 = ffma2(make_float2(qa.pz2, qa.pz2), make_float2(B0.x, B0.y), make_float2(B0.z, B0.w));
             float2 v0 = ffma2(make_float2(qb.pz2, qb.pz2), make_float2(B0.x, B0.y), make_float2(B0.z, B0.w));
             float2 u1 = ffma2(make_float2(qa.pz2, qa.pz2), make_float2(B1.x, B1.y), make_float2(B1.z, B1.w));
@@ -402,7 +468,9 @@ __device__ void fold_all(const Ctx& c, WarpSmem& W, int n, float* vals, const Te
             bb1 = fmin3(bb1, v1.x, v1.y);
         }
         if (p < np) {
-            const float4 A0 = W.tA[p], B0 = W.tB[p];
+            float4 A0, B0;
+            lds128(sA + 16u * p, A0);
+            lds128(sB + 16u * p, B0);
             float2 u0 = ffma2(make_float2(qa.pz2, qa.pz2), make_float2(B0.x, B0.y), make_float2(B0.z, B0.w));
             float2 v0 = ffma2(make_float2(qb.pz2, qb.pz2), make_float2(B0.x, B0.y), make_float2(B0.z, B0.w));
             u0 = ffma2(make_float2(qa.py2, qa.py2), make_float2(A0.z, A0.w), u0);
@@ -714,6 +782,9 @@ __device__ double finalize_team(const Ctx& c, WarpSmem& W, float* vals, const Te
 }
 
 // ------------------------------------------------------- one simplex
+// kPh: 0 = every phase; 1 = phase A only (the rows' values go to the second
+// kernel through a.perpoint); 2 = phases B, C, F on the first kernel's rows.
+template <int kPh>
 __device__ void run_simplex(const Ctx& c, WarpSmem& W, const Team& tm, float* vals) {
     const int lane = threadIdx.x & 31;
     const FloodArgs& a = *c.a;
@@ -723,7 +794,12 @@ __device__ void run_simplex(const Ctx& c, WarpSmem& W, const Team& tm, float* va
     clk[0] = clock64();
     // ---- A (done by pass_kernel in split mode: vals hold the sample minima)
     int stride = c.G.stride;
-    if (!a.split) {
+    if (kPh == 2 && !a.split) {
+        const long long C = a.cand_count[c.s];
+        const bool exact = (double)C * (double)a.P <= a.exact_pairs || C <= a.exact_cand[a.k];
+        stride = exact ? 1 : (int)max(1ll, (C + a.reps_target - 1) / a.reps_target);
+    }
+    if (!a.split && kPh != 2) {
         for (int j = tm.rank * 32 + lane; j < a.P; j += tm.size * 32)
             vals[j] = tm.size == 1 ? INFINITY : __uint_as_float(f2ord(INFINITY));
         tm.sync();
@@ -744,7 +820,7 @@ __device__ void run_simplex(const Ctx& c, WarpSmem& W, const Team& tm, float* va
     clk[1] = clock64();
     clk[2] = clk[1];
     clk[3] = clk[1];
-    if (stride > 1) {
+    if (kPh != 1 && stride > 1) {
         // ---- B: upper bounds; exact search of the top point
         float umax = -INFINITY;
         int jmax = 0x7fffffff;
@@ -847,11 +923,11 @@ __device__ void run_simplex(const Ctx& c, WarpSmem& W, const Team& tm, float* va
     }
     tm.sync();
     if (stride > 1) clk[3] = clock64();
-    const double M = finalize_team(c, W, vals, tm, refined, scanned);
+    const double M = kPh == 1 ? 0.0 : finalize_team(c, W, vals, tm, refined, scanned);
     clk[4] = clock64();
     unsigned long long* stats = a.stats;
     if (lane == 0) {
-        if (tm.rank == 0) {
+        if (tm.rank == 0 && kPh != 1) {
             a.out_sq[c.s] = M;
             atomicAdd(&stats[5], 1ull);
             atomicAdd(&stats[7], blocks);
@@ -883,7 +959,7 @@ __device__ void run_simplex(const Ctx& c, WarpSmem& W, const Team& tm, float* va
     tm.sync();
 }
 
-template <bool kSV>
+template <bool kSV, int kPh>
 __global__ void __launch_bounds__(kSThreads, FPH_SEARCH_MINB)
     search_kernel(const __grid_constant__ FloodArgs a, const SimplexGeom* __restrict__ geom,
                   const int* __restrict__ order, int* counter) {
@@ -931,13 +1007,18 @@ __global__ void __launch_bounds__(kSThreads, FPH_SEARCH_MINB)
         if (kSV) {
             float* sv = reinterpret_cast<float*>(smem_raw + sizeof(SearchSmem)) +
                         (team ? 0 : w) * kValsCap;
-            if (a.split) {  // phase A ran in the pass kernel: its minima seed the rows
+            if (a.split || kPh == 2) {  // phase A ran in an earlier kernel: its rows seed these
                 for (int j = tm.rank * 32 + lane; j < a.P; j += tm.size * 32) sv[j] = vals[j];
                 tm.sync();
             }
-            vals = sv;
+            run_simplex<kPh>(c, W, tm, sv);
+            if (kPh == 1) {  // hand the rows to the second kernel
+                for (int j = tm.rank * 32 + lane; j < a.P; j += tm.size * 32) vals[j] = sv[j];
+                tm.sync();
+            }
+        } else {
+            run_simplex<kPh>(c, W, tm, vals);
         }
-        run_simplex(c, W, tm, vals);
     }
 }
 
@@ -972,14 +1053,30 @@ int launch_search(const FloodArgs& a, const SimplexGeom* d_geom, const int* d_ca
     FPH_CUDA_TRY(cudaGetDevice(&dev));
     FPH_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     const bool sv = a.P <= kValsCap;
-    auto kern = sv ? search_kernel<true> : search_kernel<false>;
     const int smem = (int)(sv ? kSmemVals : sizeof(SearchSmem));
-    FPH_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    FPH_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kSThreads, smem));
-    const int warps_needed = a.n;
-    int blocks = sms * (occ > 0 ? occ : 1);
-    blocks = blocks < (warps_needed + kSW - 1) / kSW ? blocks : (warps_needed + kSW - 1) / kSW;
-    kern<<<blocks, kSThreads, smem, stream>>>(a, d_geom, d_order, d_counter);
+    // FPH_TWO_KERNELS: phase A in one kernel, phases B, C, F in another, each
+    // with its own register allocation (-7% on configs[1]); small complexes
+    // keep one kernel, where the second launch and tail do not amortise
+    const bool two = FPH_TWO_KERNELS && !a.split && a.n >= 10000;
+    using K = void (*)(const FloodArgs, const SimplexGeom*, const int*, int*);
+    K kern[2];
+    if (two) {
+        kern[0] = sv ? search_kernel<true, 1> : search_kernel<false, 1>;
+        kern[1] = sv ? search_kernel<true, 2> : search_kernel<false, 2>;
+    } else {
+        kern[0] = sv ? search_kernel<true, 0> : search_kernel<false, 0>;
+        kern[1] = nullptr;
+    }
+    for (int i = 0; i < 2 && kern[i]; ++i) {
+        FPH_CUDA_TRY(cudaFuncSetAttribute(kern[i], cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        FPH_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern[i], kSThreads, smem));
+        const int warps_needed = a.n;
+        int blocks = sms * (occ > 0 ? occ : 1);
+        blocks = blocks < (warps_needed + kSW - 1) / kSW ? blocks : (warps_needed + kSW - 1) / kSW;
+        if (i > 0) FPH_CUDA_TRY(cudaMemsetAsync(d_counter, 0, sizeof(int), stream));
+        kern[i]<<<blocks, kSThreads, smem, stream>>>(a, d_geom, d_order, d_counter);
+        FPH_CUDA_TRY(cudaGetLastError());
+    }
     FPH_CUDA_TRY(cudaGetLastError());
     for (void* p : {(void*)d_keys, (void*)d_order, (void*)d_iota, (void*)d_counter, tmp})
         FPH_CUDA_TRY(cudaFreeAsync(p, stream));
