@@ -364,12 +364,15 @@ def e2e_host(lib, native, w, args):
 
     tri = w["tri"]
     top = w["max_dim"]
-    X = torch.from_numpy(w["X"]).pin_memory().numpy()
-    lm = np.ascontiguousarray(tri.points)
+    def pinned(a):  # page-locked copy: the contract's "pinned host memory"
+        return torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()
+
+    X = pinned(w["X"])
+    lm = pinned(tri.points)
     counts = np.array([tri.simplices_by_dim[k].shape[0] for k in range(top + 1)], dtype=np.int64)
-    simp = [None] + [np.ascontiguousarray(tri.simplices_by_dim[k], dtype=np.int32) for k in range(1, top + 1)]
-    fac = [None] + [np.ascontiguousarray(tri.facet_links[k], dtype=np.int32) for k in range(1, top + 1)]
-    outs = [np.empty(max(int(c), 1)) for c in counts]
+    simp = [None] + [pinned(tri.simplices_by_dim[k].astype(np.int32)) for k in range(1, top + 1)]
+    fac = [None] + [pinned(tri.facet_links[k].astype(np.int32)) for k in range(1, top + 1)]
+    outs = [pinned(np.empty(max(int(c), 1))) for c in counts]
     h2d = X.nbytes + lm.nbytes + sum(a.nbytes for a in simp[1:]) + sum(a.nbytes for a in fac[1:])
     d2h = int(sum(counts) * 8)
 

@@ -538,6 +538,53 @@ int fph_flood_shard(const double* points, int64_t n_points, int32_t dim,
     return rc;
 }
 
+#ifndef FPH_CONCURRENT_DIMS
+#define FPH_CONCURRENT_DIMS 1
+#endif
+
+// Interior terms of dimensions 1..max_dim, concurrently on side streams
+// forked from (and joined back into) `stream`.  With profiling on, the
+// flooding time recorded is the fork-to-join interval.
+static int run_interiors(const Grid& g, const double* lm3, int* const* s4, double* const* interior,
+                         const int64_t* counts, int max_dim, int grid_resolution, int subset_mode,
+                         FloodTuning tune, cudaStream_t stream) {
+    static cudaStream_t side[4] = {nullptr, nullptr, nullptr, nullptr};
+    cudaEvent_t fork = nullptr, done[4] = {nullptr, nullptr, nullptr, nullptr}, p0 = nullptr,
+                p1 = nullptr;
+    const bool prof = tune.profile;
+    tune.profile = false;
+    if (prof) {
+        FPH_CUDA_TRY(cudaEventCreate(&p0));
+        FPH_CUDA_TRY(cudaEventCreate(&p1));
+        FPH_CUDA_TRY(cudaEventRecord(p0, stream));
+    }
+    FPH_CUDA_TRY(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
+    FPH_CUDA_TRY(cudaEventRecord(fork, stream));
+    int rc = FPH_OK;
+    for (int k = 1; k <= max_dim && rc == FPH_OK; ++k) {
+        if (counts[k] == 0) continue;
+        if (!side[k]) FPH_CUDA_TRY(cudaStreamCreateWithFlags(&side[k], cudaStreamNonBlocking));
+        cudaStream_t sk = FPH_CONCURRENT_DIMS ? side[k] : stream;
+        FPH_CUDA_TRY(cudaStreamWaitEvent(sk, fork, 0));
+        rc = flood_interior(g, lm3, s4[k], (int)counts[k], k, grid_resolution, subset_mode,
+                            interior[k], tune, sk);
+        count_launches(4);
+        FPH_CUDA_TRY(cudaEventCreateWithFlags(&done[k], cudaEventDisableTiming));
+        FPH_CUDA_TRY(cudaEventRecord(done[k], sk));
+    }
+    for (int k = 1; k <= max_dim; ++k)
+        if (done[k]) {
+            FPH_CUDA_TRY(cudaStreamWaitEvent(stream, done[k], 0));
+            cudaEventDestroy(done[k]);
+        }
+    cudaEventDestroy(fork);
+    if (prof) {
+        FPH_CUDA_TRY(cudaEventRecord(p1, stream));
+        profile_push(p0, p1);
+    }
+    return rc;
+}
+
 int fph_flood_filtration(const double* points, int64_t n_points, int32_t dim,
                          const double* landmarks, int64_t n_landmarks, int32_t max_dim,
                          const int64_t* counts, const int32_t* const* simplices,
@@ -577,6 +624,9 @@ int fph_flood_filtration(const double* points, int64_t n_points, int32_t dim,
             tune.exact_pairs = g_exact_pairs;
             for (int i = 0; i < 4; ++i) tune.exact_cand[i] = g_exact_cand[i];
         double* d_vals[4] = {nullptr, nullptr, nullptr, nullptr};
+        const int32_t* d_f[4] = {nullptr, nullptr, nullptr, nullptr};
+        int* s4[4] = {nullptr, nullptr, nullptr, nullptr};
+        double* interior[4] = {nullptr, nullptr, nullptr, nullptr};
         for (int k = 0; k <= max_dim && rc == FPH_OK; ++k) {
             const long long nk = counts[k];
             double* d_out = out_sq[k];
@@ -589,32 +639,35 @@ int fph_flood_filtration(const double* points, int64_t n_points, int32_t dim,
                     count_launches(1);
                 } else {
                     // vertices: nearest cloud point of each landmark
-                    int* s4;
-                    FPH_TRY(sc.alloc(&s4, (size_t)nk * 4));
+                    int* v4;
+                    FPH_TRY(sc.alloc(&v4, (size_t)nk * 4));
                     std::vector<int> ids((size_t)nk * 4, -1);
                     for (long long i = 0; i < nk; ++i) ids[i * 4] = (int)i;
-                    FPH_CUDA_TRY(cudaMemcpyAsync(s4, ids.data(), sizeof(int) * ids.size(),
+                    FPH_CUDA_TRY(cudaMemcpyAsync(v4, ids.data(), sizeof(int) * ids.size(),
                                                  cudaMemcpyHostToDevice, hc.stream));
-                    rc = flood_interior(gs.grid, lm3, s4, (int)nk, 0, grid_resolution, 0, d_out,
+                    rc = flood_interior(gs.grid, lm3, v4, (int)nk, 0, grid_resolution, 0, d_out,
                                         tune, hc.stream);
                     count_launches(4);
                 }
                 continue;
             }
-            const int32_t *d_s, *d_f;
+            const int32_t* d_s;
             FPH_TRY(stage_in(sc, simplices[k], (size_t)nk * (k + 1), memory, &d_s));
-            FPH_TRY(stage_in(sc, facets[k], (size_t)nk * (k + 1), memory, &d_f));
-            int* s4;
-            double* interior;
-            FPH_TRY(sc.alloc(&s4, (size_t)nk * 4));
-            FPH_TRY(sc.alloc(&interior, (size_t)nk));
-            pad4_kernel<<<blocks_for(nk), 256, 0, hc.stream>>>(d_s, nk, k, s4);
+            FPH_TRY(stage_in(sc, facets[k], (size_t)nk * (k + 1), memory, &d_f[k]));
+            FPH_TRY(sc.alloc(&s4[k], (size_t)nk * 4));
+            FPH_TRY(sc.alloc(&interior[k], (size_t)nk));
+            pad4_kernel<<<blocks_for(nk), 256, 0, hc.stream>>>(d_s, nk, k, s4[k]);
             count_launches(1);
-            rc = flood_interior(gs.grid, lm3, s4, (int)nk, k, grid_resolution, subset_mode,
-                                interior, tune, hc.stream);
-            count_launches(4);
-            if (rc != FPH_OK) break;
-            rc = flood_complete(interior, d_f, (int)nk, k, d_vals[k - 1], d_out, hc.stream);
+        }
+        // The interior terms of the dimensions >= 1 are independent: each runs
+        // on its own stream so one dimension's kernels fill the other's tail;
+        // the facet completion then runs in increasing dimension.
+        if (rc == FPH_OK) rc = run_interiors(gs.grid, lm3, s4, interior, counts, max_dim,
+                                            grid_resolution, subset_mode, tune, hc.stream);
+        for (int k = 1; k <= max_dim && rc == FPH_OK; ++k) {
+            if (counts[k] == 0) continue;
+            rc = flood_complete(interior[k], d_f[k], (int)counts[k], k, d_vals[k - 1], d_vals[k],
+                                hc.stream);
             count_launches(1);
         }
         if (rc == FPH_OK && memory == FPH_MEM_HOST) {

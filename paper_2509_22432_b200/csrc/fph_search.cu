@@ -50,6 +50,9 @@ constexpr int kSThreads = 32 * kSW;
 #ifndef FPH_TWO_KERNELS
 #define FPH_TWO_KERNELS 1
 #endif
+#ifndef FPH_THREE_KERNELS
+#define FPH_THREE_KERNELS 1
+#endif
 #ifndef FPH_COUNT_SKIP
 #define FPH_COUNT_SKIP 1
 #endif
@@ -782,8 +785,9 @@ __device__ double finalize_team(const Ctx& c, WarpSmem& W, float* vals, const Te
 }
 
 // ------------------------------------------------------- one simplex
-// kPh: 0 = every phase; 1 = phase A only (the rows' values go to the second
-// kernel through a.perpoint); 2 = phases B, C, F on the first kernel's rows.
+// kPh: 0 = every phase; 1 = phase A only (the rows' values go to the next
+// kernel through a.perpoint); 2 = phases B, C, F on those rows; 3 = phases
+// B, C only; 4 = phase F only.
 template <int kPh>
 __device__ void run_simplex(const Ctx& c, WarpSmem& W, const Team& tm, float* vals) {
     const int lane = threadIdx.x & 31;
@@ -794,12 +798,12 @@ __device__ void run_simplex(const Ctx& c, WarpSmem& W, const Team& tm, float* va
     clk[0] = clock64();
     // ---- A (done by pass_kernel in split mode: vals hold the sample minima)
     int stride = c.G.stride;
-    if (kPh == 2 && !a.split) {
+    if ((kPh == 2 || kPh == 3) && !a.split) {
         const long long C = a.cand_count[c.s];
         const bool exact = (double)C * (double)a.P <= a.exact_pairs || C <= a.exact_cand[a.k];
         stride = exact ? 1 : (int)max(1ll, (C + a.reps_target - 1) / a.reps_target);
     }
-    if (!a.split && kPh != 2) {
+    if (!a.split && (kPh == 0 || kPh == 1)) {
         for (int j = tm.rank * 32 + lane; j < a.P; j += tm.size * 32)
             vals[j] = tm.size == 1 ? INFINITY : __uint_as_float(f2ord(INFINITY));
         tm.sync();
@@ -820,7 +824,7 @@ __device__ void run_simplex(const Ctx& c, WarpSmem& W, const Team& tm, float* va
     clk[1] = clock64();
     clk[2] = clk[1];
     clk[3] = clk[1];
-    if (kPh != 1 && stride > 1) {
+    if ((kPh == 0 || kPh == 2 || kPh == 3) && stride > 1) {
         // ---- B: upper bounds; exact search of the top point
         float umax = -INFINITY;
         int jmax = 0x7fffffff;
@@ -923,11 +927,12 @@ __device__ void run_simplex(const Ctx& c, WarpSmem& W, const Team& tm, float* va
     }
     tm.sync();
     if (stride > 1) clk[3] = clock64();
-    const double M = kPh == 1 ? 0.0 : finalize_team(c, W, vals, tm, refined, scanned);
+    const bool fin = kPh == 0 || kPh == 2 || kPh == 4;
+    const double M = fin ? finalize_team(c, W, vals, tm, refined, scanned) : 0.0;
     clk[4] = clock64();
     unsigned long long* stats = a.stats;
     if (lane == 0) {
-        if (tm.rank == 0 && kPh != 1) {
+        if (tm.rank == 0 && fin) {
             a.out_sq[c.s] = M;
             atomicAdd(&stats[5], 1ull);
             atomicAdd(&stats[7], blocks);
@@ -1007,12 +1012,12 @@ __global__ void __launch_bounds__(kSThreads, FPH_SEARCH_MINB)
         if (kSV) {
             float* sv = reinterpret_cast<float*>(smem_raw + sizeof(SearchSmem)) +
                         (team ? 0 : w) * kValsCap;
-            if (a.split || kPh == 2) {  // phase A ran in an earlier kernel: its rows seed these
+            if (a.split || kPh >= 2) {  // an earlier kernel left the rows' values
                 for (int j = tm.rank * 32 + lane; j < a.P; j += tm.size * 32) sv[j] = vals[j];
                 tm.sync();
             }
             run_simplex<kPh>(c, W, tm, sv);
-            if (kPh == 1) {  // hand the rows to the second kernel
+            if (kPh == 1 || kPh == 3) {  // hand the rows to the next kernel
                 for (int j = tm.rank * 32 + lane; j < a.P; j += tm.size * 32) vals[j] = sv[j];
                 tm.sync();
             }
@@ -1055,19 +1060,23 @@ int launch_search(const FloodArgs& a, const SimplexGeom* d_geom, const int* d_ca
     const bool sv = a.P <= kValsCap;
     const int smem = (int)(sv ? kSmemVals : sizeof(SearchSmem));
     // FPH_TWO_KERNELS: phase A in one kernel, phases B, C, F in another, each
-    // with its own register allocation (-7% on configs[1]); small complexes
-    // keep one kernel, where the second launch and tail do not amortise
+    // with its own register allocation (-7% on configs[1]); FPH_THREE_KERNELS
+    // also separates F from B, C (phase C -16%).  Small complexes keep one
+    // kernel, where the extra launches and tails do not amortise.
     const bool two = FPH_TWO_KERNELS && !a.split && a.n >= 10000;
     using K = void (*)(const FloodArgs, const SimplexGeom*, const int*, int*);
-    K kern[2];
-    if (two) {
+    K kern[3] = {nullptr, nullptr, nullptr};
+    if (two && FPH_THREE_KERNELS) {
+        kern[0] = sv ? search_kernel<true, 1> : search_kernel<false, 1>;
+        kern[1] = sv ? search_kernel<true, 3> : search_kernel<false, 3>;
+        kern[2] = sv ? search_kernel<true, 4> : search_kernel<false, 4>;
+    } else if (two) {
         kern[0] = sv ? search_kernel<true, 1> : search_kernel<false, 1>;
         kern[1] = sv ? search_kernel<true, 2> : search_kernel<false, 2>;
     } else {
         kern[0] = sv ? search_kernel<true, 0> : search_kernel<false, 0>;
-        kern[1] = nullptr;
     }
-    for (int i = 0; i < 2 && kern[i]; ++i) {
+    for (int i = 0; i < 3 && kern[i]; ++i) {
         FPH_CUDA_TRY(cudaFuncSetAttribute(kern[i], cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         FPH_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern[i], kSThreads, smem));
         const int warps_needed = a.n;
