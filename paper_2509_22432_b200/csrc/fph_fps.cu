@@ -100,9 +100,21 @@ __device__ __forceinline__ int exchange_argmax(double bv, int bi, Slot* buf, int
             }
         }
         __syncwarp();
+        // this lane's slots (G <= 160: five) all in flight before the reduction
+        constexpr int kPer = 5;
+        double sv[kPer];
+        int si[kPer];
+#pragma unroll
+        for (int t = 0; t < kPer; ++t) {
+            const int b = l + 32 * t;
+            sv[t] = b < G ? __ldcg(&buf[b].val) : -INFINITY;
+            si[t] = b < G ? __ldcg(&buf[b].idx) : 0x7fffffff;
+        }
         v = -INFINITY;
         i = 0x7fffffff;
-        for (int b = l; b < G; b += 32) better(v, i, __ldcg(&buf[b].val), __ldcg(&buf[b].idx));
+#pragma unroll
+        for (int t = 0; t < kPer; ++t) better(v, i, sv[t], si[t]);
+        for (int b = l + 32 * kPer; b < G; b += 32) better(v, i, __ldcg(&buf[b].val), __ldcg(&buf[b].idx));
         warp_argmax(v, i);
         if (l == 0) red_i[32] = i;
     }
