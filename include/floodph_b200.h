@@ -171,14 +171,16 @@ int fph_set_tuning(double cell_occupancy, double pairs_per_task);
  * All are exact (identical values).
  * reps_target: candidates per representative (sampling) pass;
  * team_threshold: simplices with more candidates are searched by a whole
- * CTA instead of one warp.  <= 0 keeps the defaults (512, 131072).
+ * CTA instead of one warp; 0 (default) derives it per launch as
+ * beta x (total candidates / resident warps) with beta = 2, a negative value
+ * -b uses beta = b / 100.  reps_target <= 0 keeps the default 512.
  */
 int fph_set_search(int32_t algo, int32_t reps_target, int32_t team_threshold);
 
 /*
  * Bounded search: a simplex whose rows x candidates <= pairs is finished by
  * one exact pass (phase A unsampled) instead of the bounded search
- * (default 262144; negative restores the default).
+ * (default 65536; negative restores the default).
  */
 int fph_set_exact_pairs(double pairs);
 

@@ -22,8 +22,8 @@ static bool g_profile = false;
 static int g_algo = 1;
 static double g_probe_cells = 1.0;
 static int g_reps_target = 512;
-static int g_team_threshold = 131072;
-static double g_exact_pairs = 262144.0;
+static int g_team_threshold = 0;  // auto (derived per launch on the device)
+static double g_exact_pairs = 65536.0;
 static long long g_exact_cand[4] = {0, 0, 2500, 0};
 static thread_local long long g_launches = 0;
 
@@ -217,12 +217,12 @@ int fph_set_search(int32_t algo, int32_t reps_target, int32_t team_threshold) {
     }
     g_algo = algo;
     g_reps_target = reps_target > 0 ? reps_target : 512;
-    g_team_threshold = team_threshold > 0 ? team_threshold : 131072;
+    g_team_threshold = team_threshold;
     return FPH_OK;
 }
 
 int fph_set_exact_pairs(double pairs) {
-    g_exact_pairs = pairs >= 0 ? pairs : 262144.0;
+    g_exact_pairs = pairs >= 0 ? pairs : 65536.0;
     return FPH_OK;
 }
 

@@ -666,7 +666,8 @@ int flood_interior(const Grid& g, const double* d_landmarks3, const int* d_simpl
     a.nblk = search ? (int)blk_off.size() - 1 : 0;
     a.probe = tune.probe_cells * g.h;
     a.reps_target = tune.reps_target > 0 ? tune.reps_target : 384;
-    a.team_threshold = tune.team_threshold > 0 ? tune.team_threshold : 131072;
+    a.team_threshold = tune.team_threshold;
+    a.team_thr_dev = nullptr;
     a.exact_pairs = tune.exact_pairs;
     for (int i = 0; i < 4; ++i) a.exact_cand[i] = tune.exact_cand[i];
     a.split = tune.algo == 2 ? 1 : 0;

@@ -34,6 +34,8 @@ struct FloodArgs {
     int* cand_count;          // per simplex: candidates in the Lemma-4.2 ball rows
     unsigned long long* stats;  // work counters (fph_flood_stats)
     int team_threshold;       // candidates above which a whole CTA takes the simplex
+                              // (<= 0: derived on the device, see launch_search)
+    const long long* team_thr_dev;  // that derived threshold (nullptr: use team_threshold)
     const double* explicit_pts;  // n x P x 3 sample rows (uniform-random sampler), or null
     long long* dbg;           // optional: per simplex 8 values (phase cycles, counters)
     double exact_pairs;       // bounded search: one exact pass when rows x candidates <= this
@@ -55,7 +57,7 @@ struct FloodTuning {
     int algo = 1;                 // 0: brute force over the Lemma-4.2 ball, 1: block search
     double probe_cells = 1.0;     // block search: first-round margin in grid cells
     int reps_target = 384;        // block search: candidates per representative pass
-    int team_threshold = 131072;  // bounded search: CTA-cooperative simplices above this
+    int team_threshold = 0;  // bounded search: CTA-cooperative simplices above this (<= 0: auto)
     double exact_pairs = 0.0;     // bounded search: exact pass below this many pairs
     long long exact_cand[4] = {0, 0, 0, 0};  // ... or below this many candidates (per dim)
 };

@@ -973,6 +973,7 @@ __global__ void __launch_bounds__(kSThreads, FPH_SEARCH_MINB)
     for (int i = threadIdx.x; i <= a.m; i += blockDim.x) S.wt[i] = __ddiv_rn((double)i, (double)a.m);
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     WarpSmem& W = S.w[w];
+    const long long team_thr = a.team_thr_dev ? *a.team_thr_dev : (long long)a.team_threshold;
     // team mode: the whole CTA per simplex while the queue (sorted by
     // candidate count, largest first) holds big simplices; then warp mode.
     // One call site of run_simplex: the kernel body is inlined once.
@@ -986,7 +987,7 @@ __global__ void __launch_bounds__(kSThreads, FPH_SEARCH_MINB)
             __syncthreads();
             t = S.team.t;
             if (t >= a.n) return;
-            if (a.cand_count[order[t]] <= a.team_threshold) {
+            if (a.cand_count[order[t]] <= team_thr) {
                 team = false;
                 pending = t;  // first small simplex: handed to warp 0
                 continue;
@@ -1025,6 +1026,17 @@ __global__ void __launch_bounds__(kSThreads, FPH_SEARCH_MINB)
             run_simplex<kPh>(c, W, tm, vals);
         }
     }
+}
+
+// Auto team threshold: a simplex is searched by a whole CTA when its
+// candidates exceed beta x (all candidates / resident warps) -- one warp
+// would otherwise still be busy with it long after the others ran dry.
+constexpr double kTeamBeta = 2.0;
+constexpr long long kTeamMin = 32768;
+
+__global__ void team_thr_kernel(const long long* sum, double beta, int warps, long long* thr) {
+    const double t = beta * (double)*sum / (double)(warps > 0 ? warps : 1);
+    *thr = t > (double)kTeamMin ? (long long)t : kTeamMin;
 }
 
 __global__ void iota_kernel(int* out, int n) {
@@ -1076,15 +1088,34 @@ int launch_search(const FloodArgs& a, const SimplexGeom* d_geom, const int* d_ca
     } else {
         kern[0] = sv ? search_kernel<true, 0> : search_kernel<false, 0>;
     }
+    FPH_CUDA_TRY(cudaFuncSetAttribute(kern[0], cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    FPH_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern[0], kSThreads, smem));
+    int blocks = sms * (occ > 0 ? occ : 1);
+    blocks = blocks < (a.n + kSW - 1) / kSW ? blocks : (a.n + kSW - 1) / kSW;
+    FloodArgs b = a;
+    long long* d_thr = nullptr;
+    void* tmp2 = nullptr;
+    if (a.team_threshold <= 0) {
+        // threshold from the total candidate count, computed on the device so
+        // the concurrent streams never wait for the host
+        const double beta = a.team_threshold < 0 ? -a.team_threshold / 100.0 : kTeamBeta;
+        FPH_CUDA_TRY(cudaMallocAsync(&d_thr, 2 * sizeof(long long), stream));
+        size_t tb = 0;
+        cub::DeviceReduce::Sum(nullptr, tb, d_cand, d_thr + 1, a.n, stream);
+        FPH_CUDA_TRY(cudaMallocAsync(&tmp2, tb, stream));
+        FPH_CUDA_TRY(cub::DeviceReduce::Sum(tmp2, tb, d_cand, d_thr + 1, a.n, stream));
+        team_thr_kernel<<<1, 1, 0, stream>>>(d_thr + 1, beta, blocks * kSW, d_thr);
+        b.team_thr_dev = d_thr;
+    }
     for (int i = 0; i < 3 && kern[i]; ++i) {
         FPH_CUDA_TRY(cudaFuncSetAttribute(kern[i], cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        FPH_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern[i], kSThreads, smem));
-        const int warps_needed = a.n;
-        int blocks = sms * (occ > 0 ? occ : 1);
-        blocks = blocks < (warps_needed + kSW - 1) / kSW ? blocks : (warps_needed + kSW - 1) / kSW;
         if (i > 0) FPH_CUDA_TRY(cudaMemsetAsync(d_counter, 0, sizeof(int), stream));
-        kern[i]<<<blocks, kSThreads, smem, stream>>>(a, d_geom, d_order, d_counter);
+        kern[i]<<<blocks, kSThreads, smem, stream>>>(b, d_geom, d_order, d_counter);
         FPH_CUDA_TRY(cudaGetLastError());
+    }
+    if (d_thr) {
+        FPH_CUDA_TRY(cudaFreeAsync(d_thr, stream));
+        FPH_CUDA_TRY(cudaFreeAsync(tmp2, stream));
     }
     FPH_CUDA_TRY(cudaGetLastError());
     for (void* p : {(void*)d_keys, (void*)d_order, (void*)d_iota, (void*)d_counter, tmp})

@@ -157,11 +157,13 @@ def algo_switch():
     use(1)
 
 
-@pytest.mark.parametrize("reps,team", [(1024, 32768), (64, 1000), (4096, 2**30), (300, 1)])
+@pytest.mark.parametrize("reps,team", [(1024, 32768), (64, 1000), (4096, 2**30), (300, 1),
+                                       (512, 0), (512, -50)])
 def test_block_search_equals_brute_force_full_size(algo_switch, reps, team):
     """The two exact algorithms agree bit for bit on BASELINE configs[1]
     (1M points, 2k landmarks, dims <= 2) for several search tunings: sample
-    sizes, and every simplex searched by one warp / by a whole CTA."""
+    sizes, and every simplex searched by one warp / by a whole CTA / by the
+    device-derived team threshold (team <= 0)."""
     X = gen_sphere_torus_mix(1_000_000, seed=0).points
     tri = delaunay(X[farthest_point_sampling(X, 2000)])
     algo_switch(0)
