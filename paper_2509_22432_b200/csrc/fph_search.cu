@@ -53,6 +53,9 @@ constexpr int kSThreads = 32 * kSW;
 #ifndef FPH_THREE_KERNELS
 #define FPH_THREE_KERNELS 1
 #endif
+#ifndef FPH_REPS_2WIN
+#define FPH_REPS_2WIN 1
+#endif
 #ifndef FPH_COUNT_SKIP
 #define FPH_COUNT_SKIP 1
 #endif
@@ -510,6 +513,35 @@ __device__ void reps_pass(const Ctx& c, WarpSmem& W, int stride, float* vals, co
         const int total = bt.total;
         const int first = (int)((stride - fbase % stride) % stride);
         const int nsel = total > first ? (total - first - 1) / stride + 1 : 0;
+#if FPH_REPS_2WIN
+        // two windows of loads in flight (phase A runs in its own kernel, so
+        // the extra registers do not reach the search phases)
+        for (int i0 = 0; i0 < nsel; i0 += 64) {
+            int i[2];
+#pragma unroll
+            for (int d = 0; d < 2; ++d) {
+                const int f = i0 + 32 * d;
+                if (stride == 1) i[d] = window_index(W, bt, f);
+                else i[d] = f + lane < nsel ? cand_index(W, bt.nne, first + (f + lane) * stride) : 0;
+            }
+            float ax[2], ay[2], az[2], aw[2];
+#pragma unroll
+            for (int d = 0; d < 2; ++d) {
+                ax[d] = ay[d] = az[d] = aw[d] = 0.f;
+                if (i0 + 32 * d + lane < nsel) load_rel(c, i[d], ax[d], ay[d], az[d], aw[d]);
+            }
+#pragma unroll
+            for (int d = 0; d < 2; ++d)
+                if (i0 + 32 * d < nsel)
+                    tile_n = tile_push(W, tile_n, i0 + 32 * d + lane < nsel && aw[d] <= c.thr, ax[d],
+                                       ay[d], az[d], aw[d]);
+            if (tile_n > kWT - 64) {
+                staged += tile_n;
+                fold_all(c, W, tile_n, vals, tm, pairs);
+                tile_n = 0;
+            }
+        }
+#else
         for (int i0 = 0; i0 < nsel; i0 += 32) {
             const int widx = stride == 1 ? window_index(W, bt, i0) : 0;
             bool keep = false;
@@ -526,6 +558,7 @@ __device__ void reps_pass(const Ctx& c, WarpSmem& W, int stride, float* vals, co
                 tile_n = 0;
             }
         }
+#endif
         fbase += total;
     }
     if (tile_n > 0) {

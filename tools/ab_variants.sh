@@ -1,7 +1,7 @@
 #!/bin/bash
 # A/B the flooding pass across library variants built into _lib/variants/
 # usage: tools/ab_variants.sh name1 name2 ...   (on a GPU box)
-S='[[1, 512, 131072, 2.0]]'
+S='[[1, 512, 0, 2.0]]'
 for r in 1 2; do
   for v in "$@"; do
     echo "== $v"
