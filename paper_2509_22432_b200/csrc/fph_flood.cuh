@@ -25,6 +25,7 @@ struct FloodArgs {
     double pairs_per_task;
     const uchar4* tmpl;       // interior compositions, P rows (block-ordered)
     float* perpoint;          // n x P fp32 minima
+    float* lower;             // per simplex: phase B's lower bound L (split B | C kernels)
     double* out_sq;           // n squared interior maxima (-1: no interior row)
     // block search (algo 1): point blocks of <= 32 rows, probe radius, reps
     const int* blk_off;       // nblk + 1 offsets into tmpl

@@ -56,6 +56,12 @@ constexpr int kSThreads = 32 * kSW;
 #ifndef FPH_REPS_2WIN
 #define FPH_REPS_2WIN 1
 #endif
+#ifndef FPH_FOUR_KERNELS
+#define FPH_FOUR_KERNELS 1
+#endif
+#ifndef FPH_PDL
+#define FPH_PDL 1
+#endif
 #ifndef FPH_COUNT_SKIP
 #define FPH_COUNT_SKIP 1
 #endif
@@ -820,7 +826,8 @@ __device__ double finalize_team(const Ctx& c, WarpSmem& W, float* vals, const Te
 // ------------------------------------------------------- one simplex
 // kPh: 0 = every phase; 1 = phase A only (the rows' values go to the next
 // kernel through a.perpoint); 2 = phases B, C, F on those rows; 3 = phases
-// B, C only; 4 = phase F only.
+// B, C only; 4 = phase F only; 5 = phase B only (L to a.lower); 6 = phase C
+// only.
 template <int kPh>
 __device__ void run_simplex(const Ctx& c, WarpSmem& W, const Team& tm, float* vals) {
     const int lane = threadIdx.x & 31;
@@ -831,7 +838,7 @@ __device__ void run_simplex(const Ctx& c, WarpSmem& W, const Team& tm, float* va
     clk[0] = clock64();
     // ---- A (done by pass_kernel in split mode: vals hold the sample minima)
     int stride = c.G.stride;
-    if ((kPh == 2 || kPh == 3) && !a.split) {
+    if ((kPh == 2 || kPh == 3 || kPh == 5 || kPh == 6) && !a.split) {
         const long long C = a.cand_count[c.s];
         const bool exact = (double)C * (double)a.P <= a.exact_pairs || C <= a.exact_cand[a.k];
         stride = exact ? 1 : (int)max(1ll, (C + a.reps_target - 1) / a.reps_target);
@@ -857,7 +864,11 @@ __device__ void run_simplex(const Ctx& c, WarpSmem& W, const Team& tm, float* va
     clk[1] = clock64();
     clk[2] = clk[1];
     clk[3] = clk[1];
-    if ((kPh == 0 || kPh == 2 || kPh == 3) && stride > 1) {
+    if ((kPh == 0 || kPh == 2 || kPh == 3 || kPh == 5 || kPh == 6) && stride > 1) {
+      float L;
+      if (kPh == 6) {
+        L = a.lower[c.s];  // phase B ran in the previous kernel
+      } else {
         // ---- B: upper bounds; exact search of the top point
         float umax = -INFINITY;
         int jmax = 0x7fffffff;
@@ -875,14 +886,16 @@ __device__ void run_simplex(const Ctx& c, WarpSmem& W, const Team& tm, float* va
         const int jw = __reduce_min_sync(0xffffffffu, umax == um ? jmax : 0x7fffffff);
         const int jt = -(int)tm.max_f(-(float)jw);
         tm.sync();
-        float L;
         {
             const PointF q = point_at(c, jt);
             const double R = sqrt((double)um) * (1.0 + 1e-3) + 1e-4 * (double)q.B;
             const float m = point_min32(c, W, q, R, tm, scanned) + q.bb;
             L = m - err_bound(m, q.B);
         }
+        if (kPh == 5 && tm.rank == 0 && lane == 0) a.lower[c.s] = L;
+      }
         clk[2] = clock64();
+      if (kPh != 5) {
         // ---- C: blocks best-first (in order when there are too many to rank);
         // one call site, so search_block is inlined once
         const int nblk = a.nblk;
@@ -957,10 +970,11 @@ __device__ void run_simplex(const Ctx& c, WarpSmem& W, const Team& tm, float* va
             }
             tm.sync();
         }
+      }
     }
     tm.sync();
     if (stride > 1) clk[3] = clock64();
-    const bool fin = kPh == 0 || kPh == 2 || kPh == 4;
+    const bool fin = kPh == 0 || kPh == 2 || kPh == 4;  // 5: B only, 6: C only
     const double M = fin ? finalize_team(c, W, vals, tm, refined, scanned) : 0.0;
     clk[4] = clock64();
     unsigned long long* stats = a.stats;
@@ -997,10 +1011,28 @@ __device__ void run_simplex(const Ctx& c, WarpSmem& W, const Team& tm, float* va
     tm.sync();
 }
 
+__device__ __forceinline__ int ld_acquire_i(const int* p) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_i(int* p, int v) {
+    asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// Chained phase kernels (pos = place in the chain, stage != nullptr): every
+// kernel lets the next one launch at once (programmatic dependent launch),
+// so the next phase's CTAs take the SM slots the moment this phase's CTAs
+// run out of work; instead of waiting for the whole grid, a CTA waits only
+// for ITS simplex's previous phase (stage[s] >= pos, published with release
+// after the rows were written).  Every simplex of the previous phase is
+// claimed by a resident CTA before any of its CTAs exits, so the waits
+// always end.
 template <bool kSV, int kPh>
 __global__ void __launch_bounds__(kSThreads, FPH_SEARCH_MINB)
     search_kernel(const __grid_constant__ FloodArgs a, const SimplexGeom* __restrict__ geom,
-                  const int* __restrict__ order, int* counter) {
+                  const int* __restrict__ order, int* counter, int* stage, int pos) {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     extern __shared__ __align__(16) unsigned char smem_raw[];
     SearchSmem& S = *reinterpret_cast<SearchSmem*>(smem_raw);
     for (int i = threadIdx.x; i <= a.m; i += blockDim.x) S.wt[i] = __ddiv_rn((double)i, (double)a.m);
@@ -1013,6 +1045,9 @@ __global__ void __launch_bounds__(kSThreads, FPH_SEARCH_MINB)
     int pending = -1;
     bool team = true;
     for (;;) {
+#ifdef FPH_PROLOGUE_CLK
+        const long long pc0 = clock64();
+#endif
         int t;
         if (team) {
             __syncthreads();
@@ -1035,6 +1070,11 @@ __global__ void __launch_bounds__(kSThreads, FPH_SEARCH_MINB)
         if (t >= a.n) return;
         const int s = order[t];
         if (a.split && geom[s].stride == 1) continue;  // finished by the pass kernel
+        if (stage && pos > 0) {  // this simplex's previous phase
+            if ((team ? threadIdx.x : lane) == 0)
+                while (ld_acquire_i(stage + s) < pos) __nanosleep(64);
+            if (team) __syncthreads();
+        }
         __syncwarp();
         if (lane == 0) W.G = geom[s];
         if (lane == 0) load_verts(a, s, W.V);
@@ -1050,13 +1090,21 @@ __global__ void __launch_bounds__(kSThreads, FPH_SEARCH_MINB)
                 for (int j = tm.rank * 32 + lane; j < a.P; j += tm.size * 32) sv[j] = vals[j];
                 tm.sync();
             }
+#ifdef FPH_PROLOGUE_CLK
+            if (lane == 0) atomicAdd(&a.stats[2], (unsigned long long)(clock64() - pc0));
+#endif
             run_simplex<kPh>(c, W, tm, sv);
-            if (kPh == 1 || kPh == 3) {  // hand the rows to the next kernel
+            if (kPh == 1 || kPh == 3 || kPh == 5 || kPh == 6) {  // hand the rows on
                 for (int j = tm.rank * 32 + lane; j < a.P; j += tm.size * 32) vals[j] = sv[j];
                 tm.sync();
             }
         } else {
             run_simplex<kPh>(c, W, tm, vals);
+        }
+        if (stage) {  // publish: this simplex's phase is done
+            __threadfence();
+            tm.sync();
+            if (tm.rank == 0 && lane == 0) st_release_i(stage + s, pos + 1);
         }
     }
 }
@@ -1106,12 +1154,21 @@ int launch_search(const FloodArgs& a, const SimplexGeom* d_geom, const int* d_ca
     const int smem = (int)(sv ? kSmemVals : sizeof(SearchSmem));
     // FPH_TWO_KERNELS: phase A in one kernel, phases B, C, F in another, each
     // with its own register allocation (-7% on configs[1]); FPH_THREE_KERNELS
-    // also separates F from B, C (phase C -16%).  Small complexes keep one
-    // kernel, where the extra launches and tails do not amortise.
+    // also separates F from B, C (phase C -16%), FPH_FOUR_KERNELS B from C
+    // (phase C another -16%); FPH_PDL chains them per simplex so tails
+    // overlap.  Small complexes keep one kernel, where the extra launches and
+    // tails do not amortise.
     const bool two = FPH_TWO_KERNELS && !a.split && a.n >= 10000;
-    using K = void (*)(const FloodArgs, const SimplexGeom*, const int*, int*);
-    K kern[3] = {nullptr, nullptr, nullptr};
-    if (two && FPH_THREE_KERNELS) {
+    using K = void (*)(const FloodArgs, const SimplexGeom*, const int*, int*, int*, int);
+    K kern[4] = {nullptr, nullptr, nullptr, nullptr};
+    float* d_lower = nullptr;
+    if (two && FPH_FOUR_KERNELS) {
+        kern[0] = sv ? search_kernel<true, 1> : search_kernel<false, 1>;
+        kern[1] = sv ? search_kernel<true, 5> : search_kernel<false, 5>;
+        kern[2] = sv ? search_kernel<true, 6> : search_kernel<false, 6>;
+        kern[3] = sv ? search_kernel<true, 4> : search_kernel<false, 4>;
+        FPH_CUDA_TRY(cudaMallocAsync(&d_lower, sizeof(float) * a.n, stream));
+    } else if (two && FPH_THREE_KERNELS) {
         kern[0] = sv ? search_kernel<true, 1> : search_kernel<false, 1>;
         kern[1] = sv ? search_kernel<true, 3> : search_kernel<false, 3>;
         kern[2] = sv ? search_kernel<true, 4> : search_kernel<false, 4>;
@@ -1126,6 +1183,7 @@ int launch_search(const FloodArgs& a, const SimplexGeom* d_geom, const int* d_ca
     int blocks = sms * (occ > 0 ? occ : 1);
     blocks = blocks < (a.n + kSW - 1) / kSW ? blocks : (a.n + kSW - 1) / kSW;
     FloodArgs b = a;
+    b.lower = d_lower;
     long long* d_thr = nullptr;
     void* tmp2 = nullptr;
     if (a.team_threshold <= 0) {
@@ -1140,12 +1198,34 @@ int launch_search(const FloodArgs& a, const SimplexGeom* d_geom, const int* d_ca
         team_thr_kernel<<<1, 1, 0, stream>>>(d_thr + 1, beta, blocks * kSW, d_thr);
         b.team_thr_dev = d_thr;
     }
-    for (int i = 0; i < 3 && kern[i]; ++i) {
-        FPH_CUDA_TRY(cudaFuncSetAttribute(kern[i], cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        if (i > 0) FPH_CUDA_TRY(cudaMemsetAsync(d_counter, 0, sizeof(int), stream));
-        kern[i]<<<blocks, kSThreads, smem, stream>>>(b, d_geom, d_order, d_counter);
-        FPH_CUDA_TRY(cudaGetLastError());
+    int nk = 0;
+    while (nk < 4 && kern[nk]) ++nk;
+    int* d_stage = nullptr;
+    int* d_counters = nullptr;
+    FPH_CUDA_TRY(cudaMallocAsync(&d_counters, sizeof(int) * 4, stream));
+    FPH_CUDA_TRY(cudaMemsetAsync(d_counters, 0, sizeof(int) * 4, stream));
+    if (nk > 1 && FPH_PDL) {
+        FPH_CUDA_TRY(cudaMallocAsync(&d_stage, sizeof(int) * a.n, stream));
+        FPH_CUDA_TRY(cudaMemsetAsync(d_stage, 0, sizeof(int) * a.n, stream));
     }
+    for (int i = 0; i < nk; ++i) {
+        FPH_CUDA_TRY(cudaFuncSetAttribute(kern[i], cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(blocks);
+        cfg.blockDim = dim3(kSThreads);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = stream;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = (i > 0 && d_stage) ? 1 : 0;
+        FPH_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern[i], b, d_geom, (const int*)d_order, d_counters + i,
+                                        d_stage, i));
+    }
+    FPH_CUDA_TRY(cudaFreeAsync(d_counters, stream));
+    if (d_stage) FPH_CUDA_TRY(cudaFreeAsync(d_stage, stream));
+    if (d_lower) FPH_CUDA_TRY(cudaFreeAsync(d_lower, stream));
     if (d_thr) {
         FPH_CUDA_TRY(cudaFreeAsync(d_thr, stream));
         FPH_CUDA_TRY(cudaFreeAsync(tmp2, stream));

@@ -66,7 +66,7 @@ def main():
                           "staged": s[1], "refined": s[3], "blocks": s[7], "pruned_blocks": s[8],
                           "team_simplices": s[9], "st_A": s[16], "st_Csample": s[17],
                           "st_Cfull": s[18], "cyc_A": s[19], "cyc_B": s[20], "cyc_C": s[21],
-                          "cyc_F": s[22], "searches": s[15], "same": same}),
+                          "cyc_F": s[22], "searches": s[15], "cyc_prologue": s[2], "same": same}),
               flush=True)
 
 
