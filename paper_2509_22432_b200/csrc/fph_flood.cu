@@ -135,6 +135,7 @@ __global__ void setup_kernel(FloodArgs a, SimplexGeom* __restrict__ geom,
         // an estimate suffices -- fp32 row clipping, every `step`-th row
         const int step = rows > 512 ? 4 : (rows > 128 ? 2 : 1);
         const RowClipF cf = make_clip_f(a.g, c[0], c[1], c[2], G.rho);
+#pragma unroll 4
         for (int rr = lane * step; rr < rows; rr += 32 * step) {
             int2 run;
             if (a.subset) {

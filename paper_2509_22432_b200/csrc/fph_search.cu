@@ -1120,6 +1120,8 @@ __global__ void team_thr_kernel(const long long* sum, double beta, int warps, lo
     *thr = t > (double)kTeamMin ? (long long)t : kTeamMin;
 }
 
+constexpr int kSortLo = 8;
+
 __global__ void iota_kernel(int* out, int n) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) out[i] = i;
@@ -1140,13 +1142,15 @@ int launch_search(const FloodArgs& a, const SimplexGeom* d_geom, const int* d_ca
     FPH_CUDA_TRY(cudaMemsetAsync(d_counter, 0, sizeof(int), stream));
     size_t tmp_bytes = 0;
     cub::DeviceRadixSort::SortPairsDescending(nullptr, tmp_bytes, d_cand, d_keys, d_iota, d_order,
-                                              a.n, 0, 24, stream);
+                                              a.n, kSortLo, 24, stream);
     void* tmp = nullptr;
     FPH_CUDA_TRY(cudaMallocAsync(&tmp, tmp_bytes, stream));
-    // 24 key bits: counts above 2^24 only need to sort among themselves
-    // loosely (scheduling order, not correctness)
+    // key bits [kSortLo, 24): the order only schedules the work (largest
+    // first), so counts within 2^kSortLo of each other may come in any
+    // order and counts above 2^24 sort among themselves loosely -- two radix
+    // passes instead of three
     FPH_CUDA_TRY(cub::DeviceRadixSort::SortPairsDescending(tmp, tmp_bytes, d_cand, d_keys, d_iota,
-                                                           d_order, a.n, 0, 24, stream));
+                                                           d_order, a.n, kSortLo, 24, stream));
     int dev = 0, sms = 0, occ = 0;
     FPH_CUDA_TRY(cudaGetDevice(&dev));
     FPH_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
