@@ -62,6 +62,9 @@ constexpr int kSThreads = 32 * kSW;
 #ifndef FPH_PDL
 #define FPH_PDL 1
 #endif
+#ifndef FPH_PREFETCH_CLAIM
+#define FPH_PREFETCH_CLAIM 0
+#endif
 #ifndef FPH_COUNT_SKIP
 #define FPH_COUNT_SKIP 1
 #endif
@@ -1042,7 +1045,7 @@ __global__ void __launch_bounds__(kSThreads, FPH_SEARCH_MINB)
     // team mode: the whole CTA per simplex while the queue (sorted by
     // candidate count, largest first) holds big simplices; then warp mode.
     // One call site of run_simplex: the kernel body is inlined once.
-    int pending = -1;
+    int pending = -1, next = -1;
     bool team = true;
     for (;;) {
 #ifdef FPH_PROLOGUE_CLK
@@ -1064,20 +1067,36 @@ __global__ void __launch_bounds__(kSThreads, FPH_SEARCH_MINB)
             t = pending;
             pending = -1;
         } else {
-            if (lane == 0) t = atomicAdd(counter, 1);
+            // the claim for the NEXT simplex is issued now and consumed on the
+            // next pass, so its atomic round trip overlaps this simplex
+            if (lane == 0) {
+                t = next >= 0 ? next : atomicAdd(counter, 1);
+                next = FPH_PREFETCH_CLAIM ? atomicAdd(counter, 1) : -1;
+            }
             t = __shfl_sync(0xffffffffu, t, 0);
         }
         if (t >= a.n) return;
         const int s = order[t];
         if (a.split && geom[s].stride == 1) continue;  // finished by the pass kernel
-        if (stage && pos > 0) {  // this simplex's previous phase
+        // geometry and vertices on separate lanes, while lane 0 waits for this
+        // simplex's previous phase (the rows it left are read after this)
+        __syncwarp();
+        static_assert(sizeof(SimplexGeom) % 8 == 0 && sizeof(SimplexGeom) <= 8 * 16, "geom words");
+        if (lane >= 16 && lane < 16 + (int)(sizeof(SimplexGeom) / 8))
+            reinterpret_cast<long long*>(&W.G)[lane - 16] =
+                reinterpret_cast<const long long*>(geom + s)[lane - 16];
+        if (lane >= 4 && lane < 8) {
+            const int j = lane - 4;
+            const int id = j <= a.k ? a.simplices[(size_t)s * 4 + j] : -1;
+            W.V.v[j][0] = id >= 0 ? a.landmarks[(size_t)id * 3 + 0] : 0.0;
+            W.V.v[j][1] = id >= 0 ? a.landmarks[(size_t)id * 3 + 1] : 0.0;
+            W.V.v[j][2] = id >= 0 ? a.landmarks[(size_t)id * 3 + 2] : 0.0;
+        }
+        if (stage && pos > 0) {
             if ((team ? threadIdx.x : lane) == 0)
                 while (ld_acquire_i(stage + s) < pos) __nanosleep(64);
             if (team) __syncthreads();
         }
-        __syncwarp();
-        if (lane == 0) W.G = geom[s];
-        if (lane == 0) load_verts(a, s, W.V);
         __syncwarp();
         const Ctx c{&a, W.G, W.V, S.wt,
                     a.subset ? (float)(W.G.rho * W.G.rho * (1.0 + 1e-5)) : INFINITY, s};
