@@ -477,67 +477,6 @@ int fph_flood_samples(const double* points, int64_t n_points, int32_t dim,
     return rc;
 }
 
-int fph_flood_shard(const double* points, int64_t n_points, int32_t dim,
-                    const double* landmarks, int64_t n_landmarks, int32_t max_dim,
-                    const int64_t* counts, const int32_t* const* simplices, int32_t rank,
-                    int32_t world, int32_t grid_resolution, int32_t subset_mode,
-                    double* const* out_interior, int32_t memory, void* stream) {
-    g_err[0] = 0;
-    FPH_TRY(check_cloud(points, n_points, dim));
-    if (max_dim < 1 || max_dim > 3 || grid_resolution < 1 || grid_resolution > 255 ||
-        n_landmarks < 1 || !counts || world < 1 || rank < 0 || rank >= world) {
-        set_error("need 1 <= max_dim <= 3, 1 <= grid_resolution <= 255, 0 <= rank < world");
-        return FPH_EARG;
-    }
-    FPH_TRY(ensure_device());
-    HostCtx hc;
-    FPH_TRY(hc.init(memory, stream));
-    int rc = FPH_OK;
-    {
-        Scratch sc(hc.stream);
-        const double *d_pts, *d_lm;
-        FPH_TRY(stage_in(sc, points, (size_t)n_points * dim, memory, &d_pts));
-        FPH_TRY(stage_in(sc, landmarks, (size_t)n_landmarks * dim, memory, &d_lm));
-        double* lm3;
-        FPH_TRY(sc.alloc(&lm3, (size_t)n_landmarks * 3));
-        pad3_kernel<<<blocks_for(n_landmarks), 256, 0, hc.stream>>>(d_lm, n_landmarks, dim, lm3);
-        count_launches(1);
-        GridStore gs;
-        rc = grid_build(d_pts, (int)n_points, dim, 0.0, g_occupancy, hc.stream, &gs);
-        count_launches(4);
-        FloodTuning tune;
-        tune.pairs_per_task = g_pairs_per_task;
-        tune.profile = g_profile;
-        tune.algo = g_algo;
-        tune.reps_target = g_reps_target;
-        tune.team_threshold = g_team_threshold;
-            tune.exact_pairs = g_exact_pairs;
-            for (int i = 0; i < 4; ++i) tune.exact_cand[i] = g_exact_cand[i];
-        for (int k = 1; k <= max_dim && rc == FPH_OK; ++k) {
-            const long long nk = counts[k];
-            const long long mine = nk > rank ? (nk - 1 - rank) / world + 1 : 0;
-            if (mine == 0) continue;
-            const int32_t* d_s;
-            FPH_TRY(stage_in(sc, simplices[k], (size_t)nk * (k + 1), memory, &d_s));
-            int* s4;
-            FPH_TRY(sc.alloc(&s4, (size_t)mine * 4));
-            pad4_shard_kernel<<<blocks_for(mine), 256, 0, hc.stream>>>(d_s, mine, k, rank, world, s4);
-            count_launches(1);
-            double* d_out = out_interior[k];
-            if (memory == FPH_MEM_HOST) FPH_TRY(sc.alloc(&d_out, (size_t)mine));
-            rc = flood_interior(gs.grid, lm3, s4, (int)mine, k, grid_resolution, subset_mode, d_out,
-                                tune, hc.stream);
-            count_launches(4);
-            if (rc == FPH_OK && memory == FPH_MEM_HOST)
-                FPH_CUDA_TRY(cudaMemcpyAsync(out_interior[k], d_out, sizeof(double) * mine,
-                                             cudaMemcpyDeviceToHost, hc.stream));
-        }
-        gs.free_all(hc.stream);
-    }
-    if (memory == FPH_MEM_HOST) FPH_CUDA_TRY(cudaStreamSynchronize(hc.stream));
-    return rc;
-}
-
 #ifndef FPH_CONCURRENT_DIMS
 #define FPH_CONCURRENT_DIMS 1
 #endif
@@ -582,6 +521,71 @@ static int run_interiors(const Grid& g, const double* lm3, int* const* s4, doubl
         FPH_CUDA_TRY(cudaEventRecord(p1, stream));
         profile_push(p0, p1);
     }
+    return rc;
+}
+
+int fph_flood_shard(const double* points, int64_t n_points, int32_t dim,
+                    const double* landmarks, int64_t n_landmarks, int32_t max_dim,
+                    const int64_t* counts, const int32_t* const* simplices, int32_t rank,
+                    int32_t world, int32_t grid_resolution, int32_t subset_mode,
+                    double* const* out_interior, int32_t memory, void* stream) {
+    g_err[0] = 0;
+    FPH_TRY(check_cloud(points, n_points, dim));
+    if (max_dim < 1 || max_dim > 3 || grid_resolution < 1 || grid_resolution > 255 ||
+        n_landmarks < 1 || !counts || world < 1 || rank < 0 || rank >= world) {
+        set_error("need 1 <= max_dim <= 3, 1 <= grid_resolution <= 255, 0 <= rank < world");
+        return FPH_EARG;
+    }
+    FPH_TRY(ensure_device());
+    HostCtx hc;
+    FPH_TRY(hc.init(memory, stream));
+    int rc = FPH_OK;
+    {
+        Scratch sc(hc.stream);
+        const double *d_pts, *d_lm;
+        FPH_TRY(stage_in(sc, points, (size_t)n_points * dim, memory, &d_pts));
+        FPH_TRY(stage_in(sc, landmarks, (size_t)n_landmarks * dim, memory, &d_lm));
+        double* lm3;
+        FPH_TRY(sc.alloc(&lm3, (size_t)n_landmarks * 3));
+        pad3_kernel<<<blocks_for(n_landmarks), 256, 0, hc.stream>>>(d_lm, n_landmarks, dim, lm3);
+        count_launches(1);
+        GridStore gs;
+        rc = grid_build(d_pts, (int)n_points, dim, 0.0, g_occupancy, hc.stream, &gs);
+        count_launches(4);
+        FloodTuning tune;
+        tune.pairs_per_task = g_pairs_per_task;
+        tune.profile = g_profile;
+        tune.algo = g_algo;
+        tune.reps_target = g_reps_target;
+        tune.team_threshold = g_team_threshold;
+            tune.exact_pairs = g_exact_pairs;
+            for (int i = 0; i < 4; ++i) tune.exact_cand[i] = g_exact_cand[i];
+        int64_t mine[4] = {0, 0, 0, 0};
+        int* s4[4] = {nullptr, nullptr, nullptr, nullptr};
+        double* d_out[4] = {nullptr, nullptr, nullptr, nullptr};
+        for (int k = 1; k <= max_dim && rc == FPH_OK; ++k) {
+            const long long nk = counts[k];
+            mine[k] = nk > rank ? (nk - 1 - rank) / world + 1 : 0;
+            if (mine[k] == 0) continue;
+            const int32_t* d_s;
+            FPH_TRY(stage_in(sc, simplices[k], (size_t)nk * (k + 1), memory, &d_s));
+            FPH_TRY(sc.alloc(&s4[k], (size_t)mine[k] * 4));
+            pad4_shard_kernel<<<blocks_for(mine[k]), 256, 0, hc.stream>>>(d_s, mine[k], k, rank,
+                                                                         world, s4[k]);
+            count_launches(1);
+            d_out[k] = out_interior[k];
+            if (memory == FPH_MEM_HOST) FPH_TRY(sc.alloc(&d_out[k], (size_t)mine[k]));
+        }
+        // every dimension's share concurrently, as in fph_flood_filtration
+        if (rc == FPH_OK) rc = run_interiors(gs.grid, lm3, s4, d_out, mine, max_dim,
+                                            grid_resolution, subset_mode, tune, hc.stream);
+        for (int k = 1; k <= max_dim && rc == FPH_OK; ++k)
+            if (mine[k] > 0 && memory == FPH_MEM_HOST)
+                FPH_CUDA_TRY(cudaMemcpyAsync(out_interior[k], d_out[k], sizeof(double) * mine[k],
+                                             cudaMemcpyDeviceToHost, hc.stream));
+        gs.free_all(hc.stream);
+    }
+    if (memory == FPH_MEM_HOST) FPH_CUDA_TRY(cudaStreamSynchronize(hc.stream));
     return rc;
 }
 
