@@ -1078,6 +1078,16 @@ __global__ void __launch_bounds__(kSThreads, FPH_SEARCH_MINB)
         if (t >= a.n) return;
         const int s = order[t];
         if (a.split && geom[s].stride == 1) continue;  // finished by the pass kernel
+        // Simplices valued by one exact pass in phase A have no B or C: those
+        // kernels skip them outright and F waits for A's flag instead.
+        int need = pos;
+        if (stage && (kPh == 4 || kPh == 5 || kPh == 6)) {
+            const long long C = a.cand_count[s];
+            if ((double)C * (double)a.P <= a.exact_pairs || C <= a.exact_cand[a.k]) {
+                if (kPh != 4) continue;
+                need = 1;
+            }
+        }
         // geometry and vertices on separate lanes, while lane 0 waits for this
         // simplex's previous phase (the rows it left are read after this)
         __syncwarp();
@@ -1094,7 +1104,7 @@ __global__ void __launch_bounds__(kSThreads, FPH_SEARCH_MINB)
         }
         if (stage && pos > 0) {
             if ((team ? threadIdx.x : lane) == 0)
-                while (ld_acquire_i(stage + s) < pos) __nanosleep(64);
+                while (ld_acquire_i(stage + s) < need) __nanosleep(64);
             if (team) __syncthreads();
         }
         __syncwarp();
