@@ -477,6 +477,9 @@ int fph_flood_samples(const double* points, int64_t n_points, int32_t dim,
     return rc;
 }
 
+#ifndef FPH_DIM_PRIORITY
+#define FPH_DIM_PRIORITY 1
+#endif
 #ifndef FPH_CONCURRENT_DIMS
 #define FPH_CONCURRENT_DIMS 1
 #endif
@@ -502,7 +505,14 @@ static int run_interiors(const Grid& g, const double* lm3, int* const* s4, doubl
     int rc = FPH_OK;
     for (int k = 1; k <= max_dim && rc == FPH_OK; ++k) {
         if (counts[k] == 0) continue;
-        if (!side[k]) FPH_CUDA_TRY(cudaStreamCreateWithFlags(&side[k], cudaStreamNonBlocking));
+        if (!side[k]) {
+            // higher dimensions carry the longest chains: their CTAs are
+            // placed first, lower dimensions fill the tails
+            int lo = 0, hi = 0;
+            FPH_CUDA_TRY(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+            const int prio = FPH_DIM_PRIORITY ? (k >= 2 ? hi : lo) : 0;
+            FPH_CUDA_TRY(cudaStreamCreateWithPriority(&side[k], cudaStreamNonBlocking, prio));
+        }
         cudaStream_t sk = FPH_CONCURRENT_DIMS ? side[k] : stream;
         FPH_CUDA_TRY(cudaStreamWaitEvent(sk, fork, 0));
         rc = flood_interior(g, lm3, s4[k], (int)counts[k], k, grid_resolution, subset_mode,
