@@ -385,7 +385,7 @@ def e2e_host(lib, native, w, args):
     for _ in range(2):
         call()
     times = []
-    for _ in range(max(3, args.steps)):
+    for _ in range(max(10, args.steps)):  # wall-clock: a median over >= 10 calls
         t0 = time.perf_counter()
         call()
         times.append(time.perf_counter() - t0)
