@@ -289,11 +289,7 @@ def run_ours(args):
                                               "staged_phase_a": stats[16] / args.steps,
                                               "staged_block_sampling": stats[17] / args.steps,
                                               "staged_block_exact": stats[18] / args.steps,
-                                              "phase_a_pairs": stats[14] / args.steps,
-                                              "block_sampling_pairs_active_lanes": stats[10] / args.steps,
-                                              "block_sampling_pairs_executed": stats[11] / args.steps,
-                                              "block_exact_pairs_active_lanes": stats[12] / args.steps,
-                                              "block_exact_pairs_executed": stats[13] / args.steps}}
+                                              "phase_a_pairs": stats[14] / args.steps}}
         if world == 1 and not args.no_cpu_baseline:
             result["cpu_baseline"] = cpu_baseline(w, args.cpu_seconds)
     if world > 1 or args.force_sharded:

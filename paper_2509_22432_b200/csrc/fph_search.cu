@@ -65,6 +65,9 @@ constexpr int kSThreads = 32 * kSW;
 #ifndef FPH_PREFETCH_CLAIM
 #define FPH_PREFETCH_CLAIM 0
 #endif
+#ifndef FPH_LANE_STATS
+#define FPH_LANE_STATS 0  // active-lane pair counters of phase C (stats[10..13])
+#endif
 #ifndef FPH_COUNT_SKIP
 #define FPH_COUNT_SKIP 1
 #endif
@@ -165,6 +168,7 @@ struct Ctx {
     const double* wt;
     float thr;  // simplex ball (Lemma 4.2) on |a|^2; +inf when unpruned
     int s;
+    double cnt;  // the simplex's candidate count (a.cand_count[s])
 };
 
 struct PointF {
@@ -520,7 +524,7 @@ __device__ void reps_pass(const Ctx& c, WarpSmem& W, int stride, float* vals, co
     for (int rb = tm.rank * 32; rb < rows; rb += tm.size * 32) {
         const Batch bt = row_batch(rw, W, rb);
         const int total = bt.total;
-        const int first = (int)((stride - fbase % stride) % stride);
+        const int first = stride == 1 ? 0 : (int)((stride - fbase % stride) % stride);
         const int nsel = total > first ? (total - first - 1) / stride + 1 : 0;
 #if FPH_REPS_2WIN
         // two windows of loads in flight (phase A runs in its own kernel, so
@@ -684,9 +688,10 @@ __device__ void search_block(const Ctx& c, WarpSmem& W, int nb, float* vals, flo
         // a region expected to hold few candidates (the simplex's count
         // scaled by the area ratio, an over-estimate for volume data) skips
         // the counting pass
-        const double frac = c.G.rho > 0.0 ? fmin(1.0, (R * R) / (c.G.rho * c.G.rho)) : 1.0;
-        const bool small = FPH_COUNT_SKIP && a.subset &&
-                           (double)a.cand_count[c.s] * frac <= 2.0 * a.reps_target;
+        // count x min(1, R^2 / rho^2) <= 2 reps, without the division
+        const double rho2 = c.G.rho * c.G.rho;
+        const bool small = FPH_COUNT_SKIP && a.subset && rho2 > 0.0 &&
+                           c.cnt * fmin(rho2, R * R) <= 2.0 * a.reps_target * rho2;
         if (pass == 0 && !small) {
             // count the region; a large one is sampled first to tighten U
             long long cnt = 0;
@@ -698,7 +703,9 @@ __device__ void search_block(const Ctx& c, WarpSmem& W, int nb, float* vals, flo
             int tile_n = 0;
             long long fbase = 0;
             unsigned long long stg = 0;
+#if FPH_LANE_STATS
             const unsigned act = __ballot_sync(0xffffffffu, active);
+#endif
             auto take = [&](bool keep, float ax, float ay, float az, float aw) {
                 tile_n = tile_push(W, tile_n, keep, ax, ay, az, aw);
                 if (tile_n > kWT - 32) {
@@ -730,7 +737,7 @@ __device__ void search_block(const Ctx& c, WarpSmem& W, int nb, float* vals, flo
                         if (f0 + 32 < total) take(v1 && accept(x1, y1, z1, w1), x1, y1, z1, w1);
                     }
                 } else {
-                    const int first = (int)((stride - fbase % stride) % stride);
+                    const int first = stride == 1 ? 0 : (int)((stride - fbase % stride) % stride);
                     const int nsel = total > first ? (total - first - 1) / stride + 1 : 0;
                     for (int i0 = 0; i0 < nsel; i0 += 32) {
                         bool keep = false;
@@ -753,8 +760,10 @@ __device__ void search_block(const Ctx& c, WarpSmem& W, int nb, float* vals, flo
             }
             st[pass] += stg;
             st[2] += stg * (unsigned long long)nb;
+#if FPH_LANE_STATS
             st[3 + 2 * pass] += stg * (unsigned long long)__popc(act);
             st[4 + 2 * pass] += stg * (unsigned long long)nb;
+#endif
             best = tm.lane_min(best);
         }
         if (pass == 0) {
@@ -1109,7 +1118,8 @@ __global__ void __launch_bounds__(kSThreads, FPH_SEARCH_MINB)
         }
         __syncwarp();
         const Ctx c{&a, W.G, W.V, S.wt,
-                    a.subset ? (float)(W.G.rho * W.G.rho * (1.0 + 1e-5)) : INFINITY, s};
+                    a.subset ? (float)(W.G.rho * W.G.rho * (1.0 + 1e-5)) : INFINITY, s,
+                    (double)a.cand_count[s]};
         const Team tm = team ? Team{w, kSW, &S.team} : Team{0, 1, nullptr};
         float* vals = a.perpoint + (size_t)s * a.P;
         if (kSV) {
