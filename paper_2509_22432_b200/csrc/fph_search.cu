@@ -27,6 +27,8 @@
 // above is taken with it, so the result is the reference's float64 value.
 #include <cub/cub.cuh>
 
+#include <cstdlib>
+
 #include "fph_dev.cuh"
 
 namespace fph {
@@ -1201,7 +1203,11 @@ int launch_search(const FloodArgs& a, const SimplexGeom* d_geom, const int* d_ca
     // (phase C another -16%); FPH_PDL chains them per simplex so tails
     // overlap.  Small complexes keep one kernel, where the extra launches and
     // tails do not amortise.
-    const bool two = FPH_TWO_KERNELS && !a.split && a.n >= 10000;
+    // FPH_SPLIT_MIN_SIMPLICES (environment) overrides the 10 000 cut-off;
+    // the tests set it to 0 to run the small golden complexes through the chain
+    long long split_min = 10000;
+    if (const char* e = getenv("FPH_SPLIT_MIN_SIMPLICES")) split_min = atoll(e);
+    const bool two = FPH_TWO_KERNELS && !a.split && a.n >= split_min;
     using K = void (*)(const FloodArgs, const SimplexGeom*, const int*, int*, int*, int);
     K kern[4] = {nullptr, nullptr, nullptr, nullptr};
     float* d_lower = nullptr;

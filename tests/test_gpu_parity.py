@@ -188,6 +188,22 @@ def test_both_algorithms_golden(algo_switch, algo, reps, team, name):
         assert np.array_equal(np.sqrt(sq[k]), want), k
 
 
+@pytest.mark.parametrize("team", [0, 1, 2**30])
+@pytest.mark.parametrize("name", G.cases("flood"))
+def test_phase_kernel_chain_golden(algo_switch, monkeypatch, team, name):
+    """The four phase kernels chained per simplex (PDL + stage flags; the
+    default for complexes >= 10 000 simplices) forced onto every golden
+    complex, with warp-only, CTA-team-only and auto team scheduling."""
+    monkeypatch.setenv("FPH_SPLIT_MIN_SIMPLICES", "0")
+    algo_switch(1, 0, team)
+    z = G.load("flood", name)
+    tri = C.triangulation(z["tri_points"], G.simplices_by_dim(z))
+    subset = str(z["landmark_mode"]) == "subset"
+    sq = flood_sq_values(z["points"], tri, int(z["grid_resolution"]), subset)
+    for k, want in G.values_by_dim(z).items():
+        assert np.array_equal(np.sqrt(sq[k]), want), k
+
+
 @pytest.mark.parametrize("name", G.cases("sampler"))
 def test_uniform_random_sampler_golden(name):
     """Reference uniform-random sampler (filtration.py:303): same Philox draws
