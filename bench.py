@@ -490,9 +490,16 @@ def main():
         args.warmup = 3
     if args.profile:
         return run_profile(args)
+    # stdout carries exactly one JSON line: anything libraries print there
+    # (NCCL's version banner, CUDA/driver notices) goes to stderr instead
+    sys.stdout.flush()
+    json_out = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
     res = run_reference(args) if args.impl == "reference" else run_ours(args)
+    sys.stdout.flush()
     if res is not None:
-        print(json.dumps(res))
+        json_out.write(json.dumps(res) + "\n")
+    json_out.flush()
 
 
 if __name__ == "__main__":
