@@ -9,10 +9,10 @@
 //
 // Layout: one CTA per SM (cooperative launch, all CTAs co-resident), each
 // owning a contiguous slice of the cloud.  When a slice fits, its float64
-// coordinates live in shared memory (SoA) and the running minimum in
-// registers for the whole run -- a 1M-point cloud never touches HBM after
-// the first load.  Larger clouds stream coordinates and the running minimum
-// through L2/HBM.  Per iteration each CTA publishes its (value, index) to a
+// coordinates live in shared memory (SoA, padded to PT x 1024 points, PT a
+// template parameter so the per-point update is branch-free) and the running
+// minimum in registers for the whole run -- a 1M-point cloud never touches
+// HBM after the first load.  Per iteration each CTA publishes its (value, index) to a
 // double-buffered slot array and bumps one monotone arrival counter; one
 // thread per CTA polls the counter (ld.acquire) until all CTAs of this
 // iteration arrived, then its warp reads every slot and reduces them.  All
@@ -39,7 +39,7 @@ namespace fph {
 namespace {
 
 constexpr int kFpsThreads = 1024;
-constexpr int kFpsMaxPT = 9;  // points per thread in the shared-memory variant
+constexpr int kFpsMaxPT = 9;  // points per thread in the shared-memory variants
 constexpr int kMaxSlots = 160;  // CTAs per exchange of the batched (coordinate-carrying) kernel
 constexpr int kStaticSmem = 4 * kMaxSlots * 8 + 1024;  // batched kernel: stage + reduction scratch
 
@@ -245,69 +245,112 @@ __device__ __forceinline__ Winner exchange_argmax_xyz(double bv, int bi, const d
     return wn;
 }
 
-template <bool kSmem>
+// Streaming variant (slices beyond shared memory; fps_run only takes it
+// for k == 1, larger k goes to the tiled kernel): coordinates and running
+// minima stream through L2/HBM.
 __global__ void __launch_bounds__(kFpsThreads, 1)
     fps_kernel(const double* __restrict__ px, const double* __restrict__ py,
                const double* __restrict__ pz, int n, int k, int start, int chunk,
                double* __restrict__ mind, Slot* slots, unsigned long long* arrived,
                long long* __restrict__ out) {
-    extern __shared__ double sm[];
     __shared__ double red_v[32];
     __shared__ int red_i[33];
     const int beg = blockIdx.x * chunk;
-    const int end = min(n, beg + chunk);
-    const int cnt = max(0, end - beg);
-    double* sx = sm;
-    double* sy = sm + chunk;
-    double* sz = sm + 2 * chunk;
-    double md[kSmem ? kFpsMaxPT : 1];
-    if (kSmem) {
-        for (int j = threadIdx.x; j < cnt; j += blockDim.x) {
-            sx[j] = px[beg + j];
-            sy[j] = py[beg + j];
-            sz[j] = pz[beg + j];
-        }
-#pragma unroll
-        for (int t = 0; t < kFpsMaxPT; ++t) md[t] = INFINITY;
-        __syncthreads();
-    } else {
-        for (int j = threadIdx.x; j < cnt; j += blockDim.x) mind[beg + j] = INFINITY;
-    }
+    const int cnt = max(0, min(n, beg + chunk) - beg);
+    for (int j = threadIdx.x; j < cnt; j += blockDim.x) mind[beg + j] = INFINITY;
     int cur = start;
     if (blockIdx.x == 0 && threadIdx.x == 0) out[0] = start;
+    const int G = gridDim.x, rs = repl_stride(G);
     for (int it = 1; it <= k; ++it) {
         const double qx = px[cur], qy = py[cur], qz = pz[cur];
         double bv = -INFINITY;
         int bi = 0x7fffffff;
-        if (kSmem) {
-#pragma unroll
-            for (int t = 0; t < kFpsMaxPT; ++t) {
-                int j = threadIdx.x + t * kFpsThreads;
-                if (j < cnt) {
-                    int gi = beg + j;
-                    double d = sq64(sx[j], sy[j], sz[j], qx, qy, qz);
-                    double m = gi == cur ? -1.0 : fmin(md[t], d);
-                    md[t] = m;
-                    better(bv, bi, m, gi);
-                }
-            }
-        } else {
-            for (int j = threadIdx.x; j < cnt; j += blockDim.x) {
-                int gi = beg + j;
-                double d = sq64(px[gi], py[gi], pz[gi], qx, qy, qz);
-                double m = gi == cur ? -1.0 : fmin(mind[gi], d);
-                mind[gi] = m;
-                better(bv, bi, m, gi);
-            }
+        for (int j = threadIdx.x; j < cnt; j += blockDim.x) {
+            const int gi = beg + j;
+            const double d = sq64(px[gi], py[gi], pz[gi], qx, qy, qz);
+            const double m = gi == cur ? -1.0 : fmin(mind[gi], d);
+            mind[gi] = m;
+            better(bv, bi, m, gi);
         }
         if (it == k) break;
-        const int G = gridDim.x, rs = repl_stride(G);
         cur = exchange_argmax(bv, bi, slots + (it & 1) * kRepl * rs, G, blockIdx.x, arrived,
                               (unsigned long long)G * it, red_v, red_i, rs, kRepl);
         if (blockIdx.x == 0 && threadIdx.x == 0) out[it] = cur;
     }
 }
 
+// Resident variant with PT points per thread, branch-free: the shared slice
+// is padded to PT x 1024 points whose running minimum starts at -inf (a
+// padded point never wins: d < -inf is false).  Within a thread the global
+// index ascends with t, so a strict `>` keeps the lowest index among equal
+// values; the min is a compare-select (no NaN handling: coordinates are
+// finite, and d >= +0 so no signed-zero case).  ~23 instructions per point
+// instead of ~32 plus a branch.
+template <int PT>
+__global__ void __launch_bounds__(kFpsThreads, 1)
+    fps_resident_kernel(const double* __restrict__ px, const double* __restrict__ py,
+                        const double* __restrict__ pz, int n, int k, int start, int chunk,
+                        Slot* slots, unsigned long long* arrived, long long* __restrict__ out) {
+    extern __shared__ double sm[];
+    __shared__ double red_v[32];
+    __shared__ int red_i[33];
+    constexpr int kSlice = PT * kFpsThreads;
+    const int beg = blockIdx.x * chunk;
+    const int cnt = max(0, min(n, beg + chunk) - beg);
+    double* sx = sm;
+    double* sy = sm + kSlice;
+    double* sz = sm + 2 * kSlice;
+    for (int j = threadIdx.x; j < kSlice; j += blockDim.x) {
+        const bool in = j < cnt;
+        sx[j] = in ? px[beg + j] : 0.0;
+        sy[j] = in ? py[beg + j] : 0.0;
+        sz[j] = in ? pz[beg + j] : 0.0;
+    }
+    double md[PT];
+#pragma unroll
+    for (int t = 0; t < PT; ++t) md[t] = (int)threadIdx.x + t * kFpsThreads < cnt ? INFINITY : -INFINITY;
+    __syncthreads();
+    int cur = start;
+    if (blockIdx.x == 0 && threadIdx.x == 0) out[0] = start;
+    const int G = gridDim.x, rs = repl_stride(G);
+    for (int it = 1; it <= k; ++it) {
+        const double qx = px[cur], qy = py[cur], qz = pz[cur];
+        // slot t of this thread holds the new landmark iff t * 1024 == jc
+        const int jc = cur >= beg && cur < beg + cnt ? cur - beg - (int)threadIdx.x : -1;
+        double bv = -INFINITY;
+        int bi = 0x7fffffff;
+#pragma unroll
+        for (int t = 0; t < PT; ++t) {
+            const int j = threadIdx.x + t * kFpsThreads;
+            const double d = sq64(sx[j], sy[j], sz[j], qx, qy, qz);
+            double m = d < md[t] ? d : md[t];
+            m = jc == t * kFpsThreads ? -1.0 : m;
+            md[t] = m;
+            if (m > bv) {
+                bv = m;
+                bi = beg + j;
+            }
+        }
+        if (it == k) break;
+        cur = exchange_argmax(bv, bi, slots + (it & 1) * kRepl * rs, G, blockIdx.x, arrived,
+                              (unsigned long long)G * it, red_v, red_i, rs, kRepl);
+        if (blockIdx.x == 0 && threadIdx.x == 0) out[it] = cur;
+    }
+}
+
+template <int PT>
+int launch_resident(const double* d_x, const double* d_y, const double* d_z, int n, int k,
+                    int start, int chunk, int G, Slot* slots, unsigned long long* arrived,
+                    long long* d_out, cudaStream_t stream) {
+    const size_t smem = sizeof(double) * 3 * PT * kFpsThreads;
+    FPH_CUDA_TRY(cudaFuncSetAttribute(fps_resident_kernel<PT>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    void* args[] = {(void*)&d_x, (void*)&d_y,   (void*)&d_z,   (void*)&n,      (void*)&k,
+                    (void*)&start, (void*)&chunk, (void*)&slots, (void*)&arrived, (void*)&d_out};
+    FPH_CUDA_TRY(cudaLaunchCooperativeKernel((void*)fps_resident_kernel<PT>, dim3(G),
+                                             dim3(kFpsThreads), args, smem, stream));
+    return FPH_OK;
+}
 
 // ------------------------------------------------------------ tiled variant
 constexpr int kTileP = 256;  // points per tile
@@ -543,6 +586,7 @@ int fps_tiled(const double* d_x, const double* d_y, const double* d_z, int n, in
 // cloud at a time, exchanging through their own slots and counter, so
 // ngroups = gridDim / cpg clouds advance concurrently instead of every cloud
 // using (and waiting on) the whole GPU.
+template <int PT>
 __global__ void __launch_bounds__(kFpsThreads, 1)
     fps_batched_kernel(const double* __restrict__ px, const double* __restrict__ py,
                        const double* __restrict__ pz, int batch, int n, int k, int start, int cpg,
@@ -552,42 +596,47 @@ __global__ void __launch_bounds__(kFpsThreads, 1)
     __shared__ double red_v[32];
     __shared__ int red_i[34];
     __shared__ __align__(16) double stage[4 * kMaxSlots];
+    constexpr int kSlice = PT * kFpsThreads;  // padded as in fps_resident_kernel
     const int ngroups = gridDim.x / cpg;
     const int g = blockIdx.x / cpg, r = blockIdx.x % cpg;
     if (g >= ngroups) return;
     double* sx = sm;
-    double* sy = sm + chunk;
-    double* sz = sm + 2 * chunk;
+    double* sy = sm + kSlice;
+    double* sz = sm + 2 * kSlice;
     SlotXYZ* gslots = reinterpret_cast<SlotXYZ*>(slots) + (size_t)g * 2 * cpg;
     int seq = 0;
     for (int c = g; c < batch; c += ngroups, ++seq) {
         const long long cb = (long long)c * n;
         const int beg = r * chunk, cnt = max(0, min(n, beg + chunk) - beg);
         __syncthreads();
-        for (int j = threadIdx.x; j < cnt; j += blockDim.x) {
-            sx[j] = px[cb + beg + j];
-            sy[j] = py[cb + beg + j];
-            sz[j] = pz[cb + beg + j];
+        for (int j = threadIdx.x; j < kSlice; j += blockDim.x) {
+            const bool in = j < cnt;
+            sx[j] = in ? px[cb + beg + j] : 0.0;
+            sy[j] = in ? py[cb + beg + j] : 0.0;
+            sz[j] = in ? pz[cb + beg + j] : 0.0;
         }
-        double md[kFpsMaxPT];
+        double md[PT];
 #pragma unroll
-        for (int t = 0; t < kFpsMaxPT; ++t) md[t] = INFINITY;
+        for (int t = 0; t < PT; ++t)
+            md[t] = (int)threadIdx.x + t * kFpsThreads < cnt ? INFINITY : -INFINITY;
         __syncthreads();
         int cur = start;
         if (r == 0 && threadIdx.x == 0) out[(long long)c * k] = start;
         double qx = px[cb + cur], qy = py[cb + cur], qz = pz[cb + cur];
         for (int it = 1; it < k; ++it) {
+            const int jc = cur >= beg && cur < beg + cnt ? cur - beg - (int)threadIdx.x : -1;
             double bv = -INFINITY;
             int bi = 0x7fffffff;
 #pragma unroll
-            for (int t = 0; t < kFpsMaxPT; ++t) {
+            for (int t = 0; t < PT; ++t) {
                 const int j = threadIdx.x + t * kFpsThreads;
-                if (j < cnt) {
-                    const int gi = beg + j;
-                    const double d = sq64(sx[j], sy[j], sz[j], qx, qy, qz);
-                    const double m = gi == cur ? -1.0 : fmin(md[t], d);
-                    md[t] = m;
-                    better(bv, bi, m, gi);
+                const double d = sq64(sx[j], sy[j], sz[j], qx, qy, qz);
+                double m = d < md[t] ? d : md[t];
+                m = jc == t * kFpsThreads ? -1.0 : m;
+                md[t] = m;
+                if (m > bv) {
+                    bv = m;
+                    bi = beg + j;
                 }
             }
             const long long tag = (long long)seq * (k - 1) + it;  // group-wide iteration
@@ -601,6 +650,21 @@ __global__ void __launch_bounds__(kFpsThreads, 1)
             if (r == 0 && threadIdx.x == 0) out[(long long)c * k + it] = cur;
         }
     }
+}
+
+template <int PT>
+int launch_batched(const double* d_x, const double* d_y, const double* d_z, int batch, int n,
+                   int k, int start, int cpg, int chunk, int grid, Slot* slots,
+                   unsigned long long* arrived, long long* d_out, cudaStream_t stream) {
+    const size_t smem = sizeof(double) * 3 * PT * kFpsThreads;
+    FPH_CUDA_TRY(cudaFuncSetAttribute(fps_batched_kernel<PT>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    void* args[] = {(void*)&d_x, (void*)&d_y, (void*)&d_z,   (void*)&batch, (void*)&n,
+                    (void*)&k,   (void*)&start, (void*)&cpg, (void*)&chunk, (void*)&slots,
+                    (void*)&arrived, (void*)&d_out};
+    FPH_CUDA_TRY(cudaLaunchCooperativeKernel((void*)fps_batched_kernel<PT>, dim3(grid),
+                                             dim3(kFpsThreads), args, smem, stream));
+    return FPH_OK;
 }
 
 }  // namespace
@@ -635,18 +699,33 @@ int fps_run(const double* d_x, const double* d_y, const double* d_z, int n, int 
     FPH_CUDA_TRY(cudaMallocAsync(&arrived, sizeof(unsigned long long), stream));
     FPH_CUDA_TRY(cudaMemsetAsync(arrived, 0, sizeof(unsigned long long), stream));
     if (!use_smem) FPH_CUDA_TRY(cudaMallocAsync(&mind, sizeof(double) * n, stream));
-    void* args[] = {(void*)&d_x,   (void*)&d_y,  (void*)&d_z,   (void*)&n,
-                    (void*)&k,     (void*)&start, (void*)&chunk, (void*)&mind,
-                    (void*)&slots, (void*)&arrived, (void*)&d_out};
     if (use_smem) {
-        FPH_CUDA_TRY(cudaFuncSetAttribute(fps_kernel<true>,
-                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          (int)smem));
-        FPH_CUDA_TRY(cudaLaunchCooperativeKernel((void*)fps_kernel<true>, dim3(G),
-                                                 dim3(kFpsThreads), args, smem, stream));
+        int rc = FPH_OK;
+#define FPH_RESIDENT_CASE(P)                                                                   \
+    case P:                                                                                    \
+        rc = launch_resident<P>(d_x, d_y, d_z, n, k, start, chunk, G, slots, arrived, d_out,   \
+                                stream);                                                       \
+        break;
+        switch ((chunk + kFpsThreads - 1) / kFpsThreads) {
+            FPH_RESIDENT_CASE(1)
+            FPH_RESIDENT_CASE(2)
+            FPH_RESIDENT_CASE(3)
+            FPH_RESIDENT_CASE(4)
+            FPH_RESIDENT_CASE(5)
+            FPH_RESIDENT_CASE(6)
+            FPH_RESIDENT_CASE(7)
+            FPH_RESIDENT_CASE(8)
+            default:
+                FPH_RESIDENT_CASE(9)
+        }
+#undef FPH_RESIDENT_CASE
+        if (rc != FPH_OK) return rc;
     } else {
-        FPH_CUDA_TRY(cudaLaunchCooperativeKernel((void*)fps_kernel<false>, dim3(G),
-                                                 dim3(kFpsThreads), args, 0, stream));
+        void* args[] = {(void*)&d_x,   (void*)&d_y,  (void*)&d_z,   (void*)&n,
+                        (void*)&k,     (void*)&start, (void*)&chunk, (void*)&mind,
+                        (void*)&slots, (void*)&arrived, (void*)&d_out};
+        FPH_CUDA_TRY(cudaLaunchCooperativeKernel((void*)fps_kernel, dim3(G), dim3(kFpsThreads),
+                                                 args, 0, stream));
     }
     FPH_CUDA_TRY(cudaGetLastError());
     FPH_CUDA_TRY(cudaFreeAsync(slots, stream));
@@ -675,20 +754,32 @@ int fps_batched(const double* d_x, const double* d_y, const double* d_z, int bat
     if (cpg > sms || cpg > kMaxSlots) return FPH_EARG;  // caller falls back to one cloud at a time
     const int ngroups = min(sms / cpg, batch);
     const int chunk = (n + cpg - 1) / cpg;
-    const size_t smem = (size_t)chunk * 3 * sizeof(double);
     Slot* slots = nullptr;
     unsigned long long* arrived = nullptr;
     FPH_CUDA_TRY(cudaMallocAsync(&slots, sizeof(SlotXYZ) * 2 * cpg * ngroups, stream));
     FPH_CUDA_TRY(cudaMallocAsync(&arrived, sizeof(unsigned long long) * ngroups, stream));
     FPH_CUDA_TRY(cudaMemsetAsync(arrived, 0, sizeof(unsigned long long) * ngroups, stream));
-    FPH_CUDA_TRY(cudaFuncSetAttribute(fps_batched_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)smem));
-    int grid = ngroups * cpg;
-    int b = batch, nn = n, kk = k, st = start, c = cpg, ch = chunk;
-    void* args[] = {(void*)&d_x, (void*)&d_y, (void*)&d_z, (void*)&b,     (void*)&nn,      (void*)&kk,
-                    (void*)&st,  (void*)&c,   (void*)&ch,  (void*)&slots, (void*)&arrived, (void*)&d_out};
-    FPH_CUDA_TRY(cudaLaunchCooperativeKernel((void*)fps_batched_kernel, dim3(grid),
-                                             dim3(kFpsThreads), args, smem, stream));
+    const int grid = ngroups * cpg;
+    int rc = FPH_OK;
+#define FPH_BATCHED_CASE(P)                                                                    \
+    case P:                                                                                    \
+        rc = launch_batched<P>(d_x, d_y, d_z, batch, n, k, start, cpg, chunk, grid, slots,     \
+                               arrived, d_out, stream);                                        \
+        break;
+    switch ((chunk + kFpsThreads - 1) / kFpsThreads) {
+        FPH_BATCHED_CASE(1)
+        FPH_BATCHED_CASE(2)
+        FPH_BATCHED_CASE(3)
+        FPH_BATCHED_CASE(4)
+        FPH_BATCHED_CASE(5)
+        FPH_BATCHED_CASE(6)
+        FPH_BATCHED_CASE(7)
+        FPH_BATCHED_CASE(8)
+        default:
+            FPH_BATCHED_CASE(9)
+    }
+#undef FPH_BATCHED_CASE
+    if (rc != FPH_OK) return rc;
     FPH_CUDA_TRY(cudaGetLastError());
     FPH_CUDA_TRY(cudaFreeAsync(slots, stream));
     FPH_CUDA_TRY(cudaFreeAsync(arrived, stream));

@@ -56,6 +56,17 @@ def test_fps_batched_matches_oracle(batch, n, k):
         np.testing.assert_array_equal(got[b], oracle.fps(clouds[b], k, 3))
 
 
+@pytest.mark.parametrize("pt", [3, 4, 5, 6, 7, 8, 9])
+def test_fps_resident_points_per_thread(pt):
+    """Every PT instantiation of the resident kernel (PT x 1024 points per
+    CTA slot, padded), on coordinates quantised to 1/8 so ties are common and
+    a ragged last slice."""
+    n = 148 * (pt * 1024 - 300) + 77
+    pts = np.round(np.random.default_rng(pt).random((n, 3)) * 64) / 8
+    got = farthest_point_sampling(pts, 120, pt)
+    np.testing.assert_array_equal(got, oracle.fps(pts, 120, pt))
+
+
 def test_fps_ties_uniform_grid():
     # a lattice is full of exact ties: lowest index must win every time
     g = np.stack(np.meshgrid(np.arange(40.0), np.arange(40.0), np.arange(5.0)), -1).reshape(-1, 3)
