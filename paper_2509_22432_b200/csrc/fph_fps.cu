@@ -68,13 +68,37 @@ __device__ __forceinline__ void better(double& bv, int& bi, double v, int i) {
     }
 }
 
+#ifndef FPH_FPS_REDUX
+#define FPH_FPS_REDUX 1
+#endif
+
+// Warp argmax with the lowest index among equal values, result in every
+// lane.  REDUX form: the value as a monotone unsigned 64-bit key (exact for
+// every value FPS produces: +0 <= d, -1 for landmarks, -inf for padding;
+// no -0 and no NaN), then three dependent warp reductions -- max of the high
+// word, max of the low word among lanes holding that high word, min index
+// among lanes holding that key -- instead of five shuffle rounds of
+// (double, int) pairs (15 SHFL and a compare chain).
 __device__ __forceinline__ void warp_argmax(double& v, int& i) {
+#if FPH_FPS_REDUX
+    const unsigned long long b = (unsigned long long)__double_as_longlong(v);
+    const unsigned long long key = (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+    const unsigned hi = (unsigned)(key >> 32), lo = (unsigned)key;
+    const unsigned mhi = __reduce_max_sync(0xffffffffu, hi);
+    const unsigned mlo = __reduce_max_sync(0xffffffffu, hi == mhi ? lo : 0u);
+    const unsigned mi =
+        __reduce_min_sync(0xffffffffu, hi == mhi && lo == mlo ? (unsigned)i : 0x7fffffffu);
+    const unsigned long long mk = ((unsigned long long)mhi << 32) | mlo;
+    v = __longlong_as_double((long long)((mk >> 63) ? (mk & 0x7fffffffffffffffull) : ~mk));
+    i = (int)mi;
+#else
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         double ov = __shfl_xor_sync(0xffffffffu, v, o);
         int oi = __shfl_xor_sync(0xffffffffu, i, o);
         better(v, i, ov, oi);
     }
+#endif
 }
 
 // One iteration's exchange with two CTA barriers (a block-wide argmax on
