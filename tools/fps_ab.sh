@@ -4,6 +4,6 @@
 for r in 1 2; do
   for v in "$@"; do
     echo "== $v"
-    FPH_LIB=paper_2509_22432_b200/_lib/variants/$v.so python tools/fps_time.py 2>&1
+    FPH_LIB=paper_2509_22432_b200/_lib/variants/$v.so python tools/fps_time.py $FPS_ARGS 2>&1
   done
 done

@@ -35,6 +35,10 @@ def main():
     B = torch.from_numpy(np.stack([gen_uniform_box(100_000, seed=s).points for s in range(64)])).cuda()
     ms, idx = timed(lambda: farthest_point_sampling_batched(B, 1000, 0))
     print(f"batched 64 x 100k k=1000: {ms:.2f} ms")
+    if "--tiled" in sys.argv:
+        T = torch.from_numpy(gen_uniform_box(10_000_000, seed=0).points).cuda()
+        ms, idx = timed(lambda: farthest_point_sampling(T, 5000, 0))
+        print(f"box_10m k=5000 (tiled): {ms:.2f} ms")
 
 
 if __name__ == "__main__":
