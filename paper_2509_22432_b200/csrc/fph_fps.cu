@@ -9,7 +9,7 @@
 //
 // Layout: one CTA per SM (cooperative launch, all CTAs co-resident), each
 // owning a contiguous slice of the cloud.  When a slice fits, its float64
-// coordinates live in shared memory (SoA, padded to PT x 1024 points, PT a
+// coordinates live in shared memory ((x, y) pairs + z, padded to PT x 1024 points, PT a
 // template parameter so the per-point update is branch-free) and the running
 // minimum in registers for the whole run -- a 1M-point cloud never touches
 // HBM after the first load.  Per iteration each CTA publishes its (value, index) to a
@@ -192,8 +192,8 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
 // index) in registers.  The winning slot's coordinates are then one shared
 // load away -- no dependent global load of the new landmark.
 // `stage` holds 4 doubles per slot; G <= kMaxSlots (checked on the host).
-__device__ __forceinline__ Winner exchange_argmax_xyz(double bv, int bi, const double* sx,
-                                                      const double* sy, const double* sz, int beg,
+__device__ __forceinline__ Winner exchange_argmax_xyz(double bv, int bi, const double2* sxy,
+                                                      const double* sz, int beg,
                                                       SlotXYZ* buf, int G, int slot,
                                                       unsigned long long* arrived,
                                                       unsigned long long target, double* red_v,
@@ -216,8 +216,8 @@ __device__ __forceinline__ Winner exchange_argmax_xyz(double bv, int bi, const d
             s.pad = 0;
             // an empty slice publishes -inf, never the winner: coordinates unused
             const int j = v == -INFINITY ? 0 : i - beg;
-            s.x = sx[j];
-            s.y = sy[j];
+            s.x = sxy[j].x;
+            s.y = sxy[j].y;
             s.z = sz[j];
             s.pad2 = 0.0;
             buf[slot] = s;
@@ -625,8 +625,7 @@ __global__ void __launch_bounds__(kFpsThreads, 1)
     const int ngroups = gridDim.x / cpg;
     const int g = blockIdx.x / cpg, r = blockIdx.x % cpg;
     if (g >= ngroups) return;
-    double* sx = sm;
-    double* sy = sm + kSlice;
+    double2* sxy = reinterpret_cast<double2*>(sm);  // (x, y) interleaved as in fps_resident_kernel
     double* sz = sm + 2 * kSlice;
     SlotXYZ* gslots = reinterpret_cast<SlotXYZ*>(slots) + (size_t)g * 2 * cpg;
     int seq = 0;
@@ -636,8 +635,7 @@ __global__ void __launch_bounds__(kFpsThreads, 1)
         __syncthreads();
         for (int j = threadIdx.x; j < kSlice; j += blockDim.x) {
             const bool in = j < cnt;
-            sx[j] = in ? px[cb + beg + j] : 0.0;
-            sy[j] = in ? py[cb + beg + j] : 0.0;
+            sxy[j] = in ? make_double2(px[cb + beg + j], py[cb + beg + j]) : make_double2(0.0, 0.0);
             sz[j] = in ? pz[cb + beg + j] : 0.0;
         }
         double md[PT];
@@ -655,7 +653,8 @@ __global__ void __launch_bounds__(kFpsThreads, 1)
 #pragma unroll
             for (int t = 0; t < PT; ++t) {
                 const int j = threadIdx.x + t * kFpsThreads;
-                const double d = sq64(sx[j], sy[j], sz[j], qx, qy, qz);
+                const double2 xy = sxy[j];
+                const double d = sq64(xy.x, xy.y, sz[j], qx, qy, qz);
                 double m = d < md[t] ? d : md[t];
                 m = jc == t * kFpsThreads ? -1.0 : m;
                 md[t] = m;
@@ -666,7 +665,7 @@ __global__ void __launch_bounds__(kFpsThreads, 1)
             }
             const long long tag = (long long)seq * (k - 1) + it;  // group-wide iteration
             const Winner wn = exchange_argmax_xyz(
-                bv, bi, sx, sy, sz, beg, gslots + (tag & 1) * cpg, cpg, r, arrived + g,
+                bv, bi, sxy, sz, beg, gslots + (tag & 1) * cpg, cpg, r, arrived + g,
                 (unsigned long long)cpg * (unsigned long long)tag, red_v, red_i, stage);
             cur = wn.idx;
             qx = wn.x;
