@@ -39,6 +39,10 @@ namespace fph {
 namespace {
 
 constexpr int kFpsThreads = 1024;
+#ifndef FPH_FPS_RES_NT
+#define FPH_FPS_RES_NT 512
+#endif
+constexpr int kResNT = FPH_FPS_RES_NT;  // threads per CTA of the resident kernel
 constexpr int kFpsMaxPT = 9;  // points per thread in the shared-memory variants
 constexpr int kMaxSlots = 160;  // CTAs per exchange of the batched (coordinate-carrying) kernel
 constexpr int kStaticSmem = 4 * kMaxSlots * 8 + 1024;  // batched kernel: stage + reduction scratch
@@ -311,14 +315,14 @@ __global__ void __launch_bounds__(kFpsThreads, 1)
 // finite, and d >= +0 so no signed-zero case).  ~23 instructions per point
 // instead of ~32 plus a branch.
 template <int PT>
-__global__ void __launch_bounds__(kFpsThreads, 1)
+__global__ void __launch_bounds__(kResNT, 1)
     fps_resident_kernel(const double* __restrict__ px, const double* __restrict__ py,
                         const double* __restrict__ pz, int n, int k, int start, int chunk,
                         Slot* slots, unsigned long long* arrived, long long* __restrict__ out) {
     extern __shared__ double sm[];
     __shared__ double red_v[32];
     __shared__ int red_i[33];
-    constexpr int kSlice = PT * kFpsThreads;
+    constexpr int kSlice = PT * kResNT;
     const int beg = blockIdx.x * chunk;
     const int cnt = max(0, min(n, beg + chunk) - beg);
     // (x, y) interleaved: one 16-byte shared load plus one 8-byte per point
@@ -332,7 +336,7 @@ __global__ void __launch_bounds__(kFpsThreads, 1)
     }
     double md[PT];
 #pragma unroll
-    for (int t = 0; t < PT; ++t) md[t] = (int)threadIdx.x + t * kFpsThreads < cnt ? INFINITY : -INFINITY;
+    for (int t = 0; t < PT; ++t) md[t] = (int)threadIdx.x + t * kResNT < cnt ? INFINITY : -INFINITY;
     __syncthreads();
     int cur = start;
     if (blockIdx.x == 0 && threadIdx.x == 0) out[0] = start;
@@ -345,11 +349,11 @@ __global__ void __launch_bounds__(kFpsThreads, 1)
         int bi = 0x7fffffff;
 #pragma unroll
         for (int t = 0; t < PT; ++t) {
-            const int j = threadIdx.x + t * kFpsThreads;
+            const int j = threadIdx.x + t * kResNT;
             const double2 xy = sxy[j];
             const double d = sq64(xy.x, xy.y, sz[j], qx, qy, qz);
             double m = d < md[t] ? d : md[t];
-            m = jc == t * kFpsThreads ? -1.0 : m;
+            m = jc == t * kResNT ? -1.0 : m;
             md[t] = m;
             if (m > bv) {
                 bv = m;
@@ -367,13 +371,13 @@ template <int PT>
 int launch_resident(const double* d_x, const double* d_y, const double* d_z, int n, int k,
                     int start, int chunk, int G, Slot* slots, unsigned long long* arrived,
                     long long* d_out, cudaStream_t stream) {
-    const size_t smem = sizeof(double) * 3 * PT * kFpsThreads;
+    const size_t smem = sizeof(double) * 3 * PT * kResNT;
     FPH_CUDA_TRY(cudaFuncSetAttribute(fps_resident_kernel<PT>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     void* args[] = {(void*)&d_x, (void*)&d_y,   (void*)&d_z,   (void*)&n,      (void*)&k,
                     (void*)&start, (void*)&chunk, (void*)&slots, (void*)&arrived, (void*)&d_out};
     FPH_CUDA_TRY(cudaLaunchCooperativeKernel((void*)fps_resident_kernel<PT>, dim3(G),
-                                             dim3(kFpsThreads), args, smem, stream));
+                                             dim3(kResNT), args, smem, stream));
     return FPH_OK;
 }
 
@@ -730,7 +734,8 @@ int fps_run(const double* d_x, const double* d_y, const double* d_z, int n, int 
         rc = launch_resident<P>(d_x, d_y, d_z, n, k, start, chunk, G, slots, arrived, d_out,   \
                                 stream);                                                       \
         break;
-        switch ((chunk + kFpsThreads - 1) / kFpsThreads) {
+        static_assert(kResNT == 1024 || kResNT == 512, "resident kernel: 512 or 1024 threads");
+        switch ((chunk + kResNT - 1) / kResNT) {
             FPH_RESIDENT_CASE(1)
             FPH_RESIDENT_CASE(2)
             FPH_RESIDENT_CASE(3)
@@ -739,8 +744,22 @@ int fps_run(const double* d_x, const double* d_y, const double* d_z, int n, int 
             FPH_RESIDENT_CASE(6)
             FPH_RESIDENT_CASE(7)
             FPH_RESIDENT_CASE(8)
+#if FPH_FPS_RES_NT == 512
+            FPH_RESIDENT_CASE(9)
+            FPH_RESIDENT_CASE(10)
+            FPH_RESIDENT_CASE(11)
+            FPH_RESIDENT_CASE(12)
+            FPH_RESIDENT_CASE(13)
+            FPH_RESIDENT_CASE(14)
+            FPH_RESIDENT_CASE(15)
+            FPH_RESIDENT_CASE(16)
+            FPH_RESIDENT_CASE(17)
+            default:
+                FPH_RESIDENT_CASE(18)
+#else
             default:
                 FPH_RESIDENT_CASE(9)
+#endif
         }
 #undef FPH_RESIDENT_CASE
         if (rc != FPH_OK) return rc;
