@@ -616,7 +616,7 @@ int fps_tiled(const double* d_x, const double* d_y, const double* d_z, int n, in
 // ngroups = gridDim / cpg clouds advance concurrently instead of every cloud
 // using (and waiting on) the whole GPU.
 template <int PT>
-__global__ void __launch_bounds__(kFpsThreads, 1)
+__global__ void __launch_bounds__(kResNT, 1)
     fps_batched_kernel(const double* __restrict__ px, const double* __restrict__ py,
                        const double* __restrict__ pz, int batch, int n, int k, int start, int cpg,
                        int chunk, Slot* slots, unsigned long long* arrived,
@@ -625,7 +625,7 @@ __global__ void __launch_bounds__(kFpsThreads, 1)
     __shared__ double red_v[32];
     __shared__ int red_i[34];
     __shared__ __align__(16) double stage[4 * kMaxSlots];
-    constexpr int kSlice = PT * kFpsThreads;  // padded as in fps_resident_kernel
+    constexpr int kSlice = PT * kResNT;  // padded as in fps_resident_kernel
     const int ngroups = gridDim.x / cpg;
     const int g = blockIdx.x / cpg, r = blockIdx.x % cpg;
     if (g >= ngroups) return;
@@ -645,7 +645,7 @@ __global__ void __launch_bounds__(kFpsThreads, 1)
         double md[PT];
 #pragma unroll
         for (int t = 0; t < PT; ++t)
-            md[t] = (int)threadIdx.x + t * kFpsThreads < cnt ? INFINITY : -INFINITY;
+            md[t] = (int)threadIdx.x + t * kResNT < cnt ? INFINITY : -INFINITY;
         __syncthreads();
         int cur = start;
         if (r == 0 && threadIdx.x == 0) out[(long long)c * k] = start;
@@ -656,11 +656,11 @@ __global__ void __launch_bounds__(kFpsThreads, 1)
             int bi = 0x7fffffff;
 #pragma unroll
             for (int t = 0; t < PT; ++t) {
-                const int j = threadIdx.x + t * kFpsThreads;
+                const int j = threadIdx.x + t * kResNT;
                 const double2 xy = sxy[j];
                 const double d = sq64(xy.x, xy.y, sz[j], qx, qy, qz);
                 double m = d < md[t] ? d : md[t];
-                m = jc == t * kFpsThreads ? -1.0 : m;
+                m = jc == t * kResNT ? -1.0 : m;
                 md[t] = m;
                 if (m > bv) {
                     bv = m;
@@ -684,14 +684,14 @@ template <int PT>
 int launch_batched(const double* d_x, const double* d_y, const double* d_z, int batch, int n,
                    int k, int start, int cpg, int chunk, int grid, Slot* slots,
                    unsigned long long* arrived, long long* d_out, cudaStream_t stream) {
-    const size_t smem = sizeof(double) * 3 * PT * kFpsThreads;
+    const size_t smem = sizeof(double) * 3 * PT * kResNT;
     FPH_CUDA_TRY(cudaFuncSetAttribute(fps_batched_kernel<PT>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     void* args[] = {(void*)&d_x, (void*)&d_y, (void*)&d_z,   (void*)&batch, (void*)&n,
                     (void*)&k,   (void*)&start, (void*)&cpg, (void*)&chunk, (void*)&slots,
                     (void*)&arrived, (void*)&d_out};
     FPH_CUDA_TRY(cudaLaunchCooperativeKernel((void*)fps_batched_kernel<PT>, dim3(grid),
-                                             dim3(kFpsThreads), args, smem, stream));
+                                             dim3(kResNT), args, smem, stream));
     return FPH_OK;
 }
 
@@ -809,7 +809,7 @@ int fps_batched(const double* d_x, const double* d_y, const double* d_z, int bat
         rc = launch_batched<P>(d_x, d_y, d_z, batch, n, k, start, cpg, chunk, grid, slots,     \
                                arrived, d_out, stream);                                        \
         break;
-    switch ((chunk + kFpsThreads - 1) / kFpsThreads) {
+    switch ((chunk + kResNT - 1) / kResNT) {
         FPH_BATCHED_CASE(1)
         FPH_BATCHED_CASE(2)
         FPH_BATCHED_CASE(3)
@@ -818,8 +818,22 @@ int fps_batched(const double* d_x, const double* d_y, const double* d_z, int bat
         FPH_BATCHED_CASE(6)
         FPH_BATCHED_CASE(7)
         FPH_BATCHED_CASE(8)
+#if FPH_FPS_RES_NT == 512
+        FPH_BATCHED_CASE(9)
+        FPH_BATCHED_CASE(10)
+        FPH_BATCHED_CASE(11)
+        FPH_BATCHED_CASE(12)
+        FPH_BATCHED_CASE(13)
+        FPH_BATCHED_CASE(14)
+        FPH_BATCHED_CASE(15)
+        FPH_BATCHED_CASE(16)
+        FPH_BATCHED_CASE(17)
+        default:
+            FPH_BATCHED_CASE(18)
+#else
         default:
             FPH_BATCHED_CASE(9)
+#endif
     }
 #undef FPH_BATCHED_CASE
     if (rc != FPH_OK) return rc;
