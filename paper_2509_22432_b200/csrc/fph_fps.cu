@@ -734,7 +734,7 @@ int fps_run(const double* d_x, const double* d_y, const double* d_z, int n, int 
         rc = launch_resident<P>(d_x, d_y, d_z, n, k, start, chunk, G, slots, arrived, d_out,   \
                                 stream);                                                       \
         break;
-        static_assert(kResNT == 1024 || kResNT == 512, "resident kernel: 512 or 1024 threads");
+        static_assert(kResNT == 1024 || kResNT == 512 || kResNT == 256, "resident kernel: 256, 512 or 1024 threads");
         switch ((chunk + kResNT - 1) / kResNT) {
             FPH_RESIDENT_CASE(1)
             FPH_RESIDENT_CASE(2)
@@ -744,7 +744,7 @@ int fps_run(const double* d_x, const double* d_y, const double* d_z, int n, int 
             FPH_RESIDENT_CASE(6)
             FPH_RESIDENT_CASE(7)
             FPH_RESIDENT_CASE(8)
-#if FPH_FPS_RES_NT == 512
+#if FPH_FPS_RES_NT <= 512
             FPH_RESIDENT_CASE(9)
             FPH_RESIDENT_CASE(10)
             FPH_RESIDENT_CASE(11)
@@ -754,8 +754,31 @@ int fps_run(const double* d_x, const double* d_y, const double* d_z, int n, int 
             FPH_RESIDENT_CASE(15)
             FPH_RESIDENT_CASE(16)
             FPH_RESIDENT_CASE(17)
+#if FPH_FPS_RES_NT == 256
+            FPH_RESIDENT_CASE(18)
+            FPH_RESIDENT_CASE(19)
+            FPH_RESIDENT_CASE(20)
+            FPH_RESIDENT_CASE(21)
+            FPH_RESIDENT_CASE(22)
+            FPH_RESIDENT_CASE(23)
+            FPH_RESIDENT_CASE(24)
+            FPH_RESIDENT_CASE(25)
+            FPH_RESIDENT_CASE(26)
+            FPH_RESIDENT_CASE(27)
+            FPH_RESIDENT_CASE(28)
+            FPH_RESIDENT_CASE(29)
+            FPH_RESIDENT_CASE(30)
+            FPH_RESIDENT_CASE(31)
+            FPH_RESIDENT_CASE(32)
+            FPH_RESIDENT_CASE(33)
+            FPH_RESIDENT_CASE(34)
+            FPH_RESIDENT_CASE(35)
+            default:
+                FPH_RESIDENT_CASE(36)
+#else
             default:
                 FPH_RESIDENT_CASE(18)
+#endif
 #else
             default:
                 FPH_RESIDENT_CASE(9)
@@ -818,7 +841,7 @@ int fps_batched(const double* d_x, const double* d_y, const double* d_z, int bat
         FPH_BATCHED_CASE(6)
         FPH_BATCHED_CASE(7)
         FPH_BATCHED_CASE(8)
-#if FPH_FPS_RES_NT == 512
+#if FPH_FPS_RES_NT <= 512
         FPH_BATCHED_CASE(9)
         FPH_BATCHED_CASE(10)
         FPH_BATCHED_CASE(11)
@@ -828,8 +851,31 @@ int fps_batched(const double* d_x, const double* d_y, const double* d_z, int bat
         FPH_BATCHED_CASE(15)
         FPH_BATCHED_CASE(16)
         FPH_BATCHED_CASE(17)
+#if FPH_FPS_RES_NT == 256
+        FPH_BATCHED_CASE(18)
+        FPH_BATCHED_CASE(19)
+        FPH_BATCHED_CASE(20)
+        FPH_BATCHED_CASE(21)
+        FPH_BATCHED_CASE(22)
+        FPH_BATCHED_CASE(23)
+        FPH_BATCHED_CASE(24)
+        FPH_BATCHED_CASE(25)
+        FPH_BATCHED_CASE(26)
+        FPH_BATCHED_CASE(27)
+        FPH_BATCHED_CASE(28)
+        FPH_BATCHED_CASE(29)
+        FPH_BATCHED_CASE(30)
+        FPH_BATCHED_CASE(31)
+        FPH_BATCHED_CASE(32)
+        FPH_BATCHED_CASE(33)
+        FPH_BATCHED_CASE(34)
+        FPH_BATCHED_CASE(35)
+        default:
+            FPH_BATCHED_CASE(36)
+#else
         default:
             FPH_BATCHED_CASE(18)
+#endif
 #else
         default:
             FPH_BATCHED_CASE(9)
