@@ -58,9 +58,9 @@ def test_fps_batched_matches_oracle(batch, n, k):
 
 @pytest.mark.parametrize("pt", [3, 4, 5, 6, 7, 8, 9])
 def test_fps_resident_points_per_thread(pt):
-    """Every PT instantiation of the resident kernel (PT x 1024 points per
-    CTA slot, padded), on coordinates quantised to 1/8 so ties are common and
-    a ragged last slice."""
+    """Slices of 3..9 x 1024 points per CTA (PT = 6..18 points per thread at
+    the default 512 threads, padded), on coordinates quantised to 1/8 so ties
+    are common, and a ragged last slice."""
     n = 148 * (pt * 1024 - 300) + 77
     pts = np.round(np.random.default_rng(pt).random((n, 3)) * 64) / 8
     got = farthest_point_sampling(pts, 120, pt)
