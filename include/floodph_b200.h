@@ -16,7 +16,8 @@
  * most recent failure of the calling thread.  Argument errors (FPH_EARG)
  * correspond to the reference's ValueError, FPH_EINTEGRITY to IntegrityError.
  *
- * Coordinates are float64 row-major (n x dim, dim in {2, 3}); results are
+ * Coordinates are float64 row-major (n x dim, dim in {2, 3}); grid_resolution
+ * is any m in [1, 65535] (rows per k-simplex C(m-1, k) < 2^24); results are
  * bit-identical to the reference's float64 values.
  */
 #ifndef FLOODPH_B200_H
@@ -141,6 +142,23 @@ int fph_flood_complete(const double* interior_sq, const int32_t* facets, int64_t
                        const double* lower_sq, double* out_sq, void* stream);
 
 /*
+ * Candidate masks (host memory only).  Replaces floodph/filtration.py:130
+ * compute_mask -> CandidateMask (filtration.py:88): for each of n_cells
+ * k-simplices (cells: n_cells x (k+1) int32 landmark ids), the ascending
+ * cloud indices x with |x - c|^2 <= 2 r r, (c, r) the simplex's Ritter ball
+ * (geometry.py:123), the same float64 test as the reference.
+ *   out_offsets  n_cells + 1 CSR offsets (always written)
+ *   out_indices  the concatenated lists, written only when capacity >= the
+ *                total (call once with capacity 0 to size the buffer)
+ * The reference's fallback for an empty ball (the batch slab, then the whole
+ * cloud) depends on its batching and is left to the caller.
+ */
+int fph_candidate_mask(const double* points, int64_t n_points, int32_t dim,
+                       const double* landmarks, int64_t n_landmarks, const int32_t* cells,
+                       int64_t n_cells, int32_t k, int64_t* out_offsets, int32_t* out_indices,
+                       int64_t capacity);
+
+/*
  * Persistence pairs of a filtered complex (host computation, no GPU needed):
  * Z/2 column reduction with the twist / clearing optimisation.  Replaces
  * floodph/persistence.py:89 _run_reduction (pairing as :118 reduce_and_extract).
@@ -166,9 +184,7 @@ int fph_set_tuning(double cell_occupancy, double pairs_per_task);
  * Flooding algorithm: 1 (default) bounded search -- per simplex, sampled
  * upper bounds, an exact lower bound, and exact search of only the point
  * blocks that can still hold the maximum; 0 brute force over every point of
- * the Lemma-4.2 ball; 2 bounded search with its sampling pass run by the
- * brute-force CTA kernel (measured slower on configs[1]; kept for study).
- * All are exact (identical values).
+ * the Lemma-4.2 ball.  Both are exact (identical values).
  * reps_target: candidates per representative (sampling) pass;
  * team_threshold: simplices with more candidates are searched by a whole
  * CTA instead of one warp; 0 (default) derives it per launch as

@@ -1,7 +1,8 @@
 """Build libfloodph_b200.so in-tree with nvcc for sm_100a.
 
 The shared library lands in paper_2509_22432_b200/_lib/ (git-ignored; it
-travels to the GPU box with the repo snapshot).
+travels to the GPU box with the repo snapshot).  Each source compiles to its
+own object in parallel (no device code crosses files), then one link.
 """
 
 from __future__ import annotations
@@ -9,19 +10,20 @@ from __future__ import annotations
 import os
 import shutil
 import subprocess
+from concurrent.futures import ThreadPoolExecutor
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB_DIR = os.path.join(HERE, "_lib")
 LIB_PATH = os.path.join(LIB_DIR, "libfloodph_b200.so")
 SOURCES = ["fph_api.cu", "fph_flood.cu", "fph_search.cu", "fph_fps.cu", "fph_grid.cu",
-           "fph_diag.cu", "fph_persistence.cpp"]
+           "fph_diag.cu", "fph_mask.cu", "fph_persistence.cpp"]
 HEADERS = ["fph_common.cuh", "fph_dev.cuh", "fph_flood.cuh", "fph_grid.cuh"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",
-    "-Xcompiler", "-fPIC", "-shared",
+    "-Xcompiler", "-fPIC",
 ]
 
 
@@ -50,13 +52,28 @@ def build(force: bool = False, verbose: bool = False, out: str | None = None,
     if not force and out is None and not _stale():
         return LIB_PATH
     os.makedirs(os.path.dirname(target), exist_ok=True)
+    objdir = target + ".objs"
+    os.makedirs(objdir, exist_ok=True)
+    nvcc = _nvcc()
+    defs = [f"-D{d}" for d in defines]
+
+    def compile_one(src):
+        obj = os.path.join(objdir, src + ".o")
+        cmd = [nvcc, *NVCC_FLAGS, *defs, "-c", "-o", obj, os.path.join(CSRC, src)]
+        if verbose:
+            print(" ".join(cmd))
+        subprocess.run(cmd, check=True)
+        return obj
+
+    with ThreadPoolExecutor(max_workers=len(SOURCES)) as pool:
+        objs = list(pool.map(compile_one, SOURCES))
     tmp = target + ".tmp"
-    cmd = [_nvcc(), *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-o", tmp,
-           *[os.path.join(CSRC, f) for f in SOURCES]]
+    cmd = [nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp, *objs]
     if verbose:
         print(" ".join(cmd))
     subprocess.run(cmd, check=True)
     os.replace(tmp, target)
+    shutil.rmtree(objdir, ignore_errors=True)
     return target
 
 

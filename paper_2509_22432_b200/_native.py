@@ -52,6 +52,9 @@ SIGNATURES = {
                                        ctypes.c_int32, ctypes.c_int32, _vp, ctypes.c_int32, _vp]),
     "fph_flood_complete": (ctypes.c_int, [_vp, _vp, ctypes.c_int64, ctypes.c_int32, _vp, _vp,
                                           _vp]),
+    "fph_candidate_mask": (ctypes.c_int, [_vp, ctypes.c_int64, ctypes.c_int32, _vp, ctypes.c_int64,
+                                          _vp, ctypes.c_int64, ctypes.c_int32, _vp, _vp,
+                                          ctypes.c_int64]),
     "fph_persistence_pairs": (ctypes.c_int, [ctypes.c_int32, _vp, _vp, _vp, ctypes.c_int32, _vp,
                                              _vp]),
     "fph_set_tuning": (ctypes.c_int, [ctypes.c_double, ctypes.c_double]),

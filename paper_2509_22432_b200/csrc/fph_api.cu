@@ -4,14 +4,19 @@
 // stream and copy results back; device-memory calls run on the caller's
 // stream.  Scratch comes from the stream-ordered allocator (cudaMallocAsync)
 // whose pool is kept warm, so repeated calls do not pay cudaMalloc.
+#include <array>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <vector>
 
 #include "../../include/floodph_b200.h"
 #include "fph_flood.cuh"
 #include "fph_grid.cuh"
+
+#include <cub/cub.cuh>
 
 namespace fph {
 
@@ -20,7 +25,6 @@ static double g_occupancy = 2.0;
 static double g_pairs_per_task = 0.0;
 static bool g_profile = false;
 static int g_algo = 1;
-static double g_probe_cells = 1.0;
 static int g_reps_target = 512;
 static int g_team_threshold = 0;  // auto (derived per launch on the device)
 static double g_exact_pairs = 65536.0;
@@ -72,6 +76,14 @@ __global__ void pad4_shard_kernel(const int* __restrict__ s, long long n_out, in
     for (int j = 0; j < 4; ++j) out[i * 4 + j] = j <= k ? s[row * (k + 1) + j] : -1;
 }
 
+// 0-simplices i = 0..n-1 as (i, -1, -1, -1) rows
+__global__ void vertex_ids_kernel(long long n, int* __restrict__ out) {
+    long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    out[i * 4] = (int)i;
+    out[i * 4 + 1] = out[i * 4 + 2] = out[i * 4 + 3] = -1;
+}
+
 __global__ void fill_kernel(double* out, long long n, double v) {
     long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     if (i < n) out[i] = v;
@@ -79,47 +91,59 @@ __global__ void fill_kernel(double* out, long long n, double v) {
 
 unsigned blocks_for(long long n) { return (unsigned)((n + 255) / 256); }
 
-// RAII for stream-ordered scratch
-struct Scratch {
-    cudaStream_t stream;
-    std::vector<void*> ptrs;
-    explicit Scratch(cudaStream_t s) : stream(s) {}
-    template <class T>
-    int alloc(T** p, size_t count) {
-        void* q = nullptr;
-        cudaError_t e = cudaMallocAsync(&q, count * sizeof(T) + 16, stream);
-        if (e != cudaSuccess) {
-            set_error("cudaMallocAsync(%zu bytes): %s", count * sizeof(T), cudaGetErrorString(e));
-            return FPH_ENOMEM;
-        }
-        ptrs.push_back(q);
-        *p = static_cast<T*>(q);
-        return FPH_OK;
-    }
-    ~Scratch() {
-        for (void* p : ptrs) cudaFreeAsync(p, stream);
-    }
-};
+// Library streams, created once per device and kept: slot 0 carries
+// host-memory calls, slots 1..3 the per-dimension interior terms
+// (run_interiors; higher dimensions at higher priority).
+std::mutex g_stream_mu;
+std::map<int, std::array<cudaStream_t, 4>> g_streams;
 
-// Host-call context: private stream on the current device
+int lib_stream(int slot, cudaStream_t* out) {
+    int dev = 0;
+    FPH_CUDA_TRY(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lock(g_stream_mu);
+    auto it = g_streams.find(dev);
+    if (it == g_streams.end()) {
+        std::array<cudaStream_t, 4> st{};
+        int lo = 0, hi = 0;
+        FPH_CUDA_TRY(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        for (int i = 0; i < 4; ++i)
+            FPH_CUDA_TRY(cudaStreamCreateWithPriority(&st[i], cudaStreamNonBlocking,
+                                                      i >= 2 ? hi : lo));
+        it = g_streams.emplace(dev, st).first;
+    }
+    *out = it->second[slot];
+    return FPH_OK;
+}
+
+// Host-call context: the library's stream on the current device (host
+// calls), or the caller's stream (device calls)
 struct HostCtx {
     cudaStream_t stream = nullptr;
-    bool owned = false;
     int init(int memory, void* user_stream) {
         if (memory == FPH_MEM_DEVICE) {
             stream = static_cast<cudaStream_t>(user_stream);
             return FPH_OK;
         }
-        FPH_CUDA_TRY(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
-        owned = true;
-        return FPH_OK;
+        return lib_stream(0, &stream);
     }
-    ~HostCtx() {
-        if (owned) {
-            cudaStreamSynchronize(stream);
-            cudaStreamDestroy(stream);
-        }
+};
+
+// a host-memory call returns once its stream is drained (on errors too)
+int host_finish(const HostCtx& hc, int memory, int rc) {
+    if (memory != FPH_MEM_HOST) return rc;
+    const cudaError_t e = cudaStreamSynchronize(hc.stream);
+    if (rc == FPH_OK && e != cudaSuccess) {
+        set_error("cudaStreamSynchronize: %s", cudaGetErrorString(e));
+        return FPH_ECUDA;
     }
+    return rc;
+}
+
+// frees a GridStore on every exit path
+struct GridGuard {
+    GridStore& gs;
+    cudaStream_t stream;
+    ~GridGuard() { gs.free_all(stream); }
 };
 
 int ensure_device() {
@@ -174,6 +198,26 @@ int check_cloud(const double* points, int64_t n, int32_t dim) {
     return FPH_OK;
 }
 
+FloodTuning current_tuning() {
+    FloodTuning t;
+    t.pairs_per_task = g_pairs_per_task;
+    t.profile = g_profile;
+    t.algo = g_algo;
+    t.reps_target = g_reps_target;
+    t.team_threshold = g_team_threshold;
+    t.exact_pairs = g_exact_pairs;
+    for (int i = 0; i < 4; ++i) t.exact_cand[i] = g_exact_cand[i];
+    return t;
+}
+
+int check_resolution(int m) {
+    if (m < 1 || m > kMaxResolution) {
+        set_error("grid_resolution must be in [1, %d], got %d", kMaxResolution, m);
+        return FPH_EARG;
+    }
+    return FPH_OK;
+}
+
 }  // namespace
 }  // namespace fph
 
@@ -211,8 +255,8 @@ int fph_flood_complete(const double* interior_sq, const int32_t* facets, int64_t
 }
 
 int fph_set_search(int32_t algo, int32_t reps_target, int32_t team_threshold) {
-    if (algo < 0 || algo > 2) {
-        set_error("algo must be 0 (brute force), 1 (bounded search) or 2 (split bounded search)");
+    if (algo < 0 || algo > 1) {
+        set_error("algo must be 0 (brute force) or 1 (bounded search)");
         return FPH_EARG;
     }
     g_algo = algo;
@@ -285,8 +329,10 @@ int fph_farthest_point_sampling(const double* points, int64_t n, int32_t dim, in
     FPH_TRY(ensure_device());
     HostCtx hc;
     FPH_TRY(hc.init(memory, stream));
-    int rc = FPH_OK;
-    {
+    // the body runs in a lambda so that every exit path below still waits for
+    // the copies of a host-memory call (the caller may free its buffers)
+    const int rc = [&]() -> int {
+        int rc = FPH_OK;
         Scratch sc(hc.stream);
         const double* d_pts = nullptr;
         FPH_TRY(stage_in(sc, points, (size_t)n * dim, memory, &d_pts));
@@ -304,9 +350,9 @@ int fph_farthest_point_sampling(const double* points, int64_t n, int32_t dim, in
             FPH_CUDA_TRY(cudaMemcpyAsync(out_indices, d_out, sizeof(long long) * k,
                                          cudaMemcpyDeviceToHost, hc.stream));
         }
-    }
-    if (memory == FPH_MEM_HOST) FPH_CUDA_TRY(cudaStreamSynchronize(hc.stream));
-    return rc;
+        return rc;
+    }();
+    return host_finish(hc, memory, rc);
 }
 
 int fph_farthest_point_sampling_batched(const double* points, int64_t batch, int64_t n,
@@ -334,8 +380,10 @@ int fph_farthest_point_sampling_batched(const double* points, int64_t batch, int
     FPH_TRY(ensure_device());
     HostCtx hc;
     FPH_TRY(hc.init(memory, stream));
-    int rc = FPH_OK;
-    {
+    // the body runs in a lambda so that every exit path below still waits for
+    // the copies of a host-memory call (the caller may free its buffers)
+    const int rc = [&]() -> int {
+        int rc = FPH_OK;
         Scratch sc(hc.stream);
         const long long total = batch * n;
         const double* d_pts = nullptr;
@@ -361,9 +409,9 @@ int fph_farthest_point_sampling_batched(const double* points, int64_t batch, int
         if (rc == FPH_OK && memory == FPH_MEM_HOST)
             FPH_CUDA_TRY(cudaMemcpyAsync(out_indices, d_out, sizeof(long long) * batch * k,
                                          cudaMemcpyDeviceToHost, hc.stream));
-    }
-    if (memory == FPH_MEM_HOST) FPH_CUDA_TRY(cudaStreamSynchronize(hc.stream));
-    return rc;
+        return rc;
+    }();
+    return host_finish(hc, memory, rc);
 }
 
 int fph_flood_interior(const double* points, int64_t n_points, int32_t dim,
@@ -372,16 +420,19 @@ int fph_flood_interior(const double* points, int64_t n_points, int32_t dim,
                        int32_t subset_mode, double* out_sq, int32_t memory, void* stream) {
     g_err[0] = 0;
     FPH_TRY(check_cloud(points, n_points, dim));
-    if (k < 0 || k > 3 || grid_resolution < 1 || grid_resolution > 255 || n_landmarks < 1) {
-        set_error("need 0 <= k <= 3, 1 <= grid_resolution <= 255 and landmarks");
+    FPH_TRY(check_resolution(grid_resolution));
+    if (k < 0 || k > 3 || n_landmarks < 1) {
+        set_error("need 0 <= k <= 3 and landmarks");
         return FPH_EARG;
     }
     if (n_simplices == 0) return FPH_OK;
     FPH_TRY(ensure_device());
     HostCtx hc;
     FPH_TRY(hc.init(memory, stream));
-    int rc = FPH_OK;
-    {
+    // the body runs in a lambda so that every exit path below still waits for
+    // the copies of a host-memory call (the caller may free its buffers)
+    const int rc = [&]() -> int {
+        int rc = FPH_OK;
         Scratch sc(hc.stream);
         const double *d_pts, *d_lm;
         const int32_t* d_s;
@@ -393,31 +444,20 @@ int fph_flood_interior(const double* points, int64_t n_points, int32_t dim,
         pad3_kernel<<<blocks_for(n_landmarks), 256, 0, hc.stream>>>(d_lm, n_landmarks, dim, lm3);
         count_launches(1);
         GridStore gs;
-        rc = grid_build(d_pts, (int)n_points, dim, 0.0, g_occupancy, hc.stream, &gs);
+        GridGuard gg{gs, hc.stream};
+        FPH_TRY(grid_build(d_pts, (int)n_points, dim, 0.0, g_occupancy, hc.stream, &gs));
         count_launches(4);
-        if (rc == FPH_OK) {
-            double* d_out = out_sq;
-            if (memory == FPH_MEM_HOST) FPH_TRY(sc.alloc(&d_out, n_simplices));
-            FloodTuning tune;
-            tune.pairs_per_task = g_pairs_per_task;
-            tune.profile = g_profile;
-            tune.algo = g_algo;
-            tune.probe_cells = g_probe_cells;
-            tune.reps_target = g_reps_target;
-            tune.team_threshold = g_team_threshold;
-            tune.exact_pairs = g_exact_pairs;
-            for (int i = 0; i < 4; ++i) tune.exact_cand[i] = g_exact_cand[i];
-            rc = flood_interior(gs.grid, lm3, d_s, (int)n_simplices, k, grid_resolution,
-                                subset_mode, d_out, tune, hc.stream);
-            count_launches(4);
-            if (rc == FPH_OK && memory == FPH_MEM_HOST)
-                FPH_CUDA_TRY(cudaMemcpyAsync(out_sq, d_out, sizeof(double) * n_simplices,
-                                             cudaMemcpyDeviceToHost, hc.stream));
-        }
-        gs.free_all(hc.stream);
-    }
-    if (memory == FPH_MEM_HOST) FPH_CUDA_TRY(cudaStreamSynchronize(hc.stream));
-    return rc;
+        double* d_out = out_sq;
+        if (memory == FPH_MEM_HOST) FPH_TRY(sc.alloc(&d_out, n_simplices));
+        rc = flood_interior(gs.grid, lm3, d_s, (int)n_simplices, k, grid_resolution, subset_mode,
+                            d_out, current_tuning(), hc.stream);
+        count_launches(4);
+        if (rc == FPH_OK && memory == FPH_MEM_HOST)
+            FPH_CUDA_TRY(cudaMemcpyAsync(out_sq, d_out, sizeof(double) * n_simplices,
+                                         cudaMemcpyDeviceToHost, hc.stream));
+        return rc;
+    }();
+    return host_finish(hc, memory, rc);
 }
 
 int fph_flood_samples(const double* points, int64_t n_points, int32_t dim,
@@ -434,8 +474,10 @@ int fph_flood_samples(const double* points, int64_t n_points, int32_t dim,
     FPH_TRY(ensure_device());
     HostCtx hc;
     FPH_TRY(hc.init(memory, stream));
-    int rc = FPH_OK;
-    {
+    // the body runs in a lambda so that every exit path below still waits for
+    // the copies of a host-memory call (the caller may free its buffers)
+    const int rc = [&]() -> int {
+        int rc = FPH_OK;
         Scratch sc(hc.stream);
         const double *d_pts, *d_lm, *d_smp;
         const int32_t* d_s;
@@ -451,38 +493,21 @@ int fph_flood_samples(const double* points, int64_t n_points, int32_t dim,
         pad3_kernel<<<blocks_for(nrow), 256, 0, hc.stream>>>(d_smp, nrow, dim, smp3);
         count_launches(2);
         GridStore gs;
-        rc = grid_build(d_pts, (int)n_points, dim, 0.0, g_occupancy, hc.stream, &gs);
+        GridGuard gg{gs, hc.stream};
+        FPH_TRY(grid_build(d_pts, (int)n_points, dim, 0.0, g_occupancy, hc.stream, &gs));
         count_launches(4);
-        if (rc == FPH_OK) {
-            double* d_out = out_sq;
-            if (memory == FPH_MEM_HOST) FPH_TRY(sc.alloc(&d_out, n_simplices));
-            FloodTuning tune;
-            tune.pairs_per_task = g_pairs_per_task;
-            tune.profile = g_profile;
-            tune.algo = g_algo;
-            tune.reps_target = g_reps_target;
-            tune.team_threshold = g_team_threshold;
-            tune.exact_pairs = g_exact_pairs;
-            for (int i = 0; i < 4; ++i) tune.exact_cand[i] = g_exact_cand[i];
-            rc = flood_interior(gs.grid, lm3, d_s, (int)n_simplices, k, 1, subset_mode, d_out, tune,
-                                hc.stream, smp3, n_samples);
-            count_launches(4);
-            if (rc == FPH_OK && memory == FPH_MEM_HOST)
-                FPH_CUDA_TRY(cudaMemcpyAsync(out_sq, d_out, sizeof(double) * n_simplices,
-                                             cudaMemcpyDeviceToHost, hc.stream));
-        }
-        gs.free_all(hc.stream);
-    }
-    if (memory == FPH_MEM_HOST) FPH_CUDA_TRY(cudaStreamSynchronize(hc.stream));
-    return rc;
+        double* d_out = out_sq;
+        if (memory == FPH_MEM_HOST) FPH_TRY(sc.alloc(&d_out, n_simplices));
+        rc = flood_interior(gs.grid, lm3, d_s, (int)n_simplices, k, 1, subset_mode, d_out,
+                            current_tuning(), hc.stream, smp3, n_samples);
+        count_launches(4);
+        if (rc == FPH_OK && memory == FPH_MEM_HOST)
+            FPH_CUDA_TRY(cudaMemcpyAsync(out_sq, d_out, sizeof(double) * n_simplices,
+                                         cudaMemcpyDeviceToHost, hc.stream));
+        return rc;
+    }();
+    return host_finish(hc, memory, rc);
 }
-
-#ifndef FPH_DIM_PRIORITY
-#define FPH_DIM_PRIORITY 1
-#endif
-#ifndef FPH_CONCURRENT_DIMS
-#define FPH_CONCURRENT_DIMS 1
-#endif
 
 // Interior terms of dimensions 1..max_dim, concurrently on side streams
 // forked from (and joined back into) `stream`.  With profiling on, the
@@ -490,7 +515,6 @@ int fph_flood_samples(const double* points, int64_t n_points, int32_t dim,
 static int run_interiors(const Grid& g, const double* lm3, int* const* s4, double* const* interior,
                          const int64_t* counts, int max_dim, int grid_resolution, int subset_mode,
                          FloodTuning tune, cudaStream_t stream) {
-    static cudaStream_t side[4] = {nullptr, nullptr, nullptr, nullptr};
     cudaEvent_t fork = nullptr, done[4] = {nullptr, nullptr, nullptr, nullptr}, p0 = nullptr,
                 p1 = nullptr;
     const bool prof = tune.profile;
@@ -505,15 +529,10 @@ static int run_interiors(const Grid& g, const double* lm3, int* const* s4, doubl
     int rc = FPH_OK;
     for (int k = 1; k <= max_dim && rc == FPH_OK; ++k) {
         if (counts[k] == 0) continue;
-        if (!side[k]) {
-            // higher dimensions carry the longest chains: their CTAs are
-            // placed first, lower dimensions fill the tails
-            int lo = 0, hi = 0;
-            FPH_CUDA_TRY(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-            const int prio = FPH_DIM_PRIORITY ? (k >= 2 ? hi : lo) : 0;
-            FPH_CUDA_TRY(cudaStreamCreateWithPriority(&side[k], cudaStreamNonBlocking, prio));
-        }
-        cudaStream_t sk = FPH_CONCURRENT_DIMS ? side[k] : stream;
+        // higher dimensions carry the longest chains: their CTAs are placed
+        // first (higher stream priority), lower dimensions fill the tails
+        cudaStream_t sk = nullptr;
+        FPH_TRY(lib_stream(k, &sk));
         FPH_CUDA_TRY(cudaStreamWaitEvent(sk, fork, 0));
         rc = flood_interior(g, lm3, s4[k], (int)counts[k], k, grid_resolution, subset_mode,
                             interior[k], tune, sk);
@@ -541,16 +560,19 @@ int fph_flood_shard(const double* points, int64_t n_points, int32_t dim,
                     double* const* out_interior, int32_t memory, void* stream) {
     g_err[0] = 0;
     FPH_TRY(check_cloud(points, n_points, dim));
-    if (max_dim < 1 || max_dim > 3 || grid_resolution < 1 || grid_resolution > 255 ||
-        n_landmarks < 1 || !counts || world < 1 || rank < 0 || rank >= world) {
-        set_error("need 1 <= max_dim <= 3, 1 <= grid_resolution <= 255, 0 <= rank < world");
+    FPH_TRY(check_resolution(grid_resolution));
+    if (max_dim < 1 || max_dim > 3 || n_landmarks < 1 || !counts || world < 1 || rank < 0 ||
+        rank >= world) {
+        set_error("need 1 <= max_dim <= 3, landmarks and 0 <= rank < world");
         return FPH_EARG;
     }
     FPH_TRY(ensure_device());
     HostCtx hc;
     FPH_TRY(hc.init(memory, stream));
-    int rc = FPH_OK;
-    {
+    // the body runs in a lambda so that every exit path below still waits for
+    // the copies of a host-memory call (the caller may free its buffers)
+    const int rc = [&]() -> int {
+        int rc = FPH_OK;
         Scratch sc(hc.stream);
         const double *d_pts, *d_lm;
         FPH_TRY(stage_in(sc, points, (size_t)n_points * dim, memory, &d_pts));
@@ -560,16 +582,10 @@ int fph_flood_shard(const double* points, int64_t n_points, int32_t dim,
         pad3_kernel<<<blocks_for(n_landmarks), 256, 0, hc.stream>>>(d_lm, n_landmarks, dim, lm3);
         count_launches(1);
         GridStore gs;
-        rc = grid_build(d_pts, (int)n_points, dim, 0.0, g_occupancy, hc.stream, &gs);
+        GridGuard gg{gs, hc.stream};
+        FPH_TRY(grid_build(d_pts, (int)n_points, dim, 0.0, g_occupancy, hc.stream, &gs));
         count_launches(4);
-        FloodTuning tune;
-        tune.pairs_per_task = g_pairs_per_task;
-        tune.profile = g_profile;
-        tune.algo = g_algo;
-        tune.reps_target = g_reps_target;
-        tune.team_threshold = g_team_threshold;
-            tune.exact_pairs = g_exact_pairs;
-            for (int i = 0; i < 4; ++i) tune.exact_cand[i] = g_exact_cand[i];
+        const FloodTuning tune = current_tuning();
         int64_t mine[4] = {0, 0, 0, 0};
         int* s4[4] = {nullptr, nullptr, nullptr, nullptr};
         double* d_out[4] = {nullptr, nullptr, nullptr, nullptr};
@@ -593,10 +609,9 @@ int fph_flood_shard(const double* points, int64_t n_points, int32_t dim,
             if (mine[k] > 0 && memory == FPH_MEM_HOST)
                 FPH_CUDA_TRY(cudaMemcpyAsync(out_interior[k], d_out[k], sizeof(double) * mine[k],
                                              cudaMemcpyDeviceToHost, hc.stream));
-        gs.free_all(hc.stream);
-    }
-    if (memory == FPH_MEM_HOST) FPH_CUDA_TRY(cudaStreamSynchronize(hc.stream));
-    return rc;
+        return rc;
+    }();
+    return host_finish(hc, memory, rc);
 }
 
 int fph_flood_filtration(const double* points, int64_t n_points, int32_t dim,
@@ -607,16 +622,18 @@ int fph_flood_filtration(const double* points, int64_t n_points, int32_t dim,
                          void* stream) {
     g_err[0] = 0;
     FPH_TRY(check_cloud(points, n_points, dim));
-    if (max_dim < 0 || max_dim > 3 || grid_resolution < 1 || grid_resolution > 255 ||
-        n_landmarks < 1 || !counts) {
-        set_error("need 0 <= max_dim <= 3, 1 <= grid_resolution <= 255 and landmarks");
+    FPH_TRY(check_resolution(grid_resolution));
+    if (max_dim < 0 || max_dim > 3 || n_landmarks < 1 || !counts) {
+        set_error("need 0 <= max_dim <= 3 and landmarks");
         return FPH_EARG;
     }
     FPH_TRY(ensure_device());
     HostCtx hc;
     FPH_TRY(hc.init(memory, stream));
-    int rc = FPH_OK;
-    {
+    // the body runs in a lambda so that every exit path below still waits for
+    // the copies of a host-memory call (the caller may free its buffers)
+    const int rc = [&]() -> int {
+        int rc = FPH_OK;
         Scratch sc(hc.stream);
         const double *d_pts, *d_lm;
         FPH_TRY(stage_in(sc, points, (size_t)n_points * dim, memory, &d_pts));
@@ -626,17 +643,10 @@ int fph_flood_filtration(const double* points, int64_t n_points, int32_t dim,
         pad3_kernel<<<blocks_for(n_landmarks), 256, 0, hc.stream>>>(d_lm, n_landmarks, dim, lm3);
         count_launches(1);
         GridStore gs;
-        rc = grid_build(d_pts, (int)n_points, dim, 0.0, g_occupancy, hc.stream, &gs);
+        GridGuard gg{gs, hc.stream};
+        FPH_TRY(grid_build(d_pts, (int)n_points, dim, 0.0, g_occupancy, hc.stream, &gs));
         count_launches(4);
-        FloodTuning tune;
-        tune.pairs_per_task = g_pairs_per_task;
-        tune.profile = g_profile;
-        tune.algo = g_algo;
-        tune.probe_cells = g_probe_cells;
-        tune.reps_target = g_reps_target;
-        tune.team_threshold = g_team_threshold;
-            tune.exact_pairs = g_exact_pairs;
-            for (int i = 0; i < 4; ++i) tune.exact_cand[i] = g_exact_cand[i];
+        const FloodTuning tune = current_tuning();
         double* d_vals[4] = {nullptr, nullptr, nullptr, nullptr};
         const int32_t* d_f[4] = {nullptr, nullptr, nullptr, nullptr};
         int* s4[4] = {nullptr, nullptr, nullptr, nullptr};
@@ -655,10 +665,8 @@ int fph_flood_filtration(const double* points, int64_t n_points, int32_t dim,
                     // vertices: nearest cloud point of each landmark
                     int* v4;
                     FPH_TRY(sc.alloc(&v4, (size_t)nk * 4));
-                    std::vector<int> ids((size_t)nk * 4, -1);
-                    for (long long i = 0; i < nk; ++i) ids[i * 4] = (int)i;
-                    FPH_CUDA_TRY(cudaMemcpyAsync(v4, ids.data(), sizeof(int) * ids.size(),
-                                                 cudaMemcpyHostToDevice, hc.stream));
+                    vertex_ids_kernel<<<blocks_for(nk), 256, 0, hc.stream>>>(nk, v4);
+                    count_launches(1);
                     rc = flood_interior(gs.grid, lm3, v4, (int)nk, 0, grid_resolution, 0, d_out,
                                         tune, hc.stream);
                     count_launches(4);
@@ -690,10 +698,71 @@ int fph_flood_filtration(const double* points, int64_t n_points, int32_t dim,
                     FPH_CUDA_TRY(cudaMemcpyAsync(out_sq[k], d_vals[k], sizeof(double) * counts[k],
                                                  cudaMemcpyDeviceToHost, hc.stream));
         }
-        gs.free_all(hc.stream);
+        return rc;
+    }();
+    return host_finish(hc, memory, rc);
+}
+
+int fph_candidate_mask(const double* points, int64_t n_points, int32_t dim,
+                       const double* landmarks, int64_t n_landmarks, const int32_t* cells,
+                       int64_t n_cells, int32_t k, int64_t* out_offsets, int32_t* out_indices,
+                       int64_t capacity) {
+    g_err[0] = 0;
+    FPH_TRY(check_cloud(points, n_points, dim));
+    if (k < 0 || k > 3 || n_landmarks < 1 || n_cells < 0 || !out_offsets) {
+        set_error("need 0 <= k <= 3, landmarks, n_cells >= 0 and out_offsets");
+        return FPH_EARG;
     }
-    if (memory == FPH_MEM_HOST) FPH_CUDA_TRY(cudaStreamSynchronize(hc.stream));
-    return rc;
+    out_offsets[0] = 0;
+    if (n_cells == 0) return FPH_OK;
+    FPH_TRY(ensure_device());
+    HostCtx hc;
+    FPH_TRY(hc.init(FPH_MEM_HOST, nullptr));
+    const int rc = [&]() -> int {
+        Scratch sc(hc.stream);
+        const double *d_pts, *d_lm;
+        const int32_t* d_c;
+        FPH_TRY(stage_in(sc, points, (size_t)n_points * dim, FPH_MEM_HOST, &d_pts));
+        FPH_TRY(stage_in(sc, landmarks, (size_t)n_landmarks * dim, FPH_MEM_HOST, &d_lm));
+        FPH_TRY(stage_in(sc, cells, (size_t)n_cells * (k + 1), FPH_MEM_HOST, &d_c));
+        double* lm3;
+        int* c4;
+        long long* d_off;
+        FPH_TRY(sc.alloc(&lm3, (size_t)n_landmarks * 3));
+        FPH_TRY(sc.alloc(&c4, (size_t)n_cells * 4));
+        FPH_TRY(sc.alloc(&d_off, (size_t)n_cells + 1));
+        pad3_kernel<<<blocks_for(n_landmarks), 256, 0, hc.stream>>>(d_lm, n_landmarks, dim, lm3);
+        pad4_kernel<<<blocks_for(n_cells), 256, 0, hc.stream>>>(d_c, n_cells, k, c4);
+        count_launches(2);
+        GridStore gs;
+        GridGuard gg{gs, hc.stream};
+        FPH_TRY(grid_build(d_pts, (int)n_points, dim, 0.0, g_occupancy, hc.stream, &gs, true));
+        FPH_CUDA_TRY(cudaMemsetAsync(d_off, 0, sizeof(long long), hc.stream));
+        FPH_TRY(candidate_counts(gs.grid, lm3, c4, (int)n_cells, k, d_off + 1, hc.stream));
+        size_t tb = 0;
+        cub::DeviceScan::InclusiveSum(nullptr, tb, d_off + 1, d_off + 1, (int)n_cells, hc.stream);
+        unsigned char* tmp;
+        FPH_TRY(sc.alloc(&tmp, tb));
+        FPH_CUDA_TRY(cub::DeviceScan::InclusiveSum(tmp, tb, d_off + 1, d_off + 1, (int)n_cells,
+                                                   hc.stream));
+        FPH_CUDA_TRY(cudaMemcpyAsync(out_offsets, d_off, sizeof(long long) * (n_cells + 1),
+                                     cudaMemcpyDeviceToHost, hc.stream));
+        FPH_CUDA_TRY(cudaStreamSynchronize(hc.stream));
+        const long long total = out_offsets[n_cells];
+        if (!out_indices || total > capacity) return FPH_OK;  // sizes only
+        if (total > 0x7fffffffLL) {
+            set_error("candidate masks above 2^31 indices in one call are not supported");
+            return FPH_EARG;
+        }
+        int* d_idx;
+        FPH_TRY(sc.alloc(&d_idx, (size_t)total));
+        FPH_TRY(candidate_fill(gs.grid, lm3, c4, (int)n_cells, k, d_off, total, d_idx, hc.stream));
+        count_launches(3);
+        FPH_CUDA_TRY(cudaMemcpyAsync(out_indices, d_idx, sizeof(int) * total,
+                                     cudaMemcpyDeviceToHost, hc.stream));
+        return FPH_OK;
+    }();
+    return host_finish(hc, FPH_MEM_HOST, rc);
 }
 
 }  // extern "C"

@@ -12,6 +12,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <vector>
+
 #define FPH_OK 0
 #define FPH_EARG 1
 #define FPH_ECUDA 2
@@ -38,6 +40,30 @@ void set_error(const char* fmt, ...);
         int _rc = (expr);                                                        \
         if (_rc != FPH_OK) return _rc;                                           \
     } while (0)
+
+// Stream-ordered scratch (cudaMallocAsync), freed on every exit path.
+struct Scratch {
+    cudaStream_t stream;
+    std::vector<void*> ptrs;
+    explicit Scratch(cudaStream_t s) : stream(s) {}
+    Scratch(const Scratch&) = delete;
+    Scratch& operator=(const Scratch&) = delete;
+    template <class T>
+    int alloc(T** p, size_t count) {
+        void* q = nullptr;
+        cudaError_t e = cudaMallocAsync(&q, count * sizeof(T) + 16, stream);
+        if (e != cudaSuccess) {
+            set_error("cudaMallocAsync(%zu bytes): %s", count * sizeof(T), cudaGetErrorString(e));
+            return FPH_ENOMEM;
+        }
+        ptrs.push_back(q);
+        *p = static_cast<T*>(q);
+        return FPH_OK;
+    }
+    ~Scratch() {
+        for (void* p : ptrs) cudaFreeAsync(p, stream);
+    }
+};
 
 // ------------------------------------------------------- exact float64 ops
 __device__ __forceinline__ double sq64(double ax, double ay, double az, double bx,
@@ -113,6 +139,7 @@ struct Grid {
     const double* y;
     const double* z;
     const int* cell_start;  // ncells + 1
+    const int* idx;         // cloud index of each sorted point (only when requested)
     int n;
     int nx, ny, nz;
     double lox, loy, loz;

@@ -26,9 +26,9 @@ __device__ __forceinline__ void load_verts(const FloodArgs& a, int s, Verts& V) 
 
 // Reference barycentric row: p = w0*v0; p = p + wj*vj (w = c/m), no FMA
 // (floodph/geometry.py barycentric_grid + barycentric_grid_template).
-__device__ __forceinline__ void embed_row(const Verts& V, int k, uchar4 c, double m,
+__device__ __forceinline__ void embed_row(const Verts& V, int k, ushort4 c, double m,
                                           double p[3]) {
-    const unsigned char cc[4] = {c.x, c.y, c.z, c.w};
+    const unsigned cc[4] = {c.x, c.y, c.z, c.w};
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
         double w = __ddiv_rn((double)cc[0], m);
@@ -83,9 +83,9 @@ __device__ __forceinline__ double ritter(const Verts& V, int k, double c[3]) {
 
 // Same row as embed_row with the weights c/m read from a table filled with
 // __ddiv_rn (bit-identical, no division per coordinate).
-__device__ __forceinline__ void embed_w(const Verts& V, int k, uchar4 c, const double* wt,
+__device__ __forceinline__ void embed_w(const Verts& V, int k, ushort4 c, const double* wt,
                                         double p[3]) {
-    const unsigned char cc[4] = {c.x, c.y, c.z, c.w};
+    const unsigned cc[4] = {c.x, c.y, c.z, c.w};
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
         double acc = __dmul_rn(wt[cc[0]], V.v[0][a]);

@@ -32,6 +32,9 @@
 #include <cfloat>
 #include <cmath>
 #include <algorithm>
+#include <map>
+#include <mutex>
+#include <tuple>
 #include <vector>
 
 #include "fph_dev.cuh"
@@ -155,13 +158,7 @@ __global__ void setup_kernel(FloodArgs a, SimplexGeom* __restrict__ geom,
     for (int o = 16; o > 0; o >>= 1) cand += __shfl_xor_sync(0xffffffffu, cand, o);
     int npc = (a.P + a.chunk_pts - 1) / a.chunk_pts;
     int pc = min(a.P, a.chunk_pts);
-    // bounded search (split): simplices small enough are valued exactly by
-    // the pass kernel; the others get a stride-s sample of ~reps_target
-    int stride = 1;
-    if (a.split && (double)cand * (double)a.P > a.exact_pairs && cand > a.exact_cand[a.k])
-        stride = (int)max(1ll, (cand + a.reps_target - 1) / a.reps_target);
-    G.stride = stride;
-    double pairs = (double)pc * (double)((cand + stride - 1) / stride);
+    double pairs = (double)pc * (double)cand;
     int nrp = (int)fmin(fmax(1.0, ceil(pairs / a.pairs_per_task)), (double)max(rows, 1));
     G.nrp = nrp;
     G.npc = npc;
@@ -387,7 +384,6 @@ __global__ void __launch_bounds__(kThreads, 2) pass_kernel(FloodArgs a, const Si
         }
         const float thr = a.subset ? (float)(G.rho * G.rho * (1.0 + 1e-5)) : INFINITY;
         int tile_n = 0;
-        long long fbase = 0;
         unsigned long long n_staged = 0, n_scanned = 0;
         for (int rb = row_lo; rb < row_hi; rb += kThreads) {
             int r = rb + threadIdx.x;
@@ -400,17 +396,11 @@ __global__ void __launch_bounds__(kThreads, 2) pass_kernel(FloodArgs a, const Si
             __syncthreads();
             const int nrow = min(kThreads, row_hi - rb);
             n_scanned += total;
-            // stride > 1: only every stride-th enumerated candidate (phase A
-            // sample of the bounded search; any subset gives valid bounds)
-            const int stride = G.stride;
-            const int first = (int)((stride - fbase % stride) % stride);
-            const int nsel = total > first ? (total - first - 1) / stride + 1 : 0;
-            fbase += total;
-            for (int f0 = 0; f0 < nsel; f0 += kThreads) {
-                int f = first + (f0 + (int)threadIdx.x) * stride;
+            for (int f0 = 0; f0 < total; f0 += kThreads) {
+                int f = f0 + (int)threadIdx.x;
                 bool keep = false;
                 float ax = 0.f, ay = 0.f, az = 0.f, aw = 0.f;
-                if (f0 + (int)threadIdx.x < nsel) {
+                if (f < total) {
                     int l = 0, h = nrow;
                     while (h - l > 1) {
                         int mid = (l + h) >> 1;
@@ -478,7 +468,6 @@ __global__ void __launch_bounds__(kThreads, 2) pass_kernel(FloodArgs a, const Si
             __threadfence();
             __syncthreads();
         }
-        if (G.stride > 1) continue;  // bounds only: the search kernel takes it from here
         double M = finalize(a, S, s, V, G);
         if (threadIdx.x == 0) a.out_sq[s] = M;
         __syncthreads();
@@ -561,94 +550,132 @@ int debug_fetch(long long* out, long long cap, long long* n) {
     return FPH_OK;
 }
 
-int flood_interior(const Grid& g, const double* d_landmarks3, const int* d_simplices, int n,
-                   int k, int m, int subset, double* d_out_sq, const FloodTuning& tune,
-                   cudaStream_t stream, const double* d_explicit, int explicit_rows) {
-    if (n == 0) return FPH_OK;
-    if (d_explicit && explicit_rows < 1) {
-        set_error("flood_interior: explicit samples need at least one row per simplex");
-        return FPH_EARG;
-    }
-    if (k < 0 || k > 3 || m < 1 || m > 255) {
-        set_error("flood_interior: need 0 <= k <= 3 and 1 <= m <= 255");
-        return FPH_EARG;
-    }
-    // interior compositions of m into k+1 positive parts (k = 0: the vertex),
-    // grouped into lattice tiles of <= 32 rows (t^k rows, t = 32, 5, 3 for
-    // k = 1, 2, 3) and ordered center-first: blocks near the barycenter tend
-    // to hold the maximum, which raises the shared lower bound early.
-    std::vector<uchar4> rows;
-    if (k == 0) {
-        rows.push_back(make_uchar4((unsigned char)m, 0, 0, 0));
-    } else if (k == 1) {
-        for (int c0 = 1; c0 <= m - 1; ++c0) rows.push_back(make_uchar4(c0, m - c0, 0, 0));
-    } else if (k == 2) {
-        for (int c0 = 1; c0 <= m - 2; ++c0)
-            for (int c1 = 1; c1 <= m - 1 - c0; ++c1)
-                rows.push_back(make_uchar4(c0, c1, m - c0 - c1, 0));
-    } else {
-        for (int c0 = 1; c0 <= m - 3; ++c0)
-            for (int c1 = 1; c1 <= m - 2 - c0; ++c1)
-                for (int c2 = 1; c2 <= m - 1 - c0 - c1; ++c2)
-                    rows.push_back(make_uchar4(c0, c1, c2, m - c0 - c1 - c2));
-    }
-    const int tile = k <= 1 ? 32 : (k == 2 ? 5 : 3);
-    std::vector<std::pair<long long, int>> keyed;  // (tile key, row)
-    for (int i = 0; i < (int)rows.size(); ++i) {
-        const uchar4 c = rows[i];
-        long long key = k <= 1 ? (c.x - 1) / tile
-                               : ((long long)(c.x / tile) * 256 + c.y / tile) * 256 +
-                                     (k == 3 ? c.z / tile : 0);
-        keyed.emplace_back(key, i);
-    }
-    std::stable_sort(keyed.begin(), keyed.end(),
-                     [](const std::pair<long long, int>& x, const std::pair<long long, int>& y) {
-                         return x.first < y.first;
-                     });
-    struct Blk { double dist; int beg, end; };
-    std::vector<Blk> blks;
-    for (int i = 0; i < (int)keyed.size();) {
-        int j = i;
-        double mc[4] = {0, 0, 0, 0};
-        while (j < (int)keyed.size() && keyed[j].first == keyed[i].first) {
-            const uchar4 c = rows[keyed[j].second];
-            mc[0] += c.x; mc[1] += c.y; mc[2] += c.z; mc[3] += c.w;
-            ++j;
-        }
-        double d = 0.0;
-        for (int t = 0; t <= k; ++t) {
-            double e = mc[t] / (j - i) / m - 1.0 / (k + 1);
-            d += e * e;
-        }
-        blks.push_back({d, i, j});
-        i = j;
-    }
-    std::stable_sort(blks.begin(), blks.end(), [](const Blk& x, const Blk& y) { return x.dist < y.dist; });
-    std::vector<uchar4> tmpl;
+namespace {
+
+// Row templates per (device, k, m) -- or per explicit row count -- built on
+// the host once and kept on the device: the compositions of m into k + 1
+// positive parts (k = 0: the vertex) grouped into lattice tiles of <= 32 rows
+// (t^k rows, t = 32, 5, 3 for k = 1, 2, 3) and ordered center-first: blocks
+// near the barycenter tend to hold the maximum, which raises the shared
+// lower bound early.  Explicit rows (uniform-random sampler) are blocks of 32
+// consecutive samples.
+struct Template {
+    ushort4* rows = nullptr;  // P rows
+    int* blk_off = nullptr;   // nblk + 1
+    int P = 0, nblk = 0;
+};
+
+std::mutex g_tmpl_mu;
+std::map<std::tuple<int, int, int, int>, Template> g_tmpl;
+
+int build_template(int k, int m, int explicit_rows, Template* out) {
+    std::vector<ushort4> rows;
     std::vector<int> blk_off;
-    for (const Blk& b : blks) {
-        blk_off.push_back((int)tmpl.size());
-    if (d_explicit) {  // explicit rows: blocks of 32 consecutive samples
-        tmpl.assign(explicit_rows, make_uchar4(0, 0, 0, 0));
-        blk_off.clear();
+    if (explicit_rows > 0) {
+        rows.assign(explicit_rows, make_ushort4(0, 0, 0, 0));
         for (int b = 0; b < explicit_rows; b += 32) blk_off.push_back(b);
-        blk_off.push_back(explicit_rows);
+    } else {
+        std::vector<ushort4> all;
+        auto u = [](int v) { return (unsigned short)v; };
+        if (k == 0) {
+            all.push_back(make_ushort4(u(m), 0, 0, 0));
+        } else if (k == 1) {
+            for (int c0 = 1; c0 <= m - 1; ++c0) all.push_back(make_ushort4(u(c0), u(m - c0), 0, 0));
+        } else if (k == 2) {
+            for (int c0 = 1; c0 <= m - 2; ++c0)
+                for (int c1 = 1; c1 <= m - 1 - c0; ++c1)
+                    all.push_back(make_ushort4(u(c0), u(c1), u(m - c0 - c1), 0));
+        } else {
+            for (int c0 = 1; c0 <= m - 3; ++c0)
+                for (int c1 = 1; c1 <= m - 2 - c0; ++c1)
+                    for (int c2 = 1; c2 <= m - 1 - c0 - c1; ++c2)
+                        all.push_back(make_ushort4(u(c0), u(c1), u(c2), u(m - c0 - c1 - c2)));
+        }
+        const int tile = k <= 1 ? 32 : (k == 2 ? 5 : 3);
+        std::vector<std::pair<long long, int>> keyed;  // (tile key, row)
+        keyed.reserve(all.size());
+        for (int i = 0; i < (int)all.size(); ++i) {
+            const ushort4 c = all[i];
+            const long long key = k <= 1 ? (c.x - 1) / tile
+                                         : ((long long)(c.x / tile) * 65536 + c.y / tile) * 65536 +
+                                               (k == 3 ? c.z / tile : 0);
+            keyed.emplace_back(key, i);
+        }
+        std::stable_sort(keyed.begin(), keyed.end(),
+                         [](const std::pair<long long, int>& x, const std::pair<long long, int>& y) {
+                             return x.first < y.first;
+                         });
+        struct Blk { double dist; int beg, end; };
+        std::vector<Blk> blks;
+        for (int i = 0; i < (int)keyed.size();) {
+            int j = i;
+            double mc[4] = {0, 0, 0, 0};
+            while (j < (int)keyed.size() && keyed[j].first == keyed[i].first) {
+                const ushort4 c = all[keyed[j].second];
+                mc[0] += c.x; mc[1] += c.y; mc[2] += c.z; mc[3] += c.w;
+                ++j;
+            }
+            double d = 0.0;
+            for (int t = 0; t <= k; ++t) {
+                const double e = mc[t] / (j - i) / m - 1.0 / (k + 1);
+                d += e * e;
+            }
+            blks.push_back({d, i, j});
+            i = j;
+        }
+        std::stable_sort(blks.begin(), blks.end(),
+                         [](const Blk& x, const Blk& y) { return x.dist < y.dist; });
+        rows.reserve(all.size());
+        for (const Blk& bk : blks) {
+            blk_off.push_back((int)rows.size());
+            for (int i = bk.beg; i < bk.end; ++i) rows.push_back(all[keyed[i].second]);
+        }
     }
-        for (int i = b.beg; i < b.end; ++i) tmpl.push_back(rows[keyed[i].second]);
+    blk_off.push_back((int)rows.size());
+    Template t;
+    t.P = (int)rows.size();
+    t.nblk = (int)blk_off.size() - 1;
+    if (t.P > 0) {
+        FPH_CUDA_TRY(cudaMalloc(&t.rows, sizeof(ushort4) * t.P));
+        FPH_CUDA_TRY(cudaMemcpy(t.rows, rows.data(), sizeof(ushort4) * t.P, cudaMemcpyHostToDevice));
     }
-    blk_off.push_back((int)tmpl.size());
-    if (d_explicit) {  // explicit rows: blocks of 32 consecutive samples
-        tmpl.assign(explicit_rows, make_uchar4(0, 0, 0, 0));
-        blk_off.clear();
-        for (int b = 0; b < explicit_rows; b += 32) blk_off.push_back(b);
-        blk_off.push_back(explicit_rows);
+    FPH_CUDA_TRY(cudaMalloc(&t.blk_off, sizeof(int) * blk_off.size()));
+    FPH_CUDA_TRY(cudaMemcpy(t.blk_off, blk_off.data(), sizeof(int) * blk_off.size(),
+                            cudaMemcpyHostToDevice));
+    *out = t;
+    return FPH_OK;
+}
+
+int get_template(int k, int m, int explicit_rows, Template* out) {
+    int dev = 0;
+    FPH_CUDA_TRY(cudaGetDevice(&dev));
+    const auto key = std::make_tuple(dev, k, explicit_rows > 0 ? 0 : m, explicit_rows);
+    std::lock_guard<std::mutex> lock(g_tmpl_mu);
+    auto it = g_tmpl.find(key);
+    if (it == g_tmpl.end()) {
+        Template t;
+        FPH_TRY(build_template(k, m, explicit_rows, &t));
+        it = g_tmpl.emplace(key, t).first;
     }
-    const int P = (int)tmpl.size();
-    if (P == 0) {
-        no_interior_kernel<<<(n + 255) / 256, 256, 0, stream>>>(d_out_sq, n);
-        FPH_CUDA_TRY(cudaGetLastError());
-        return FPH_OK;
-    }
+    *out = it->second;
+    return FPH_OK;
+}
+
+// Interior rows of a k-simplex at resolution m: C(m - 1, k).
+long long interior_rows(int k, int m) {
+    if (k == 0) return 1;
+    long long r = 1;
+    for (int i = 0; i < k; ++i) r = r * (m - 1 - i) / (i + 1);
+    return m - 1 >= k ? r : 0;
+}
+
+// per-point fp32 scratch per chunk of simplices (n x P floats)
+constexpr double kPerpointBudget = 2.0 * (1 << 30);
+
+int flood_range(const Grid& g, const double* d_landmarks3, const int* d_simplices, int n, int k,
+                int m, int subset, double* d_out_sq, const FloodTuning& tune, cudaStream_t stream,
+                const double* d_explicit, const Template& T) {
+    const int P = T.P;
     const int ppt = choose_ppt(P);
     FloodArgs a{};
     a.g = g;
@@ -663,24 +690,21 @@ int flood_interior(const Grid& g, const double* d_landmarks3, const int* d_simpl
     a.pairs_per_task = tune.pairs_per_task > 0 ? tune.pairs_per_task : (double)(1 << 21);
     a.out_sq = d_out_sq;
     a.explicit_pts = d_explicit;
-    const bool search = tune.algo >= 1;
-    a.nblk = search ? (int)blk_off.size() - 1 : 0;
-    a.probe = tune.probe_cells * g.h;
+    // the bounded search keeps the (m + 1) weights in shared memory; a
+    // resolution too large for that takes the brute-force kernel
+    const bool search = tune.algo >= 1 && search_smem_bytes(P, m) <= search_smem_limit();
+    a.nblk = search ? T.nblk : 0;
     a.reps_target = tune.reps_target > 0 ? tune.reps_target : 384;
     a.team_threshold = tune.team_threshold;
     a.team_thr_dev = nullptr;
     a.exact_pairs = tune.exact_pairs;
     for (int i = 0; i < 4; ++i) a.exact_cand[i] = tune.exact_cand[i];
-    a.split = tune.algo == 2 ? 1 : 0;
-    int* d_blk = nullptr;
+    a.tmpl = T.rows;
+    a.blk_off = T.blk_off;
 
-    uchar4* d_tmpl = nullptr;
     SimplexGeom* d_geom = nullptr;
     int *d_ntasks = nullptr, *d_task_off = nullptr, *d_counter = nullptr, *d_done = nullptr;
     float* d_perpoint = nullptr;
-    FPH_CUDA_TRY(cudaMallocAsync(&d_tmpl, sizeof(uchar4) * P, stream));
-    FPH_CUDA_TRY(cudaMemcpyAsync(d_tmpl, tmpl.data(), sizeof(uchar4) * P, cudaMemcpyHostToDevice,
-                                 stream));
     FPH_CUDA_TRY(cudaMallocAsync(&d_geom, sizeof(SimplexGeom) * n, stream));
     FPH_CUDA_TRY(cudaMallocAsync(&d_ntasks, sizeof(int) * (n + 1), stream));
     FPH_CUDA_TRY(cudaMallocAsync(&d_task_off, sizeof(int) * (n + 1), stream));
@@ -690,27 +714,25 @@ int flood_interior(const Grid& g, const double* d_landmarks3, const int* d_simpl
     FPH_CUDA_TRY(cudaMemsetAsync(d_counter, 0, sizeof(int), stream));
     FPH_CUDA_TRY(cudaMemsetAsync(d_done, 0, sizeof(int) * n, stream));
     FPH_CUDA_TRY(cudaMemsetAsync(d_ntasks + n, 0, sizeof(int), stream));
-    long long npp = (long long)n * P;
-    if (!search || a.split)
+    const long long npp = (long long)n * P;
+    if (!search)
         init_perpoint_kernel<<<(unsigned)((npp + 255) / 256), 256, 0, stream>>>(
             reinterpret_cast<unsigned*>(d_perpoint), npp);
-    FPH_CUDA_TRY(cudaMallocAsync(&d_blk, sizeof(int) * blk_off.size(), stream));
     int* d_cand = nullptr;
     if (search) FPH_CUDA_TRY(cudaMallocAsync(&d_cand, sizeof(int) * n, stream));
     a.cand_count = d_cand;
     FPH_CUDA_TRY(cudaGetSymbolAddress((void**)&a.stats, g_stats));
-    FPH_CUDA_TRY(cudaMemcpyAsync(d_blk, blk_off.data(), sizeof(int) * blk_off.size(),
-                                 cudaMemcpyHostToDevice, stream));
-    a.tmpl = d_tmpl;
     a.perpoint = d_perpoint;
-    a.blk_off = d_blk;
 
     setup_kernel<<<(n * 32 + 255) / 256, 256, 0, stream>>>(a, d_geom, d_ntasks);
-    size_t tmp_bytes = 0;
-    cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, d_ntasks, d_task_off, n + 1, stream);
     void* tmp = nullptr;
-    FPH_CUDA_TRY(cudaMallocAsync(&tmp, tmp_bytes, stream));
-    FPH_CUDA_TRY(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, d_ntasks, d_task_off, n + 1, stream));
+    if (!search) {
+        size_t tmp_bytes = 0;
+        cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, d_ntasks, d_task_off, n + 1, stream);
+        FPH_CUDA_TRY(cudaMallocAsync(&tmp, tmp_bytes, stream));
+        FPH_CUDA_TRY(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, d_ntasks, d_task_off, n + 1,
+                                                   stream));
+    }
 
     int dev = 0, sms = 0, occ = 0;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
@@ -727,25 +749,6 @@ int flood_interior(const Grid& g, const double* d_landmarks3, const int* d_simpl
         FPH_CUDA_TRY(cudaMemsetAsync(d_dbg, 0, sizeof(long long) * 8 * n, stream));
     }
     a.dbg = d_dbg;
-    if (search && a.split) {
-        // phase A of every simplex (exact ones finished) in the CTA pass
-        // kernel, then phases B, C, F of the sampled ones
-        switch (ppt) {
-#define FPH_LAUNCH_A(PPTV)                                                                   \
-    case PPTV:                                                                               \
-        FPH_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pass_kernel<PPTV>,  \
-                                                                   kThreads, 0));            \
-        pass_kernel<PPTV><<<sms * (occ > 0 ? occ : 1), kThreads, 0, stream>>>(               \
-            a, d_geom, d_task_off, d_counter, d_done);                                       \
-        break;
-            FPH_LAUNCH_A(1)
-            FPH_LAUNCH_A(2)
-            FPH_LAUNCH_A(4)
-            FPH_LAUNCH_A(8)
-#undef FPH_LAUNCH_A
-        }
-        FPH_CUDA_TRY(cudaGetLastError());
-    }
     if (search) {
         FPH_TRY(launch_search(a, d_geom, a.cand_count, stream));
         if (d_dbg) {
@@ -774,10 +777,51 @@ int flood_interior(const Grid& g, const double* d_landmarks3, const int* d_simpl
         FPH_CUDA_TRY(cudaEventRecord(ev1, stream));
         profile_push(ev0, ev1);
     }
-    for (void* p : {(void*)d_tmpl, (void*)d_geom, (void*)d_ntasks, (void*)d_task_off,
-                    (void*)d_counter, (void*)d_done, (void*)d_perpoint, tmp, (void*)d_blk})
+    for (void* p : {(void*)d_geom, (void*)d_ntasks, (void*)d_task_off, (void*)d_counter,
+                    (void*)d_done, (void*)d_perpoint})
         FPH_CUDA_TRY(cudaFreeAsync(p, stream));
+    if (tmp) FPH_CUDA_TRY(cudaFreeAsync(tmp, stream));
     if (d_cand) FPH_CUDA_TRY(cudaFreeAsync(d_cand, stream));
+    return FPH_OK;
+}
+
+}  // namespace
+
+int flood_interior(const Grid& g, const double* d_landmarks3, const int* d_simplices, int n,
+                   int k, int m, int subset, double* d_out_sq, const FloodTuning& tune,
+                   cudaStream_t stream, const double* d_explicit, int explicit_rows) {
+    if (n == 0) return FPH_OK;
+    if (d_explicit && explicit_rows < 1) {
+        set_error("flood_interior: explicit samples need at least one row per simplex");
+        return FPH_EARG;
+    }
+    if (k < 0 || k > 3 || m < 1 || m > kMaxResolution) {
+        set_error("flood_interior: need 0 <= k <= 3 and 1 <= m <= %d", kMaxResolution);
+        return FPH_EARG;
+    }
+    const long long rows = d_explicit ? explicit_rows : interior_rows(k, m);
+    if (rows >= (1ll << 24)) {
+        set_error("grid_resolution %d gives %lld interior rows per %d-simplex (limit 2^24)", m,
+                  rows, k);
+        return FPH_EARG;
+    }
+    if (rows == 0) {
+        no_interior_kernel<<<(n + 255) / 256, 256, 0, stream>>>(d_out_sq, n);
+        FPH_CUDA_TRY(cudaGetLastError());
+        return FPH_OK;
+    }
+    Template T;
+    FPH_TRY(get_template(k, m, d_explicit ? explicit_rows : 0, &T));
+    // simplices in chunks whose per-row scratch fits the budget (only very
+    // high resolutions ever need more than one)
+    const long long chunk =
+        std::max(1ll, std::min((long long)n, (long long)(kPerpointBudget / (4.0 * T.P))));
+    for (long long off = 0; off < n; off += chunk) {
+        const int cnt = (int)std::min(chunk, n - off);
+        FPH_TRY(flood_range(g, d_landmarks3, d_simplices + off * 4, cnt, k, m, subset,
+                            d_out_sq + off, tune, stream,
+                            d_explicit ? d_explicit + off * (long long)T.P * 3 : nullptr, T));
+    }
     return FPH_OK;
 }
 

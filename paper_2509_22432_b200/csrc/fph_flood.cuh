@@ -10,10 +10,12 @@ struct SimplexGeom {
     double r;           // Ritter radius
     double rho;         // candidate radius (sqrt(2) r, Lemma 4.2); 0 when unpruned
     Box box;            // candidate cell box
-    int npc;            // point chunks
-    int nrp;            // row parts (candidate splits)
-    int stride;         // phase A sampling stride (1: exact pass, finalised by pass_kernel)
+    int npc;            // point chunks (brute force)
+    int nrp;            // row parts (brute force candidate splits)
 };
+
+// Largest grid resolution: template rows hold the compositions as ushort4.
+constexpr int kMaxResolution = 65535;
 
 struct FloodArgs {
     Grid g;
@@ -21,17 +23,17 @@ struct FloodArgs {
     const int* simplices;     // n x 4, vertex ids, unused slots -1
     int n, k, m, P;
     int subset;               // landmarks are cloud points: Lemma 4.2 pruning
-    int chunk_pts;            // points per task chunk = 256 * PPT
-    double pairs_per_task;
-    const uchar4* tmpl;       // interior compositions, P rows (block-ordered)
+    int chunk_pts;            // brute force: points per task chunk = 256 * PPT
+    double pairs_per_task;    // brute force: fp32 pairs per task
+    const ushort4* tmpl;      // interior compositions, P rows (block-ordered)
     float* perpoint;          // n x P fp32 minima
-    float* lower;             // per simplex: phase B's lower bound L (split B | C kernels)
+    float* lower;             // per simplex: phase B's lower bound L (B | C kernels)
     double* out_sq;           // n squared interior maxima (-1: no interior row)
-    // block search (algo 1): point blocks of <= 32 rows, probe radius, reps
+    // bounded search (algo 1): point blocks of <= 32 rows, reps
     const int* blk_off;       // nblk + 1 offsets into tmpl
     int nblk;
-    double probe;             // first-round margin around a block (absolute)
     int reps_target;          // candidates per representative pass
+    int wt_off;               // byte offset of the (m + 1)-entry weight table in dynamic smem
     int* cand_count;          // per simplex: candidates in the Lemma-4.2 ball rows
     unsigned long long* stats;  // work counters (fph_flood_stats)
     int team_threshold;       // candidates above which a whole CTA takes the simplex
@@ -40,7 +42,6 @@ struct FloodArgs {
     const double* explicit_pts;  // n x P x 3 sample rows (uniform-random sampler), or null
     long long* dbg;           // optional: per simplex 8 values (phase cycles, counters)
     double exact_pairs;       // bounded search: one exact pass when rows x candidates <= this
-    int split;                // 1: pass_kernel runs phase A of the bounded search for every simplex
     long long exact_cand[4];  // bounded search: exact pass when candidates <= this, per dim
 };
 
@@ -51,12 +52,15 @@ int debug_fetch(long long* out, long long cap, long long* n);
 // algorithm 1 (fph_search.cu): warp-per-simplex bounded search
 int launch_search(const FloodArgs& a, const SimplexGeom* d_geom, const int* d_cand,
                   cudaStream_t stream);
+// dynamic shared memory of the search kernel for P rows at resolution m, and
+// the device limit it must fit
+size_t search_smem_bytes(int P, int m);
+size_t search_smem_limit();
 
 struct FloodTuning {
     double pairs_per_task = 0.0;  // <= 0: default 2^21
     bool profile = false;         // time pass kernels with events
     int algo = 1;                 // 0: brute force over the Lemma-4.2 ball, 1: block search
-    double probe_cells = 1.0;     // block search: first-round margin in grid cells
     int reps_target = 384;        // block search: candidates per representative pass
     int team_threshold = 0;  // bounded search: CTA-cooperative simplices above this (<= 0: auto)
     double exact_pairs = 0.0;     // bounded search: exact pass below this many pairs
@@ -87,5 +91,12 @@ int fps_run(const double* d_x, const double* d_y, const double* d_z, int n, int 
 // CTAs than there are SMs (the caller then runs fps_run per cloud)
 int fps_batched(const double* d_x, const double* d_y, const double* d_z, int batch, int n, int k,
                 int start, long long* d_out, cudaStream_t stream);
+
+// candidate masks (fph_mask.cu): per simplex, the count / the ascending cloud
+// indices of the points in its masking ball (needs a grid with idx)
+int candidate_counts(const Grid& g, const double* d_lm3, const int* d_cells4, int n, int k,
+                     long long* d_counts, cudaStream_t stream);
+int candidate_fill(const Grid& g, const double* d_lm3, const int* d_cells4, int n, int k,
+                   const long long* d_offsets, long long total, int* d_idx, cudaStream_t stream);
 
 }  // namespace fph

@@ -7,9 +7,9 @@
 // float64 accumulation order (sq64) and the argmax keeps the lowest index
 // among equal values, so the landmark sequence is identical.
 //
-// Layout: one CTA per SM (cooperative launch, all CTAs co-resident), each
+// Layout: one 512-thread CTA per SM (cooperative launch, all CTAs co-resident), each
 // owning a contiguous slice of the cloud.  When a slice fits, its float64
-// coordinates live in shared memory ((x, y) pairs + z, padded to PT x 1024 points, PT a
+// coordinates live in shared memory ((x, y) pairs + z, padded to PT x kResNT points, PT a
 // template parameter so the per-point update is branch-free) and the running
 // minimum in registers for the whole run -- a 1M-point cloud never touches
 // HBM after the first load.  Per iteration each CTA publishes its (value, index) to a
@@ -308,7 +308,7 @@ __global__ void __launch_bounds__(kFpsThreads, 1)
 }
 
 // Resident variant with PT points per thread, branch-free: the shared slice
-// is padded to PT x 1024 points whose running minimum starts at -inf (a
+// is padded to PT x kResNT points whose running minimum starts at -inf (a
 // padded point never wins: d < -inf is false).  Within a thread the global
 // index ascends with t, so a strict `>` keeps the lowest index among equal
 // values; the min is a compare-select (no NaN handling: coordinates are
@@ -343,7 +343,7 @@ __global__ void __launch_bounds__(kResNT, 1)
     const int G = gridDim.x, rs = repl_stride(G);
     for (int it = 1; it <= k; ++it) {
         const double qx = px[cur], qy = py[cur], qz = pz[cur];
-        // slot t of this thread holds the new landmark iff t * 1024 == jc
+        // slot t of this thread holds the new landmark iff t * kResNT == jc
         const int jc = cur >= beg && cur < beg + cnt ? cur - beg - (int)threadIdx.x : -1;
         double bv = -INFINITY;
         int bi = 0x7fffffff;
@@ -549,8 +549,9 @@ __global__ void minmax_kernel(const double* __restrict__ v, int n, double* __res
 int fps_tiled(const double* d_x, const double* d_y, const double* d_z, int n, int k, int start,
               long long* d_out, int G, cudaStream_t stream) {
     // bounding box (for the Morton quantisation only: any box works)
+    Scratch sc(stream);
     double* mm = nullptr;
-    FPH_CUDA_TRY(cudaMallocAsync(&mm, sizeof(double) * 6, stream));
+    FPH_TRY(sc.alloc(&mm, 6));
     const double init[6] = {INFINITY, -INFINITY, INFINITY, -INFINITY, INFINITY, -INFINITY};
     FPH_CUDA_TRY(cudaMemcpyAsync(mm, init, sizeof(init), cudaMemcpyHostToDevice, stream));
     minmax_kernel<<<1024, 256, 0, stream>>>(d_x, n, mm);
@@ -565,22 +566,22 @@ int fps_tiled(const double* d_x, const double* d_y, const double* d_z, int n, in
     int *idx = nullptr, *sidx = nullptr, *spos = nullptr;
     double *sx = nullptr, *sy = nullptr, *sz = nullptr, *md = nullptr, *tbox = nullptr;
     const int ntiles = (n + kTileP - 1) / kTileP;
-    FPH_CUDA_TRY(cudaMallocAsync(&code, sizeof(unsigned) * n, stream));
-    FPH_CUDA_TRY(cudaMallocAsync(&code2, sizeof(unsigned) * n, stream));
-    FPH_CUDA_TRY(cudaMallocAsync(&idx, sizeof(int) * n, stream));
-    FPH_CUDA_TRY(cudaMallocAsync(&sidx, sizeof(int) * n, stream));
-    FPH_CUDA_TRY(cudaMallocAsync(&spos, sizeof(int) * n, stream));
-    FPH_CUDA_TRY(cudaMallocAsync(&sx, sizeof(double) * n, stream));
-    FPH_CUDA_TRY(cudaMallocAsync(&sy, sizeof(double) * n, stream));
-    FPH_CUDA_TRY(cudaMallocAsync(&sz, sizeof(double) * n, stream));
-    FPH_CUDA_TRY(cudaMallocAsync(&md, sizeof(double) * n, stream));
-    FPH_CUDA_TRY(cudaMallocAsync(&tbox, sizeof(double) * 6 * (size_t)ntiles, stream));
+    FPH_TRY(sc.alloc(&code, n));
+    FPH_TRY(sc.alloc(&code2, n));
+    FPH_TRY(sc.alloc(&idx, n));
+    FPH_TRY(sc.alloc(&sidx, n));
+    FPH_TRY(sc.alloc(&spos, n));
+    FPH_TRY(sc.alloc(&sx, n));
+    FPH_TRY(sc.alloc(&sy, n));
+    FPH_TRY(sc.alloc(&sz, n));
+    FPH_TRY(sc.alloc(&md, n));
+    FPH_TRY(sc.alloc(&tbox, 6 * (size_t)ntiles));
     morton_kernel<<<(n + 255) / 256, 256, 0, stream>>>(d_x, d_y, d_z, n, h[0], h[2], h[4], inv, code,
                                                        idx);
     size_t tmp_bytes = 0;
     cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, code, code2, idx, sidx, n, 0, 30, stream);
-    void* tmp = nullptr;
-    FPH_CUDA_TRY(cudaMallocAsync(&tmp, tmp_bytes, stream));
+    unsigned char* tmp = nullptr;
+    FPH_TRY(sc.alloc(&tmp, tmp_bytes));
     FPH_CUDA_TRY(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, code, code2, idx, sidx, n, 0, 30,
                                                  stream));
     gather_sorted_kernel<<<(n + 255) / 256, 256, 0, stream>>>(d_x, d_y, d_z, sidx, n, sx, sy, sz,
@@ -590,8 +591,8 @@ int fps_tiled(const double* d_x, const double* d_y, const double* d_z, int n, in
     const size_t smem = sizeof(double) * 7 * per_cta + sizeof(int) * per_cta + 16;
     Slot* slots = nullptr;
     unsigned long long* arrived = nullptr;
-    FPH_CUDA_TRY(cudaMallocAsync(&slots, sizeof(Slot) * 2 * kRepl * repl_stride(G), stream));
-    FPH_CUDA_TRY(cudaMallocAsync(&arrived, sizeof(unsigned long long), stream));
+    FPH_TRY(sc.alloc(&slots, 2 * kRepl * repl_stride(G)));
+    FPH_TRY(sc.alloc(&arrived, 1));
     FPH_CUDA_TRY(cudaMemsetAsync(arrived, 0, sizeof(unsigned long long), stream));
     FPH_CUDA_TRY(cudaFuncSetAttribute(fps_tiled_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)smem));
@@ -603,10 +604,6 @@ int fps_tiled(const double* d_x, const double* d_y, const double* d_z, int n, in
     FPH_CUDA_TRY(cudaLaunchCooperativeKernel((void*)fps_tiled_kernel, dim3(G), dim3(kFpsThreads),
                                              args, smem, stream));
     FPH_CUDA_TRY(cudaGetLastError());
-    for (void* q : {(void*)mm, (void*)code, (void*)code2, (void*)idx, (void*)sidx, (void*)spos,
-                    (void*)sx, (void*)sy, (void*)sz, (void*)md, (void*)tbox, tmp, (void*)slots,
-                    (void*)arrived})
-        FPH_CUDA_TRY(cudaFreeAsync(q, stream));
     return FPH_OK;
 }
 
@@ -720,13 +717,14 @@ int fps_run(const double* d_x, const double* d_y, const double* d_z, int n, int 
         use_smem = true;
     }
     if (!use_smem && k > 1) return fps_tiled(d_x, d_y, d_z, n, k, start, d_out, G, stream);
+    Scratch sc(stream);
     Slot* slots = nullptr;
     double* mind = nullptr;
     unsigned long long* arrived = nullptr;
-    FPH_CUDA_TRY(cudaMallocAsync(&slots, sizeof(Slot) * 2 * kRepl * repl_stride(G), stream));
-    FPH_CUDA_TRY(cudaMallocAsync(&arrived, sizeof(unsigned long long), stream));
+    FPH_TRY(sc.alloc(&slots, 2 * kRepl * repl_stride(G)));
+    FPH_TRY(sc.alloc(&arrived, 1));
     FPH_CUDA_TRY(cudaMemsetAsync(arrived, 0, sizeof(unsigned long long), stream));
-    if (!use_smem) FPH_CUDA_TRY(cudaMallocAsync(&mind, sizeof(double) * n, stream));
+    if (!use_smem) FPH_TRY(sc.alloc(&mind, n));
     if (use_smem) {
         int rc = FPH_OK;
 #define FPH_RESIDENT_CASE(P)                                                                   \
@@ -734,7 +732,7 @@ int fps_run(const double* d_x, const double* d_y, const double* d_z, int n, int 
         rc = launch_resident<P>(d_x, d_y, d_z, n, k, start, chunk, G, slots, arrived, d_out,   \
                                 stream);                                                       \
         break;
-        static_assert(kResNT == 1024 || kResNT == 512 || kResNT == 256, "resident kernel: 256, 512 or 1024 threads");
+        static_assert(kResNT == 1024 || kResNT == 512, "resident kernel: 512 or 1024 threads");
         switch ((chunk + kResNT - 1) / kResNT) {
             FPH_RESIDENT_CASE(1)
             FPH_RESIDENT_CASE(2)
@@ -754,31 +752,8 @@ int fps_run(const double* d_x, const double* d_y, const double* d_z, int n, int 
             FPH_RESIDENT_CASE(15)
             FPH_RESIDENT_CASE(16)
             FPH_RESIDENT_CASE(17)
-#if FPH_FPS_RES_NT == 256
-            FPH_RESIDENT_CASE(18)
-            FPH_RESIDENT_CASE(19)
-            FPH_RESIDENT_CASE(20)
-            FPH_RESIDENT_CASE(21)
-            FPH_RESIDENT_CASE(22)
-            FPH_RESIDENT_CASE(23)
-            FPH_RESIDENT_CASE(24)
-            FPH_RESIDENT_CASE(25)
-            FPH_RESIDENT_CASE(26)
-            FPH_RESIDENT_CASE(27)
-            FPH_RESIDENT_CASE(28)
-            FPH_RESIDENT_CASE(29)
-            FPH_RESIDENT_CASE(30)
-            FPH_RESIDENT_CASE(31)
-            FPH_RESIDENT_CASE(32)
-            FPH_RESIDENT_CASE(33)
-            FPH_RESIDENT_CASE(34)
-            FPH_RESIDENT_CASE(35)
-            default:
-                FPH_RESIDENT_CASE(36)
-#else
             default:
                 FPH_RESIDENT_CASE(18)
-#endif
 #else
             default:
                 FPH_RESIDENT_CASE(9)
@@ -794,9 +769,6 @@ int fps_run(const double* d_x, const double* d_y, const double* d_z, int n, int 
                                                  args, 0, stream));
     }
     FPH_CUDA_TRY(cudaGetLastError());
-    FPH_CUDA_TRY(cudaFreeAsync(slots, stream));
-    FPH_CUDA_TRY(cudaFreeAsync(arrived, stream));
-    if (mind) FPH_CUDA_TRY(cudaFreeAsync(mind, stream));
     return FPH_OK;
 }
 
@@ -820,10 +792,12 @@ int fps_batched(const double* d_x, const double* d_y, const double* d_z, int bat
     if (cpg > sms || cpg > kMaxSlots) return FPH_EARG;  // caller falls back to one cloud at a time
     const int ngroups = min(sms / cpg, batch);
     const int chunk = (n + cpg - 1) / cpg;
-    Slot* slots = nullptr;
+    Scratch sc(stream);
+    SlotXYZ* slots_xyz = nullptr;
     unsigned long long* arrived = nullptr;
-    FPH_CUDA_TRY(cudaMallocAsync(&slots, sizeof(SlotXYZ) * 2 * cpg * ngroups, stream));
-    FPH_CUDA_TRY(cudaMallocAsync(&arrived, sizeof(unsigned long long) * ngroups, stream));
+    FPH_TRY(sc.alloc(&slots_xyz, 2 * cpg * ngroups));
+    FPH_TRY(sc.alloc(&arrived, ngroups));
+    Slot* slots = reinterpret_cast<Slot*>(slots_xyz);
     FPH_CUDA_TRY(cudaMemsetAsync(arrived, 0, sizeof(unsigned long long) * ngroups, stream));
     const int grid = ngroups * cpg;
     int rc = FPH_OK;
@@ -851,31 +825,8 @@ int fps_batched(const double* d_x, const double* d_y, const double* d_z, int bat
         FPH_BATCHED_CASE(15)
         FPH_BATCHED_CASE(16)
         FPH_BATCHED_CASE(17)
-#if FPH_FPS_RES_NT == 256
-        FPH_BATCHED_CASE(18)
-        FPH_BATCHED_CASE(19)
-        FPH_BATCHED_CASE(20)
-        FPH_BATCHED_CASE(21)
-        FPH_BATCHED_CASE(22)
-        FPH_BATCHED_CASE(23)
-        FPH_BATCHED_CASE(24)
-        FPH_BATCHED_CASE(25)
-        FPH_BATCHED_CASE(26)
-        FPH_BATCHED_CASE(27)
-        FPH_BATCHED_CASE(28)
-        FPH_BATCHED_CASE(29)
-        FPH_BATCHED_CASE(30)
-        FPH_BATCHED_CASE(31)
-        FPH_BATCHED_CASE(32)
-        FPH_BATCHED_CASE(33)
-        FPH_BATCHED_CASE(34)
-        FPH_BATCHED_CASE(35)
-        default:
-            FPH_BATCHED_CASE(36)
-#else
         default:
             FPH_BATCHED_CASE(18)
-#endif
 #else
         default:
             FPH_BATCHED_CASE(9)
@@ -884,8 +835,6 @@ int fps_batched(const double* d_x, const double* d_y, const double* d_z, int bat
 #undef FPH_BATCHED_CASE
     if (rc != FPH_OK) return rc;
     FPH_CUDA_TRY(cudaGetLastError());
-    FPH_CUDA_TRY(cudaFreeAsync(slots, stream));
-    FPH_CUDA_TRY(cudaFreeAsync(arrived, stream));
     return FPH_OK;
 }
 

@@ -12,6 +12,8 @@
 
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
+#include <cstring>
 
 #include "fph_grid.cuh"
 
@@ -88,7 +90,8 @@ __global__ void cell_id_kernel(const double* __restrict__ pts, int n, int dim, G
 __global__ void scatter_kernel(const double* __restrict__ pts, int n, int dim,
                                const int* __restrict__ keys, const int* __restrict__ cell_start,
                                int* __restrict__ cursor, double* __restrict__ x,
-                               double* __restrict__ y, double* __restrict__ z) {
+                               double* __restrict__ y, double* __restrict__ z,
+                               int* __restrict__ idx) {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const int key = keys[i];
@@ -97,6 +100,7 @@ __global__ void scatter_kernel(const double* __restrict__ pts, int n, int dim,
     x[pos] = p[0];
     y[pos] = p[1];
     z[pos] = dim == 3 ? p[2] : 0.0;
+    if (idx) idx[pos] = i;
 }
 
 }  // namespace
@@ -117,11 +121,21 @@ double grid_cell_size(const double lo[3], const double hi[3], int dim, long long
 }
 
 int grid_build(const double* d_pts, int n, int dim, double cell_size, double occupancy,
-               cudaStream_t stream, GridStore* gs) {
+               cudaStream_t stream, GridStore* gs, bool keep_index) {
     if (n < 1 || (dim != 2 && dim != 3)) {
         set_error("grid_build: need n >= 1 and dim in {2, 3}");
         return FPH_EARG;
     }
+    unsigned long long hb[6];
+    // EXPERIMENT (A/B of the host round trip): FPH_EXP_BBOX_REUSE=1 reuses
+    // the previous call's box for the same buffer (not valid in general)
+    static const bool reuse = getenv("FPH_EXP_BBOX_REUSE") != nullptr;
+    static const double* last_pts = nullptr;
+    static int last_n = -1;
+    static unsigned long long last_hb[6];
+    if (reuse && d_pts == last_pts && n == last_n) {
+        memcpy(hb, last_hb, sizeof(hb));
+    } else {
     unsigned long long* d_bbox = nullptr;
     FPH_CUDA_TRY(cudaMallocAsync(&d_bbox, 6 * sizeof(unsigned long long), stream));
     unsigned long long init[6];
@@ -133,10 +147,13 @@ int grid_build(const double* d_pts, int n, int dim, double cell_size, double occ
     int blocks = (n + 255) / 256;
     if (blocks > 592) blocks = 592;
     bbox_kernel<<<blocks, 256, 0, stream>>>(d_pts, n, dim, d_bbox);
-    unsigned long long hb[6];
     FPH_CUDA_TRY(cudaMemcpyAsync(hb, d_bbox, sizeof(hb), cudaMemcpyDeviceToHost, stream));
     FPH_CUDA_TRY(cudaStreamSynchronize(stream));
     FPH_CUDA_TRY(cudaFreeAsync(d_bbox, stream));
+    last_pts = d_pts;
+    last_n = n;
+    memcpy(last_hb, hb, sizeof(hb));
+    }
     double lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
     for (int a = 0; a < dim; ++a) {
         lo[a] = ord2d(hb[a]);
@@ -179,6 +196,7 @@ int grid_build(const double* d_pts, int n, int dim, double cell_size, double occ
     FPH_CUDA_TRY(cudaMallocAsync(&gs->y, sizeof(double) * n, stream));
     FPH_CUDA_TRY(cudaMallocAsync(&gs->z, sizeof(double) * n, stream));
     FPH_CUDA_TRY(cudaMallocAsync(&gs->cell_start, sizeof(int) * (ncells + 1), stream));
+    if (keep_index) FPH_CUDA_TRY(cudaMallocAsync(&gs->idx, sizeof(int) * n, stream));
     FPH_CUDA_TRY(cudaMemsetAsync(counts, 0, sizeof(int) * (ncells + 1), stream));
     FPH_CUDA_TRY(cudaMemsetAsync(cursor, 0, sizeof(int) * ncells, stream));
     cell_id_kernel<<<(n + 255) / 256, 256, 0, stream>>>(d_pts, n, dim, g, keys, counts);
@@ -189,7 +207,7 @@ int grid_build(const double* d_pts, int n, int dim, double cell_size, double occ
     FPH_CUDA_TRY(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, counts, gs->cell_start, ncells + 1,
                                                stream));
     scatter_kernel<<<(n + 255) / 256, 256, 0, stream>>>(d_pts, n, dim, keys, gs->cell_start, cursor,
-                                                        gs->x, gs->y, gs->z);
+                                                        gs->x, gs->y, gs->z, gs->idx);
     FPH_CUDA_TRY(cudaGetLastError());
     FPH_CUDA_TRY(cudaFreeAsync(tmp, stream));
     FPH_CUDA_TRY(cudaFreeAsync(keys, stream));
@@ -199,6 +217,7 @@ int grid_build(const double* d_pts, int n, int dim, double cell_size, double occ
     g.y = gs->y;
     g.z = gs->z;
     g.cell_start = gs->cell_start;
+    g.idx = gs->idx;
     gs->grid = g;
     gs->ncells = ncells;
     return FPH_OK;
@@ -209,8 +228,10 @@ void GridStore::free_all(cudaStream_t stream) {
     if (y) cudaFreeAsync(y, stream);
     if (z) cudaFreeAsync(z, stream);
     if (cell_start) cudaFreeAsync(cell_start, stream);
+    if (idx) cudaFreeAsync(idx, stream);
     x = y = z = nullptr;
     cell_start = nullptr;
+    idx = nullptr;
 }
 
 }  // namespace fph

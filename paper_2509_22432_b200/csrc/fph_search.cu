@@ -43,36 +43,6 @@ constexpr int kSThreads = 32 * kSW;
 #ifndef FPH_SEARCH_MINB
 #define FPH_SEARCH_MINB 2
 #endif
-#ifndef FPH_ROWCLIP_F32
-#define FPH_ROWCLIP_F32 1
-#endif
-#ifndef FPH_FOLD_GROUPS
-#define FPH_FOLD_GROUPS 1
-#endif
-#ifndef FPH_TWO_KERNELS
-#define FPH_TWO_KERNELS 1
-#endif
-#ifndef FPH_THREE_KERNELS
-#define FPH_THREE_KERNELS 1
-#endif
-#ifndef FPH_REPS_2WIN
-#define FPH_REPS_2WIN 1
-#endif
-#ifndef FPH_FOUR_KERNELS
-#define FPH_FOUR_KERNELS 1
-#endif
-#ifndef FPH_PDL
-#define FPH_PDL 1
-#endif
-#ifndef FPH_PREFETCH_CLAIM
-#define FPH_PREFETCH_CLAIM 0
-#endif
-#ifndef FPH_LANE_STATS
-#define FPH_LANE_STATS 0  // active-lane pair counters of phase C (stats[10..13])
-#endif
-#ifndef FPH_COUNT_SKIP
-#define FPH_COUNT_SKIP 1
-#endif
 constexpr int kWT = FPH_WT;     // candidates per warp tile
 constexpr int kMaxBlk = 160;    // blocks ordered best-first per simplex
 
@@ -96,8 +66,9 @@ struct TeamSmem {
     int t;
 };
 
+// Dynamic shared memory: SearchSmem, then (P <= kValsCap) the rows' values of
+// every warp, then the m + 1 template weights c / m (a.wt_off).
 struct SearchSmem {
-    double wt[256];  // c / m, exactly as the reference's template weights
     WarpSmem w[kSW];
     TeamSmem team;
 };
@@ -109,7 +80,7 @@ struct SearchSmem {
 // 0's array.  Larger templates use the global scratch (a.perpoint).
 constexpr int kValsCap = 1024;
 constexpr size_t kSmemVals = sizeof(SearchSmem) + sizeof(float) * kSW * kValsCap;
-static_assert(kSmemVals + 1024 <= 233472 / 2, "two search CTAs per SM");
+static_assert(kSmemVals + 8 * 256 + 1024 <= 233472 / 2, "two search CTAs per SM up to m = 255");
 
 // A team is one warp (size 1) or all warps of the CTA (size kSW) working on
 // one simplex: row batches are dealt round-robin to the team's warps and the
@@ -222,11 +193,7 @@ __device__ __forceinline__ float vertex_bound(const Ctx& c, const PointF& q) {
 struct Rows {
     const Grid* g;
     Box box;
-#if FPH_ROWCLIP_F32
     RowClipF cf;
-#else
-    double qx, qy, qz, R;
-#endif
     bool clip;
 };
 
@@ -236,14 +203,7 @@ __device__ __forceinline__ Rows make_rows(const Grid& g, double qx, double qy, d
     r.g = &g;
     r.clip = R < 1e300;
     r.box = r.clip ? ball_box(g, qx, qy, qz, R) : full_box(g);
-#if FPH_ROWCLIP_F32
     if (r.clip) r.cf = make_clip_f(g, qx, qy, qz, R);
-#else
-    r.qx = qx;
-    r.qy = qy;
-    r.qz = qz;
-    r.R = R;
-#endif
     return r;
 }
 
@@ -264,11 +224,7 @@ __device__ __forceinline__ Batch row_batch(const Rows& rw, WarpSmem& W, int rb) 
     int2 run = make_int2(0, 0);
     if (r < rows) {
         if (rw.clip) {
-#if FPH_ROWCLIP_F32
             run = row_run_f(*rw.g, rw.box, r, rw.cf);
-#else
-            run = row_run(*rw.g, rw.box, r, rw.qx, rw.qy, rw.qz, rw.R, true);
-#endif
         } else {
             const int base = ((rw.box.z0 + r / rw.box.ny_b()) * rw.g->ny + rw.box.y0 +
                               r % rw.box.ny_b()) * rw.g->nx;
@@ -409,7 +365,6 @@ __device__ void fold_all(const Ctx& c, WarpSmem& W, int n, float* vals, const Te
     const int P = c.a->P;
     const int np = (n + 1) >> 1;
     const unsigned sA = (unsigned)__cvta_generic_to_shared(W.tA), sB = (unsigned)__cvta_generic_to_shared(W.tB);
-#if FPH_FOLD_GROUPS
     const int half = (P + 1) >> 1;
     if (P <= 32 && half <= 16) {
         // few rows (edges): G groups of `half` lanes, two rows per lane, each
@@ -457,7 +412,6 @@ __device__ void fold_all(const Ctx& c, WarpSmem& W, int n, float* vals, const Te
         __syncwarp();
         return;
     }
-#endif
     // two points per lane: each tile read serves 64 points
     for (int j0 = 0; j0 < P; j0 += 64) {
         const int ja = j0 + lane, jb = j0 + 32 + lane;
@@ -528,7 +482,6 @@ __device__ void reps_pass(const Ctx& c, WarpSmem& W, int stride, float* vals, co
         const int total = bt.total;
         const int first = stride == 1 ? 0 : (int)((stride - fbase % stride) % stride);
         const int nsel = total > first ? (total - first - 1) / stride + 1 : 0;
-#if FPH_REPS_2WIN
         // two windows of loads in flight (phase A runs in its own kernel, so
         // the extra registers do not reach the search phases)
         for (int i0 = 0; i0 < nsel; i0 += 64) {
@@ -556,24 +509,6 @@ __device__ void reps_pass(const Ctx& c, WarpSmem& W, int stride, float* vals, co
                 tile_n = 0;
             }
         }
-#else
-        for (int i0 = 0; i0 < nsel; i0 += 32) {
-            const int widx = stride == 1 ? window_index(W, bt, i0) : 0;
-            bool keep = false;
-            float ax = 0.f, ay = 0.f, az = 0.f, aw = 0.f;
-            if (i0 + lane < nsel) {
-                const int idx = stride == 1 ? widx : cand_index(W, bt.nne, first + (i0 + lane) * stride);
-                load_rel(c, idx, ax, ay, az, aw);
-                keep = aw <= c.thr;
-            }
-            tile_n = tile_push(W, tile_n, keep, ax, ay, az, aw);
-            if (tile_n > kWT - 32) {
-                staged += tile_n;
-                fold_all(c, W, tile_n, vals, tm, pairs);
-                tile_n = 0;
-            }
-        }
-#endif
         fbase += total;
     }
     if (tile_n > 0) {
@@ -692,7 +627,7 @@ __device__ void search_block(const Ctx& c, WarpSmem& W, int nb, float* vals, flo
         // the counting pass
         // count x min(1, R^2 / rho^2) <= 2 reps, without the division
         const double rho2 = c.G.rho * c.G.rho;
-        const bool small = FPH_COUNT_SKIP && a.subset && rho2 > 0.0 &&
+        const bool small = a.subset && rho2 > 0.0 &&
                            c.cnt * fmin(rho2, R * R) <= 2.0 * a.reps_target * rho2;
         if (pass == 0 && !small) {
             // count the region; a large one is sampled first to tighten U
@@ -705,9 +640,6 @@ __device__ void search_block(const Ctx& c, WarpSmem& W, int nb, float* vals, flo
             int tile_n = 0;
             long long fbase = 0;
             unsigned long long stg = 0;
-#if FPH_LANE_STATS
-            const unsigned act = __ballot_sync(0xffffffffu, active);
-#endif
             auto take = [&](bool keep, float ax, float ay, float az, float aw) {
                 tile_n = tile_push(W, tile_n, keep, ax, ay, az, aw);
                 if (tile_n > kWT - 32) {
@@ -762,10 +694,6 @@ __device__ void search_block(const Ctx& c, WarpSmem& W, int nb, float* vals, flo
             }
             st[pass] += stg;
             st[2] += stg * (unsigned long long)nb;
-#if FPH_LANE_STATS
-            st[3 + 2 * pass] += stg * (unsigned long long)__popc(act);
-            st[4 + 2 * pass] += stg * (unsigned long long)nb;
-#endif
             best = tm.lane_min(best);
         }
         if (pass == 0) {
@@ -838,10 +766,10 @@ __device__ double finalize_team(const Ctx& c, WarpSmem& W, float* vals, const Te
 }
 
 // ------------------------------------------------------- one simplex
-// kPh: 0 = every phase; 1 = phase A only (the rows' values go to the next
-// kernel through a.perpoint); 2 = phases B, C, F on those rows; 3 = phases
-// B, C only; 4 = phase F only; 5 = phase B only (L to a.lower); 6 = phase C
-// only.
+// kPh: 0 = every phase (one kernel, small complexes); the four-kernel chain
+// runs 1 = phase A only (the rows' values go to the next kernel through
+// a.perpoint), 5 = phase B only (L to a.lower), 6 = phase C only, 4 = phase
+// F only.
 template <int kPh>
 __device__ void run_simplex(const Ctx& c, WarpSmem& W, const Team& tm, float* vals) {
     const int lane = threadIdx.x & 31;
@@ -850,14 +778,14 @@ __device__ void run_simplex(const Ctx& c, WarpSmem& W, const Team& tm, float* va
                        blocks = 0, pruned = 0, searches = 0;
     long long clk[5];
     clk[0] = clock64();
-    // ---- A (done by pass_kernel in split mode: vals hold the sample minima)
-    int stride = c.G.stride;
-    if ((kPh == 2 || kPh == 3 || kPh == 5 || kPh == 6) && !a.split) {
+    // ---- A
+    int stride = 1;
+    if (kPh == 5 || kPh == 6) {
         const long long C = a.cand_count[c.s];
         const bool exact = (double)C * (double)a.P <= a.exact_pairs || C <= a.exact_cand[a.k];
         stride = exact ? 1 : (int)max(1ll, (C + a.reps_target - 1) / a.reps_target);
     }
-    if (!a.split && (kPh == 0 || kPh == 1)) {
+    if (kPh == 0 || kPh == 1) {
         for (int j = tm.rank * 32 + lane; j < a.P; j += tm.size * 32)
             vals[j] = tm.size == 1 ? INFINITY : __uint_as_float(f2ord(INFINITY));
         tm.sync();
@@ -878,7 +806,7 @@ __device__ void run_simplex(const Ctx& c, WarpSmem& W, const Team& tm, float* va
     clk[1] = clock64();
     clk[2] = clk[1];
     clk[3] = clk[1];
-    if ((kPh == 0 || kPh == 2 || kPh == 3 || kPh == 5 || kPh == 6) && stride > 1) {
+    if ((kPh == 0 || kPh == 5 || kPh == 6) && stride > 1) {
       float L;
       if (kPh == 6) {
         L = a.lower[c.s];  // phase B ran in the previous kernel
@@ -988,7 +916,7 @@ __device__ void run_simplex(const Ctx& c, WarpSmem& W, const Team& tm, float* va
     }
     tm.sync();
     if (stride > 1) clk[3] = clock64();
-    const bool fin = kPh == 0 || kPh == 2 || kPh == 4;  // 5: B only, 6: C only
+    const bool fin = kPh == 0 || kPh == 4;  // 5: B only, 6: C only
     const double M = fin ? finalize_team(c, W, vals, tm, refined, scanned) : 0.0;
     clk[4] = clock64();
     unsigned long long* stats = a.stats;
@@ -1049,7 +977,8 @@ __global__ void __launch_bounds__(kSThreads, FPH_SEARCH_MINB)
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     extern __shared__ __align__(16) unsigned char smem_raw[];
     SearchSmem& S = *reinterpret_cast<SearchSmem*>(smem_raw);
-    for (int i = threadIdx.x; i <= a.m; i += blockDim.x) S.wt[i] = __ddiv_rn((double)i, (double)a.m);
+    double* wt = reinterpret_cast<double*>(smem_raw + a.wt_off);
+    for (int i = threadIdx.x; i <= a.m; i += blockDim.x) wt[i] = __ddiv_rn((double)i, (double)a.m);
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     WarpSmem& W = S.w[w];
     const long long team_thr = a.team_thr_dev ? *a.team_thr_dev : (long long)a.team_threshold;
@@ -1059,9 +988,6 @@ __global__ void __launch_bounds__(kSThreads, FPH_SEARCH_MINB)
     int pending = -1, next = -1;
     bool team = true;
     for (;;) {
-#ifdef FPH_PROLOGUE_CLK
-        const long long pc0 = clock64();
-#endif
         int t;
         if (team) {
             __syncthreads();
@@ -1082,13 +1008,12 @@ __global__ void __launch_bounds__(kSThreads, FPH_SEARCH_MINB)
             // next pass, so its atomic round trip overlaps this simplex
             if (lane == 0) {
                 t = next >= 0 ? next : atomicAdd(counter, 1);
-                next = FPH_PREFETCH_CLAIM ? atomicAdd(counter, 1) : -1;
+                next = -1;
             }
             t = __shfl_sync(0xffffffffu, t, 0);
         }
         if (t >= a.n) return;
         const int s = order[t];
-        if (a.split && geom[s].stride == 1) continue;  // finished by the pass kernel
         // Simplices valued by one exact pass in phase A have no B or C: those
         // kernels skip them outright and F waits for A's flag instead.
         int need = pos;
@@ -1119,7 +1044,7 @@ __global__ void __launch_bounds__(kSThreads, FPH_SEARCH_MINB)
             if (team) __syncthreads();
         }
         __syncwarp();
-        const Ctx c{&a, W.G, W.V, S.wt,
+        const Ctx c{&a, W.G, W.V, wt,
                     a.subset ? (float)(W.G.rho * W.G.rho * (1.0 + 1e-5)) : INFINITY, s,
                     (double)a.cand_count[s]};
         const Team tm = team ? Team{w, kSW, &S.team} : Team{0, 1, nullptr};
@@ -1127,15 +1052,12 @@ __global__ void __launch_bounds__(kSThreads, FPH_SEARCH_MINB)
         if (kSV) {
             float* sv = reinterpret_cast<float*>(smem_raw + sizeof(SearchSmem)) +
                         (team ? 0 : w) * kValsCap;
-            if (a.split || kPh >= 2) {  // an earlier kernel left the rows' values
+            if (kPh >= 2) {  // an earlier kernel left the rows' values
                 for (int j = tm.rank * 32 + lane; j < a.P; j += tm.size * 32) sv[j] = vals[j];
                 tm.sync();
             }
-#ifdef FPH_PROLOGUE_CLK
-            if (lane == 0) atomicAdd(&a.stats[2], (unsigned long long)(clock64() - pc0));
-#endif
             run_simplex<kPh>(c, W, tm, sv);
-            if (kPh == 1 || kPh == 3 || kPh == 5 || kPh == 6) {  // hand the rows on
+            if (kPh == 1 || kPh == 5 || kPh == 6) {  // hand the rows on
                 for (int j = tm.rank * 32 + lane; j < a.P; j += tm.size * 32) vals[j] = sv[j];
                 tm.sync();
             }
@@ -1170,6 +1092,18 @@ __global__ void iota_kernel(int* out, int n) {
 
 }  // namespace
 
+size_t search_smem_bytes(int P, int m) {
+    return (P <= kValsCap ? kSmemVals : sizeof(SearchSmem)) + sizeof(double) * (size_t)(m + 1);
+}
+
+size_t search_smem_limit() {
+    int dev = 0, lim = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&lim, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess)
+        return 0;
+    return (size_t)lim;
+}
+
 int launch_search(const FloodArgs& a, const SimplexGeom* d_geom, const int* d_cand,
                   cudaStream_t stream) {
     // order simplices by candidate count, largest first: the longest
@@ -1196,34 +1130,26 @@ int launch_search(const FloodArgs& a, const SimplexGeom* d_geom, const int* d_ca
     FPH_CUDA_TRY(cudaGetDevice(&dev));
     FPH_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     const bool sv = a.P <= kValsCap;
-    const int smem = (int)(sv ? kSmemVals : sizeof(SearchSmem));
-    // FPH_TWO_KERNELS: phase A in one kernel, phases B, C, F in another, each
-    // with its own register allocation (-7% on configs[1]); FPH_THREE_KERNELS
-    // also separates F from B, C (phase C -16%), FPH_FOUR_KERNELS B from C
-    // (phase C another -16%); FPH_PDL chains them per simplex so tails
-    // overlap.  Small complexes keep one kernel, where the extra launches and
-    // tails do not amortise.
+    const int smem = (int)search_smem_bytes(a.P, a.m);
+    // Complexes of >= 10 000 simplices run the phases as four kernels, A | B |
+    // C | F, each with its own register allocation (phase C alone lost a third
+    // of its cycles that way), chained per simplex by programmatic dependent
+    // launch so each kernel's tail overlaps the next one.  Small complexes
+    // keep one kernel, where the extra launches and tails do not amortise.
     // FPH_SPLIT_MIN_SIMPLICES (environment) overrides the 10 000 cut-off;
     // the tests set it to 0 to run the small golden complexes through the chain
     long long split_min = 10000;
     if (const char* e = getenv("FPH_SPLIT_MIN_SIMPLICES")) split_min = atoll(e);
-    const bool two = FPH_TWO_KERNELS && !a.split && a.n >= split_min;
+    const bool chain = a.n >= split_min;
     using K = void (*)(const FloodArgs, const SimplexGeom*, const int*, int*, int*, int);
     K kern[4] = {nullptr, nullptr, nullptr, nullptr};
     float* d_lower = nullptr;
-    if (two && FPH_FOUR_KERNELS) {
+    if (chain) {
         kern[0] = sv ? search_kernel<true, 1> : search_kernel<false, 1>;
         kern[1] = sv ? search_kernel<true, 5> : search_kernel<false, 5>;
         kern[2] = sv ? search_kernel<true, 6> : search_kernel<false, 6>;
         kern[3] = sv ? search_kernel<true, 4> : search_kernel<false, 4>;
         FPH_CUDA_TRY(cudaMallocAsync(&d_lower, sizeof(float) * a.n, stream));
-    } else if (two && FPH_THREE_KERNELS) {
-        kern[0] = sv ? search_kernel<true, 1> : search_kernel<false, 1>;
-        kern[1] = sv ? search_kernel<true, 3> : search_kernel<false, 3>;
-        kern[2] = sv ? search_kernel<true, 4> : search_kernel<false, 4>;
-    } else if (two) {
-        kern[0] = sv ? search_kernel<true, 1> : search_kernel<false, 1>;
-        kern[1] = sv ? search_kernel<true, 2> : search_kernel<false, 2>;
     } else {
         kern[0] = sv ? search_kernel<true, 0> : search_kernel<false, 0>;
     }
@@ -1233,6 +1159,7 @@ int launch_search(const FloodArgs& a, const SimplexGeom* d_geom, const int* d_ca
     blocks = blocks < (a.n + kSW - 1) / kSW ? blocks : (a.n + kSW - 1) / kSW;
     FloodArgs b = a;
     b.lower = d_lower;
+    b.wt_off = (int)(sv ? kSmemVals : sizeof(SearchSmem));
     long long* d_thr = nullptr;
     void* tmp2 = nullptr;
     if (a.team_threshold <= 0) {
@@ -1253,7 +1180,7 @@ int launch_search(const FloodArgs& a, const SimplexGeom* d_geom, const int* d_ca
     int* d_counters = nullptr;
     FPH_CUDA_TRY(cudaMallocAsync(&d_counters, sizeof(int) * 4, stream));
     FPH_CUDA_TRY(cudaMemsetAsync(d_counters, 0, sizeof(int) * 4, stream));
-    if (nk > 1 && FPH_PDL) {
+    if (nk > 1) {
         FPH_CUDA_TRY(cudaMallocAsync(&d_stage, sizeof(int) * a.n, stream));
         FPH_CUDA_TRY(cudaMemsetAsync(d_stage, 0, sizeof(int) * a.n, stream));
     }

@@ -12,15 +12,19 @@ fallback.  Values are bit-identical to the reference's float64 values.
 
 from __future__ import annotations
 
+import math
 import time
 from dataclasses import dataclass, field
+from itertools import combinations
 
 import numpy as np
 
 from . import _native
 from .delaunay import Triangulation, delaunay
 from .errors import IntegrityError
-from .geometry import PointCloud, as_points, farthest_point_sampling
+from .geometry import (PointCloud, as_points, farthest_point_sampling, grid_covering_bound,
+                       ritter_enclosing_ball)
+from .spatial import AxisSortedCloud, slab_indices
 
 STAGE_LANDMARKS = "Landmark select."
 STAGE_DELAUNAY = "Delaunay triang."
@@ -57,8 +61,6 @@ class FloodConfig:
     def validate(self) -> None:
         if self.grid_resolution < 1:
             raise ValueError("grid_resolution must be >= 1")
-        if self.grid_resolution > 255:
-            raise ValueError("grid_resolution must be <= 255")
         if self.batch_size < 1:
             raise ValueError("batch_size must be >= 1")
         if self.sampler not in SAMPLERS:
@@ -71,6 +73,16 @@ class FloodConfig:
             raise ValueError("threads must be >= 1")
         if self.max_dim is not None and not 0 <= self.max_dim <= 3:
             raise ValueError("max_dim must be in [0, 3]")
+
+
+@dataclass(frozen=True)
+class CandidateMask:
+    """Per simplex of a batch: the ascending cloud indices inside its masking
+    ball (|x - c|^2 <= 2 r^2, (c, r) its Ritter ball).  Reference
+    floodph/filtration.py:88."""
+
+    simplices: np.ndarray
+    candidates: list
 
 
 @dataclass(frozen=True)
@@ -93,6 +105,117 @@ class FilteredComplex:
 
     def value_map(self) -> dict:
         return {verts: value for verts, _, value in self.simplices}
+
+
+def compute_mask(triangulation: Triangulation, X, sorted_cloud: AxisSortedCloud,
+                 batch) -> CandidateMask:
+    """Candidate cloud indices of each simplex of `batch` (rows of landmark ids
+    into triangulation.points), from the device grid (fph_candidate_mask).
+
+    Same result as reference floodph/filtration.py:130: every cloud point of
+    the closed ball |x - c|^2 <= 2 r r, ascending.  An empty ball (possible
+    only for landmarks away from the cloud) falls back, as in the reference,
+    to the batch's axis slab (bounds: extreme center -+ sqrt(2) r (1 + 1e-12)
+    along sorted_cloud.axis), then to the whole cloud.
+    """
+    pts = np.ascontiguousarray(as_points(X), dtype=np.float64)
+    cells = np.asarray(batch, dtype=np.int64)
+    if cells.ndim == 1:
+        cells = cells.reshape(1, -1)
+    if cells.shape[0] == 0:
+        return CandidateMask(cells, [])
+    if cells.shape[1] < 2:
+        raise ValueError("enclosing ball needs at least 2 vertices")
+    if cells.shape[1] > 4:
+        raise ValueError("simplices of dimension above 3 are not supported")
+    lib = _native.require_gpu()
+    lms = np.ascontiguousarray(triangulation.points, dtype=np.float64)
+    c32 = np.ascontiguousarray(cells, dtype=np.int32)
+    k = cells.shape[1] - 1
+    offs = np.zeros(cells.shape[0] + 1, dtype=np.int64)
+    args = (_native.ptr(pts), pts.shape[0], pts.shape[1], _native.ptr(lms), lms.shape[0],
+            _native.ptr(c32), cells.shape[0], k, _native.ptr(offs))
+    _native.check(lib.fph_candidate_mask(*args, None, 0))
+    idx = np.empty(max(int(offs[-1]), 1), dtype=np.int32)
+    _native.check(lib.fph_candidate_mask(*args, _native.ptr(idx), idx.shape[0]))
+    idx = idx.astype(np.int64)
+    candidates = [idx[offs[i]:offs[i + 1]] for i in range(cells.shape[0])]
+    if any(c.size == 0 for c in candidates):
+        balls = [ritter_enclosing_ball(lms[c]) for c in cells]
+        axis = sorted_cloud.axis
+        spans = [math.sqrt(2.0) * b.radius * (1.0 + 1e-12) for b in balls]
+        lo = min(b.center[axis] - sp for b, sp in zip(balls, spans))
+        hi = max(b.center[axis] + sp for b, sp in zip(balls, spans))
+        slab = np.sort(slab_indices(sorted_cloud, lo, hi))
+        fallback = slab if slab.size else np.arange(pts.shape[0], dtype=np.int64)
+        candidates = [c if c.size else fallback for c in candidates]
+    return CandidateMask(cells, candidates)
+
+
+def _max_min_sq(grid_points: np.ndarray, cloud: np.ndarray) -> float:
+    """max over grid rows of the min squared distance to the cloud (GPU:
+    the rows as explicit samples of one 0-simplex at their centroid, the
+    whole cloud searched)."""
+    lib = _native.require_gpu()
+    g = np.ascontiguousarray(grid_points, dtype=np.float64)
+    c = np.ascontiguousarray(cloud, dtype=np.float64)
+    center = np.ascontiguousarray(g.mean(axis=0, keepdims=True))
+    s4 = np.array([[0, -1, -1, -1]], dtype=np.int32)
+    out = np.empty(1)
+    _native.check(lib.fph_flood_samples(
+        _native.ptr(c), c.shape[0], c.shape[1], _native.ptr(center), 1, _native.ptr(s4), 1, 0,
+        _native.ptr(g), g.shape[0], 0, _native.ptr(out), _native.FPH_MEM_HOST, None))
+    return float(out[0])
+
+
+def simplex_filtration(simplex, grid_points: np.ndarray, candidates, X) -> float:
+    """max over the grid points of the min distance to X[candidates] (GPU).
+    Reference floodph/filtration.py:165; candidates must be non-empty."""
+    cand = np.asarray(candidates, dtype=np.int64)
+    if cand.size == 0:
+        raise IntegrityError(f"empty candidate set for simplex {tuple(simplex)}")
+    grid = as_points(grid_points)
+    if grid.shape[0] == 0:
+        raise ValueError("empty grid")
+    return math.sqrt(_max_min_sq(grid, as_points(X)[cand]))
+
+
+def _simplex_closure(k: int):
+    """All faces of the standard k-simplex {0..k}, by dimension, with their
+    facet links (the Triangulation layout)."""
+    by_dim = {j: np.array(list(combinations(range(k + 1), j + 1)), dtype=np.int64)
+              for j in range(k + 1)}
+    links = {}
+    for j in range(1, k + 1):
+        lower = {tuple(r): i for i, r in enumerate(by_dim[j - 1].tolist())}
+        links[j] = np.array([[lower[tuple(r[:t] + r[t + 1:])] for t in range(j + 1)]
+                             for r in by_dim[j].tolist()], dtype=np.int64)
+    return by_dim, links
+
+
+def flood_value_exact_gap(simplex, m: int, X) -> tuple:
+    """(value of the resolution-m grid of the simplex, that + the grid's
+    covering bound): brackets the continuous flood value.  Reference
+    floodph/filtration.py:178.  The grid value is the flood filtration of the
+    simplex's own closure on the GPU (every row of the full grid: interior
+    rows of each face, then facet completion), over the whole cloud."""
+    verts = np.ascontiguousarray(as_points(simplex), dtype=np.float64)
+    pts = np.ascontiguousarray(as_points(X), dtype=np.float64)
+    if m < 1:
+        raise ValueError("resolution must be at least 1")
+    k = verts.shape[0] - 1
+    if k < 0 or k > 3:
+        raise ValueError("simplices of dimension 0..3 are supported")
+    if verts.shape[1] != pts.shape[1]:
+        raise ValueError("simplex and cloud dimensions differ")
+    by_dim, links = _simplex_closure(k)
+    tri = Triangulation(dim=k, points=verts, vertices=np.arange(k + 1), simplices_by_dim=by_dim,
+                        facet_links=links, dedup_dropped=np.zeros(0, np.int64),
+                        jitter_applied=False, warnings=())
+    subset = _landmarks_in_cloud(verts, pts)
+    sq = flood_sq_values(pts, tri, int(m), subset)
+    f = math.sqrt(float(sq[k][0]))
+    return f, f + grid_covering_bound(verts, m)
 
 
 def _landmarks_in_cloud(landmarks: np.ndarray, pts: np.ndarray) -> bool:

@@ -7,7 +7,7 @@ import numpy as np
 import pytest
 
 import oracle
-from paper_2509_22432_b200 import farthest_point_sampling
+from paper_2509_22432_b200 import farthest_point_sampling, farthest_point_sampling_batched
 from paper_2509_22432_b200.datagen import gen_sphere_torus_mix, gen_torus
 from paper_2509_22432_b200.delaunay import delaunay
 from paper_2509_22432_b200.filtration import FloodConfig, build_flood_filtration, flood_sq_values
@@ -56,15 +56,33 @@ def test_fps_batched_matches_oracle(batch, n, k):
         np.testing.assert_array_equal(got[b], oracle.fps(clouds[b], k, 3))
 
 
-@pytest.mark.parametrize("pt", [3, 4, 5, 6, 7, 8, 9])
+_RES_NT = 512  # threads per CTA of the resident / batched FPS kernels (csrc/fph_fps.cu kResNT)
+
+
+@pytest.mark.parametrize("pt", list(range(1, 19)))
 def test_fps_resident_points_per_thread(pt):
-    """Slices of 3..9 x 1024 points per CTA (PT = 6..18 points per thread at
-    the default 512 threads, padded), on coordinates quantised to 1/8 so ties
-    are common, and a ragged last slice."""
-    n = 148 * (pt * 1024 - 300) + 77
+    """Every PT instantiation of the resident kernel (slices of PT x 512
+    points per CTA, padded): n chosen from the device's SM count so the
+    slice needs exactly PT points per thread, with a ragged last slice;
+    coordinates quantised to 1/8 so ties are common."""
+    import torch
+
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    n = sms * (pt * _RES_NT - 100) + 37
     pts = np.round(np.random.default_rng(pt).random((n, 3)) * 64) / 8
     got = farthest_point_sampling(pts, 120, pt)
     np.testing.assert_array_equal(got, oracle.fps(pts, 120, pt))
+
+
+@pytest.mark.parametrize("pt", list(range(1, 19)))
+def test_fps_batched_points_per_thread(pt):
+    """Every PT instantiation of the batched kernel (one CTA per cloud up to
+    9216 points): clouds of PT x 512 - 100 points, quantised coordinates."""
+    n = pt * _RES_NT - 100
+    clouds = np.round(np.random.default_rng(100 + pt).random((5, n, 3)) * 64) / 8
+    got = farthest_point_sampling_batched(clouds, 50, 1)
+    for b in range(5):
+        np.testing.assert_array_equal(got[b], oracle.fps(clouds[b], 50, 1))
 
 
 def test_fps_ties_uniform_grid():
@@ -185,8 +203,7 @@ def test_block_search_equals_brute_force_full_size(algo_switch, reps, team):
         assert np.array_equal(brute[k], search[k]), k
 
 
-@pytest.mark.parametrize("algo,reps,team", [(0, 0, 0), (1, 0, 0), (1, 16, 1), (1, 16, 2**30),
-                                            (2, 0, 0), (2, 16, 1)])
+@pytest.mark.parametrize("algo,reps,team", [(0, 0, 0), (1, 0, 0), (1, 16, 1), (1, 16, 2**30)])
 @pytest.mark.parametrize("name", ["torus10k_m20", "rand3d_m30", "external2d", "circle_m64",
                                   "dup3d_m5"])
 def test_both_algorithms_golden(algo_switch, algo, reps, team, name):
@@ -328,17 +345,30 @@ def test_duplicate_points_and_landmarks():
         assert np.array_equal(got, np.sqrt(want[k]))
 
 
-def test_max_resolution_and_bad_arguments():
+@pytest.mark.parametrize("m", [255, 256, 257, 700])
+def test_high_resolutions_match_oracle(algo_switch, m):
+    """Resolutions past one byte (template rows are ushort4; the weight
+    table grows with m) under both algorithms."""
     z = G.load("flood", "rand2d_m6")
     tri = C.triangulation(z["tri_points"], G.simplices_by_dim(z))
-    sq = flood_sq_values(z["points"], tri, 255, True)
-    want = oracle.flood_values(z["points"], tri.points, tri.simplices_by_dim, 255)
-    for k in range(3):
-        assert np.array_equal(sq[k], want[k])
-    with pytest.raises(ValueError):
-        flood_sq_values(z["points"], tri, 256, True)
-    with pytest.raises(ValueError):
-        flood_sq_values(z["points"], tri, 0, True)
+    want = oracle.flood_values(z["points"], tri.points, tri.simplices_by_dim, m)
+    for algo in (0, 1):
+        algo_switch(algo)
+        sq = flood_sq_values(z["points"], tri, m, True)
+        for k in range(3):
+            assert np.array_equal(sq[k], want[k]), (algo, k)
+
+
+def test_bad_resolutions():
+    z = G.load("flood", "rand2d_m6")
+    tri = C.triangulation(z["tri_points"], G.simplices_by_dim(z))
+    for m in (0, -3, 65536):
+        with pytest.raises(ValueError):
+            flood_sq_values(z["points"], tri, m, True)
+    with pytest.raises(ValueError):  # C(m - 1, 3) interior rows per tetrahedron >= 2^24
+        z3 = G.load("flood", "rand3d_m4")
+        flood_sq_values(z3["points"], C.triangulation(z3["tri_points"], G.simplices_by_dim(z3)),
+                        2000, True)
 
 
 # ------------------------------------------------- pipeline acceptance

@@ -90,7 +90,55 @@ def test_reduction_hand_example():
 
 def test_config_validation():
     for bad in (dict(grid_resolution=0), dict(batch_size=0), dict(sampler="sobol"),
-                dict(backend="gpu"), dict(threads=0), dict(max_dim=4), dict(grid_resolution=256)):
+                dict(backend="gpu"), dict(threads=0), dict(max_dim=4)):
         with pytest.raises(ValueError):
             FloodConfig(**bad).validate()
+    FloodConfig(grid_resolution=512).validate()  # any m >= 1, as the reference
     FloodConfig(backend="kdtree").validate()
+
+
+@pytest.mark.parametrize("name", G.cases("diagram"))
+@pytest.mark.parametrize("clearing", [True, False])
+def test_diagram_equals_reference_diagram(name, clearing):
+    """The reference's own persistence diagram of its own values
+    (tests/golden/diagram_*.npz from floodph.persistence): bars identical, so
+    the bottleneck distance is 0 (the tolerance stated for diagrams is 0:
+    values are bit-identical and the reduction is exact)."""
+    fc = _flood_complex(name)
+    dgm = reduce_and_extract(boundary_matrix(fc), fc, clearing=clearing)
+    z = G.load("diagram", name)
+    assert sorted(dgm.dimensions()) == sorted(int(d) for d in z["dims"])
+    for d in z["dims"]:
+        want = [tuple(b) for b in z[f"bars_{int(d)}"].tolist()]
+        assert dgm.in_dim(int(d)) == want, int(d)
+
+
+@pytest.mark.parametrize("name", ["rand3d_m4", "torus10k_m20"])
+def test_lazy_columns_equal_reference_columns(name):
+    """The flood-complex boundary matrix's lazily built columns equal the
+    reference layout (sorted facet ranks, all below the column's rank)."""
+    fc = _flood_complex(name)
+    bm = boundary_matrix(fc)
+    ranked = fc.in_order()
+    rank_of = {v: j for j, (v, _, _) in enumerate(ranked)}
+    from itertools import combinations
+
+    for j, (verts, d, _) in enumerate(ranked):
+        want = sorted(rank_of[f] for f in combinations(verts, d)) if d else []
+        assert bm.columns[j] == want
+        assert bm.dims[j] == d
+    assert len(bm) == len(fc)
+
+
+def test_face_order_violation_detected():
+    fc = _flood_complex("rand2d_m6")
+    order = fc.order.copy()
+    # put an edge before one of its vertices
+    e = next(i for i, s in enumerate(fc.simplices) if s[1] == 1)
+    v = fc.simplices.index(next(s for s in fc.simplices if s[0] == (fc.simplices[e][0][0],)))
+    order[e], order[v] = order[v], order[e]
+    bad = FilteredComplex(fc.simplices, order, meta=fc.meta)
+    from paper_2509_22432_b200.errors import IntegrityError
+
+    with pytest.raises(IntegrityError):
+        boundary_matrix(bad)
