@@ -83,7 +83,11 @@ def load(path: str | None = None):
             "or __graft_entry__.build()")
     lib = ctypes.CDLL(path)
     for name, (res, args) in SIGNATURES.items():
-        fn = getattr(lib, name)
+        fn = getattr(lib, name, None)
+        if fn is None:  # an older build loaded through FPH_LIB for an A/B run
+            if path == LIB_PATH:
+                raise RuntimeError(f"{path} does not export {name}")
+            continue
         fn.restype = res
         fn.argtypes = args
     if lib.fph_abi_version() != 1:

@@ -12,8 +12,6 @@
 
 #include <cmath>
 #include <cstdio>
-#include <cstdlib>
-#include <cstring>
 
 #include "fph_grid.cuh"
 
@@ -127,33 +125,17 @@ int grid_build(const double* d_pts, int n, int dim, double cell_size, double occ
         return FPH_EARG;
     }
     unsigned long long hb[6];
-    // EXPERIMENT (A/B of the host round trip): FPH_EXP_BBOX_REUSE=1 reuses
-    // the previous call's box for the same buffer (not valid in general)
-    static const bool reuse = getenv("FPH_EXP_BBOX_REUSE") != nullptr;
-    static const double* last_pts = nullptr;
-    static int last_n = -1;
-    static unsigned long long last_hb[6];
-    if (reuse && d_pts == last_pts && n == last_n) {
-        memcpy(hb, last_hb, sizeof(hb));
-    } else {
     unsigned long long* d_bbox = nullptr;
     FPH_CUDA_TRY(cudaMallocAsync(&d_bbox, 6 * sizeof(unsigned long long), stream));
-    unsigned long long init[6];
-    for (int a = 0; a < 3; ++a) {
-        init[a] = ~0ull;
-        init[3 + a] = 0ull;
-    }
-    FPH_CUDA_TRY(cudaMemcpyAsync(d_bbox, init, sizeof(init), cudaMemcpyHostToDevice, stream));
+    // ordered-int identities: mins start at ~0, maxes at 0 (no host copy)
+    FPH_CUDA_TRY(cudaMemsetAsync(d_bbox, 0xff, 3 * sizeof(unsigned long long), stream));
+    FPH_CUDA_TRY(cudaMemsetAsync(d_bbox + 3, 0, 3 * sizeof(unsigned long long), stream));
     int blocks = (n + 255) / 256;
     if (blocks > 592) blocks = 592;
     bbox_kernel<<<blocks, 256, 0, stream>>>(d_pts, n, dim, d_bbox);
     FPH_CUDA_TRY(cudaMemcpyAsync(hb, d_bbox, sizeof(hb), cudaMemcpyDeviceToHost, stream));
     FPH_CUDA_TRY(cudaStreamSynchronize(stream));
     FPH_CUDA_TRY(cudaFreeAsync(d_bbox, stream));
-    last_pts = d_pts;
-    last_n = n;
-    memcpy(last_hb, hb, sizeof(hb));
-    }
     double lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
     for (int a = 0; a < dim; ++a) {
         lo[a] = ord2d(hb[a]);
