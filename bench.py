@@ -6,13 +6,17 @@ kernel for every simplex of dim <= max_dim, facet completion.  The default
 workload is BASELINE configs[1]: 1M points, noisy sphere+torus mix, 2000
 FPS landmarks, simplices of dim <= 2 of their 3-D Delaunay complex, grid
 resolution m = 20 (the reference default).  Farthest point sampling and the
-host Delaunay are timed as separate stages (fps_ms, delaunay_s).
+host Delaunay are timed as separate stages (fps_ms, delaunay_s); fps_ms has
+the CPU oracle's time beside it (fps_cpu_baseline).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--config sphere_torus_1m|dense30_1m|box_10m|torus_10k|modelnet_batch]
 
-N > 1 (torchrun): every rank builds the grid, values an interleaved shard of
-the simplices, and the shards are all-gathered over NCCL (weak scaling is
-not meaningful here: the complex is fixed, so "scaling" is "strong").
+Single-cloud configs at N > 1 (torchrun): every rank builds the grid, values
+an interleaved shard of the simplices, and the shards are all-gathered over
+NCCL ("scaling": "strong", the complex is fixed).  modelnet_batch (configs[3])
+gives every rank its own 64 clouds ("scaling": "weak"; 512 clouds at N = 8):
+the step values all of them, no collective.
 --impl reference times the CPU oracle (oracle/, a C restatement of the
 reference algorithm, all host threads) on a bounded sample of the same
 complex; rank 0 only.
@@ -27,6 +31,7 @@ import subprocess
 import sys
 import threading
 import time
+from concurrent.futures import ThreadPoolExecutor
 
 import numpy as np
 
@@ -39,17 +44,21 @@ CONFIGS = {
     "dense30_1m": ("sphere_torus", 1_000_000, 2000, 30, 2),
     "box_10m": ("box", 10_000_000, 5000, 20, 3),
     "torus_10k": ("torus", 10_000, 500, 20, 2),
+    "modelnet_batch": ("modelnet", 100_000, 1000, 20, 3),
 }
+BATCH_PER_RANK = 64  # modelnet_batch: clouds per GPU (512 over 8 GPUs)
 
 
-def _cloud(kind: str, n: int):
+def _cloud(kind: str, n: int, seed: int = 0):
     from paper_2509_22432_b200 import datagen
 
     if kind == "sphere_torus":
-        return datagen.gen_sphere_torus_mix(n, seed=0).points
+        return datagen.gen_sphere_torus_mix(n, seed=seed).points
     if kind == "box":
-        return datagen.gen_uniform_box(n, seed=0).points
-    return datagen.gen_torus(n, seed=0).points
+        return datagen.gen_uniform_box(n, seed=seed).points
+    if kind == "modelnet":
+        return datagen.gen_modelnet_like(n, seed=seed).points
+    return datagen.gen_torus(n, seed=seed).points
 
 
 class ClockSampler:
@@ -112,77 +121,73 @@ def _dist():
     return world, rank, local
 
 
-def prepare(cfg_name: str, device: int):
-    """Untimed setup: cloud, GPU FPS (timed as its own stage), host Delaunay."""
+def prepare(cfg_name: str, device: int, rank: int = 0):
+    """Untimed setup: clouds, GPU FPS (timed as its own stage), host Delaunay,
+    device complexes.  Batch configs hold this rank's BATCH_PER_RANK clouds."""
     import torch
 
-    from paper_2509_22432_b200 import farthest_point_sampling
+    from paper_2509_22432_b200 import farthest_point_sampling, farthest_point_sampling_batched
+    from paper_2509_22432_b200.batch import DeviceComplex
     from paper_2509_22432_b200.delaunay import delaunay
 
     kind, n, nl, m, max_dim = CONFIGS[cfg_name]
-    X = _cloud(kind, n)
-    Xd = torch.from_numpy(X).to(f"cuda:{device}")
-    farthest_point_sampling(Xd, 16, 0)  # warm the FPS kernel
+    batch = kind == "modelnet"
+    dev = torch.device(f"cuda:{device}")
+    if batch:
+        seeds = [rank * BATCH_PER_RANK + i for i in range(BATCH_PER_RANK)]
+        Xs = [_cloud(kind, n, s) for s in seeds]
+        Xd = torch.from_numpy(np.stack(Xs)).to(dev)
+        fps = lambda: farthest_point_sampling_batched(Xd, nl, 0)  # noqa: E731
+    else:
+        Xs = [_cloud(kind, n)]
+        Xd = torch.from_numpy(Xs[0]).to(dev)
+        fps = lambda: farthest_point_sampling(Xd, nl, 0).reshape(1, -1)  # noqa: E731
+    fps()  # warm the FPS kernel
     torch.cuda.synchronize()
     fps_ms = []
     for _ in range(2):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        idx = farthest_point_sampling(Xd, nl, 0)
+        idx = fps()
         e1.record()
         torch.cuda.synchronize()
         fps_ms.append(e0.elapsed_time(e1))
     idx = idx.cpu().numpy()
     t0 = time.perf_counter()
-    tri = delaunay(X[idx])
+    with ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as pool:
+        tris = list(pool.map(lambda i: delaunay(Xs[i][idx[i]]), range(len(Xs))))
     delaunay_s = time.perf_counter() - t0
-    return dict(X=X, Xd=Xd, idx=idx, tri=tri, m=m, max_dim=min(max_dim, tri.dim), n=n, nl=nl,
-                fps_ms=min(fps_ms), delaunay_s=delaunay_s, kind=kind)
+    items = []
+    for i, tri in enumerate(tris):
+        dc = DeviceComplex(tri, dev, max_dim)
+        items.append((Xd[i] if batch else Xd, dc))
+    top = min(max_dim, tris[0].dim)
+    return dict(X=Xs[0], Xs=Xs, Xd=Xd, idx=idx[0], idxs=idx, tri=tris[0], tris=tris, m=m,
+                max_dim=top, n=n, nl=nl, fps_ms=min(fps_ms), delaunay_s=delaunay_s, kind=kind,
+                items=items, batch=batch, dev=dev)
 
 
-class DeviceComplex:
-    """Device buffers of one (shard of a) complex for the C-ABI calls."""
+def step_single(lib, native, w, stream):
+    """One cloud (or each cloud of a batch) in one fph_flood_filtration call."""
+    from paper_2509_22432_b200.batch import flood_sq_device
 
-    def __init__(self, w, device, world=1, rank=0):
-        import torch
-
-        tri = w["tri"]
-        self.top = w["max_dim"]
-        self.dev = torch.device(f"cuda:{device}")
-        self.lm = torch.from_numpy(np.ascontiguousarray(tri.points)).to(self.dev)
-        self.counts_full = [int(tri.simplices_by_dim[k].shape[0]) for k in range(self.top + 1)]
-        self.facets = {}
-        for k in range(1, self.top + 1):
-            self.facets[k] = torch.from_numpy(
-                np.ascontiguousarray(tri.facet_links[k], dtype=np.int32)).to(self.dev)
-        self.full_simp = {k: torch.from_numpy(np.ascontiguousarray(tri.simplices_by_dim[k], dtype=np.int32)).to(self.dev)
-                          for k in range(1, self.top + 1)}
-        self.counts = torch.tensor(self.counts_full, dtype=torch.int64)
-        self.vert_ids = torch.arange(self.counts_full[0], dtype=torch.int32, device=self.dev)
-        self.out = [torch.empty(max(c, 1), dtype=torch.float64, device=self.dev) for c in self.counts_full]
-        self.world, self.rank = world, rank
+    for Xd, dc in w["items"]:
+        flood_sq_device(Xd, dc, w["m"], True, stream)
 
 
-def step_single(lib, native, w, dc, stream):
-    """N = 1: the whole complex in one fph_flood_filtration call."""
-    simp = [None] + [dc.full_simp[k] for k in range(1, dc.top + 1)]
-    fac = [None] + [dc.facets[k] for k in range(1, dc.top + 1)]
-    native.check(lib.fph_flood_filtration(
-        w["Xd"].data_ptr(), w["n"], w["X"].shape[1], dc.lm.data_ptr(), dc.lm.shape[0], dc.top,
-        dc.counts.data_ptr(), native.ptr_array(simp, None), native.ptr_array(fac, None),
-        w["m"], 1, native.ptr_array(dc.out, None), native.FPH_MEM_DEVICE, stream))
-
-
-def step_sharded(lib, native, w, dc, stream):
+def step_sharded(lib, native, w, stream):
     """N > 1: this rank's interleaved share of every dimension in one
     fph_flood_shard call (grid built once), NCCL all-gather back into row
     order, then facet completion on every rank."""
+    import torch
     import torch.distributed as dist
 
     from paper_2509_22432_b200.parallel import flood_sq_values_sharded
 
-    by_dim = {0: dc.vert_ids, **dc.full_simp}
-    vals = flood_sq_values_sharded(w["Xd"], dc.lm, by_dim, dc.facets, dc.top, w["m"], dist)
+    Xd, dc = w["items"][0]
+    vert_ids = torch.arange(dc.counts_full[0], dtype=torch.int32, device=dc.dev)
+    by_dim = {0: vert_ids, **dc.simp}
+    vals = flood_sq_values_sharded(Xd, dc.lm, by_dim, dc.facets, dc.top, w["m"], dist)
     for k in range(dc.top + 1):
         dc.out[k][: vals[k].shape[0]] = vals[k]
 
@@ -199,13 +204,13 @@ def run_ours(args):
 
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
     lib = _native.require_gpu()
-    w = prepare(args.config, local)
-    dc = DeviceComplex(w, local, world, rank)
+    w = prepare(args.config, local, rank)
     stream = torch.cuda.current_stream().cuda_stream
-    step = step_single if world == 1 and not args.force_sharded else step_sharded
-    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dc.dev)  # > 126 MB L2
+    sharded = (world > 1 or args.force_sharded) and not w["batch"]
+    step = step_sharded if sharded else step_single
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=w["dev"])  # > 126 MB L2
     for _ in range(args.warmup):
-        step(lib, _native, w, dc, stream)
+        step(lib, _native, w, stream)
     torch.cuda.synchronize()
     if world > 1:
         torch.distributed.barrier()
@@ -220,31 +225,44 @@ def run_ours(args):
         for i in range(args.steps):
             flush.zero_()
             starts[i].record()
-            step(lib, _native, w, dc, stream)
+            step(lib, _native, w, stream)
             ends[i].record()
         torch.cuda.synchronize()
     launches = int(lib.fph_launch_count(0))
     lib.fph_flood_stats(stats.ctypes.data, 1)
     lib.fph_set_profiling(0)
     sharded_ok = None
-    if step is step_sharded:  # the gathered values must equal a single-call pass
+    if sharded:  # the gathered values must equal a single-call pass
+        dc = w["items"][0][1]
         got = [t.clone() for t in dc.out]
-        step_single(lib, _native, w, dc, stream)
+        step_single(lib, _native, w, stream)
         torch.cuda.synchronize()
         sharded_ok = all(torch.equal(a[: c], b[: c]) for a, b, c in zip(got, dc.out, dc.counts_full))
     ms = sum(s.elapsed_time(e) for s, e in zip(starts, ends)) / args.steps
+    n_simplices = sum(dc.n_simplices for _, dc in w["items"])
+    if not sharded and world > 1:  # weak scaling: every rank its own clouds
+        t = torch.tensor([float(n_simplices)], dtype=torch.float64, device=w["dev"])
+        torch.distributed.all_reduce(t)
+        n_simplices = int(t.item())
     if world > 1:
-        import torch.distributed as dist
-
-        t = torch.tensor([ms], device=dc.dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t = torch.tensor([ms], device=w["dev"])
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         ms = float(t.item())
-    n_simplices = sum(dc.counts_full)
     value = n_simplices / (ms / 1e3)
 
     result = None
     if rank == 0:
         e2e = e2e_host(lib, _native, w, args) if world == 1 else None
+        dc0 = w["items"][0][1]
+        config = {"workload": args.config, "points": w["n"], "landmarks": w["nl"],
+                  "grid_resolution": w["m"], "max_dim": w["max_dim"], "simplices": n_simplices,
+                  "l2": "flushed (256 MB write) between timed steps"}
+        if w["batch"]:
+            config.update({"clouds_per_gpu": len(w["items"]), "clouds": len(w["items"]) * world,
+                           "parallelism": f"whole clouds per GPU x{world}, no collective"})
+        else:
+            config.update({"counts": dc0.counts_full,
+                           "parallelism": f"simplex shards x{world}, cloud replicated"})
         result = {
             "metric": "flood-filtration simplices/s",
             "value": value,
@@ -254,18 +272,19 @@ def run_ours(args):
             "warmup": args.warmup,
             "ms_per_step": ms,
             "higher_is_better": True,
-            "scaling": "strong",
+            "scaling": "weak" if w["batch"] else "strong",
             "vs_baseline": None,
             "dtype": "f64",
             "numerics": "fp32 FFMA2 filter with a rigorous error bound + exact float64 refine; "
                         "values bit-identical to the reference's float64",
-            "data": "synthetic: seeded generator (noisy sphere+torus mix), no dataset download",
-            "config": {"workload": args.config, "points": w["n"], "landmarks": w["nl"],
-                       "grid_resolution": w["m"], "max_dim": w["max_dim"],
-                       "simplices": n_simplices, "counts": dc.counts_full,
-                       "l2": "flushed (256 MB write) between timed steps",
-                       "parallelism": f"simplex shards x{world}, cloud replicated"},
+            "data": "synthetic: seeded generator (" + {
+                "sphere_torus": "noisy sphere+torus mix", "box": "uniform box",
+                "torus": "torus surface", "modelnet": "ModelNet-shaped primitive unions"}[w["kind"]]
+                    + "), no dataset download",
+            "config": config,
             "fps_ms": w["fps_ms"],
+            "fps_scope": ("one batched launch over this GPU's clouds" if w["batch"]
+                          else "one cloud"),
             "delaunay_s": w["delaunay_s"],
             "gpu_launches": launches,
             "clocks": clocks.summary(),
@@ -275,7 +294,7 @@ def run_ours(args):
         if e2e:
             result["e2e"] = e2e
         result["roofline"] = roofline(lib, stats, ms, args.steps, clocks.summary(),
-                                      brute_pairs=brute_pairs(lib, _native, w, dc, stream))
+                                      brute_pairs=brute_pairs(lib, _native, w, stream))
         result["work_per_step"] = {"fp32_pairs": stats[0] / args.steps,
                                    "candidates_staged": stats[1] / args.steps,
                                    "candidates_scanned": stats[2] / args.steps,
@@ -289,9 +308,12 @@ def run_ours(args):
                                               "staged_phase_a": stats[16] / args.steps,
                                               "staged_block_sampling": stats[17] / args.steps,
                                               "staged_block_exact": stats[18] / args.steps,
-                                              "phase_a_pairs": stats[14] / args.steps}}
+                                              "phase_a_pairs": stats[14] / args.steps,
+                                              "warp_cycles_a_b_c_f": [stats[19 + i] / args.steps
+                                                                      for i in range(4)]}}
         if world == 1 and not args.no_cpu_baseline:
             result["cpu_baseline"] = cpu_baseline(w, args.cpu_seconds)
+            result["fps_cpu_baseline"] = fps_cpu_baseline(w)
     if world > 1 or args.force_sharded:
         import torch.distributed as dist
 
@@ -338,7 +360,7 @@ def _traffic():
         return None
 
 
-def brute_pairs(lib, native, w, dc, stream):
+def brute_pairs(lib, native, w, stream):
     """Pairs the reference algorithm evaluates on this complex (one untimed
     brute-force pass, algorithm 0, counts them on the device)."""
     import torch
@@ -346,7 +368,7 @@ def brute_pairs(lib, native, w, dc, stream):
     stats = np.zeros(24)
     native.check(lib.fph_set_search(0, 0, 0))
     lib.fph_flood_stats(stats.ctypes.data, 1)
-    step_single(lib, native, w, dc, stream)
+    step_single(lib, native, w, stream)
     torch.cuda.synchronize()
     lib.fph_flood_stats(stats.ctypes.data, 1)
     native.check(lib.fph_set_search(1, 0, 0))
@@ -354,45 +376,54 @@ def brute_pairs(lib, native, w, dc, stream):
 
 
 def e2e_host(lib, native, w, args):
-    """Same metric through the C ABI with HOST buffers: H2D of the cloud and
-    complex, the GPU pass, D2H of the values, all inside the timed region."""
+    """Same metric through the C ABI with HOST buffers: H2D of the cloud(s)
+    and complex(es), the GPU pass, D2H of the values, all inside the timed
+    region (pinned host memory)."""
     import torch
 
-    tri = w["tri"]
     top = w["max_dim"]
+
     def pinned(a):  # page-locked copy: the contract's "pinned host memory"
         return torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()
 
-    X = pinned(w["X"])
-    lm = pinned(tri.points)
-    counts = np.array([tri.simplices_by_dim[k].shape[0] for k in range(top + 1)], dtype=np.int64)
-    simp = [None] + [pinned(tri.simplices_by_dim[k].astype(np.int32)) for k in range(1, top + 1)]
-    fac = [None] + [pinned(tri.facet_links[k].astype(np.int32)) for k in range(1, top + 1)]
-    outs = [pinned(np.empty(max(int(c), 1))) for c in counts]
-    h2d = X.nbytes + lm.nbytes + sum(a.nbytes for a in simp[1:]) + sum(a.nbytes for a in fac[1:])
-    d2h = int(sum(counts) * 8)
+    calls, h2d, d2h = [], 0, 0
+    for X, tri in zip(w["Xs"], w["tris"]):
+        Xp, lm = pinned(X), pinned(tri.points)
+        counts = np.array([tri.simplices_by_dim[k].shape[0] for k in range(top + 1)], dtype=np.int64)
+        simp = [None] + [pinned(tri.simplices_by_dim[k].astype(np.int32)) for k in range(1, top + 1)]
+        fac = [None] + [pinned(tri.facet_links[k].astype(np.int32)) for k in range(1, top + 1)]
+        outs = [pinned(np.empty(max(int(c), 1))) for c in counts]
+        h2d += Xp.nbytes + lm.nbytes + sum(a.nbytes for a in simp[1:]) + sum(a.nbytes for a in fac[1:])
+        d2h += int(sum(counts) * 8)
+        calls.append((Xp, lm, counts, native.ptr_array(simp, None), native.ptr_array(fac, None),
+                      native.ptr_array(outs, None), simp, fac, outs))
+    nsimp = sum(int(c[2].sum()) for c in calls)
 
-    def call():
-        native.check(lib.fph_flood_filtration(
-            native.ptr(X), X.shape[0], X.shape[1], native.ptr(lm), lm.shape[0], top,
-            native.ptr(counts), native.ptr_array(simp, None), native.ptr_array(fac, None),
-            w["m"], 1, native.ptr_array(outs, None), native.FPH_MEM_HOST, None))
+    def run():
+        for Xp, lm, counts, sp, fp, op, *_ in calls:
+            native.check(lib.fph_flood_filtration(
+                native.ptr(Xp), Xp.shape[0], Xp.shape[1], native.ptr(lm), lm.shape[0], top,
+                native.ptr(counts), sp, fp, w["m"], 1, op, native.FPH_MEM_HOST, None))
 
     for _ in range(2):
-        call()
+        run()
     times = []
     for _ in range(max(10, args.steps)):  # wall-clock: a median over >= 10 calls
         t0 = time.perf_counter()
-        call()
+        run()
         times.append(time.perf_counter() - t0)
     sec = float(np.median(times))
-    return {"value": float(sum(counts)) / sec, "unit": "simplices/s", "h2d_bytes_per_step": int(h2d),
+    return {"value": nsimp / sec, "unit": "simplices/s", "h2d_bytes_per_step": int(h2d),
             "d2h_bytes_per_step": d2h, "ms_per_step": sec * 1e3}
 
 
 def cpu_sample(w, seconds: float, threads: int):
     """Time the oracle (reference algorithm, C, all threads) on a random
-    sample of top-dimensional simplices (with their faces) of the complex."""
+    sample of the complex's top simplices (each with its faces, as the
+    reference values them: one grid per top cell, filtration.py:246-253).
+    The reference's cost is per top cell, so a sample of |S| of the n_top
+    cells is credited with |S| / n_top of the complex's simplices (crediting
+    the faces the sample happens to carry would over-count them ~2x)."""
     import oracle
 
     sys.path.insert(0, os.path.join(ROOT, "tests"))
@@ -409,7 +440,8 @@ def cpu_sample(w, seconds: float, threads: int):
         t0 = time.perf_counter()
         oracle.flood_values(w["X"], tri.points, sub, m, threads=threads, top_dim=top)
         dt = time.perf_counter() - t0
-        nsimp = sum(v.shape[0] for v in sub.values())
+        total = sum(tri.simplices_by_dim[k].shape[0] for k in range(top + 1))
+        nsimp = total * len(rows) / n_top
         if dt > 0.25 * seconds or sample >= n_top:
             return nsimp, dt, len(rows)
         sample = int(min(n_top, sample * max(2.0, 0.5 * seconds / max(dt, 1e-3))))
@@ -419,8 +451,26 @@ def cpu_baseline(w, seconds: float):
     threads = os.cpu_count() or 1
     nsimp, dt, ntop = cpu_sample(w, seconds, threads)
     return {"value": nsimp / dt, "unit": "simplices/s", "cores": threads, "kind": "port",
-            "sample": f"{ntop} random top simplices (dim {w['max_dim']}) + their faces = "
-                      f"{nsimp} simplices of the same complex, {dt:.1f} s"}
+            "sample": f"{ntop} random top simplices (dim {w['max_dim']}) with their faces, "
+                      f"{dt:.1f} s, credited {ntop}/{w['tri'].simplices_by_dim[w['max_dim']].shape[0]}"
+                      f" of the complex's simplices ({nsimp:.0f})"}
+
+
+def fps_cpu_baseline(w):
+    """The oracle's farthest point sampling (reference geometry.py:88, C
+    port, all host threads) on the same cloud and landmark count as fps_ms,
+    checked index for index against the GPU's landmarks."""
+    import oracle
+
+    threads = os.cpu_count() or 1
+    t0 = time.perf_counter()
+    idx = oracle.fps(w["X"], w["nl"], 0, threads=threads)
+    dt = time.perf_counter() - t0
+    per_cloud = w["fps_ms"] / len(w["Xs"])
+    return {"value": dt * 1e3, "unit": "ms per cloud", "cores": threads, "kind": "port",
+            "sample": f"full FPS of one cloud ({w['n']} points, {w['nl']} landmarks)",
+            "gpu_ms_per_cloud": per_cloud, "speedup": dt * 1e3 / per_cloud,
+            "indices_equal_gpu": bool(np.array_equal(idx, w["idx"]))}
 
 
 def run_reference(args):
@@ -432,10 +482,12 @@ def run_reference(args):
 
     kind, n, nl, m, max_dim = CONFIGS[args.config]
     X = _cloud(kind, n)
-    idx = oracle.fps(X, nl, 0)  # reference algorithm (C port) for the landmarks
+    threads = os.cpu_count() or 1
+    t0 = time.perf_counter()
+    idx = oracle.fps(X, nl, 0, threads=threads)  # reference algorithm (C port) for the landmarks
+    fps_ms = (time.perf_counter() - t0) * 1e3
     tri = delaunay(X[idx])
     w = dict(X=X, tri=tri, m=m, max_dim=min(max_dim, tri.dim))
-    threads = os.cpu_count() or 1
     for _ in range(args.warmup):
         cpu_sample(w, args.cpu_seconds / 4, threads)
     vals = []
@@ -443,7 +495,8 @@ def run_reference(args):
     for _ in range(args.steps):
         nsimp, dt, ntop = cpu_sample(w, args.cpu_seconds, threads)
         vals.append(nsimp / dt)
-        desc = f"{ntop} random top simplices + faces ({nsimp} simplices) per step"
+        desc = (f"{ntop} random top simplices + faces per step, credited {ntop}/"
+                f"{tri.simplices_by_dim[w['max_dim']].shape[0]} of the complex ({nsimp:.0f} simplices)")
     value = float(np.median(vals))
     return {"impl": "reference", "metric": "flood-filtration simplices/s", "value": value,
             "unit": "simplices/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -451,6 +504,7 @@ def run_reference(args):
             "dtype": "f64", "data": "synthetic (seeded generator)",
             "config": {"workload": args.config, "points": n, "landmarks": nl, "grid_resolution": m,
                        "max_dim": w["max_dim"]},
+            "fps_ms": fps_ms,
             "cpu_baseline": {"value": value, "unit": "simplices/s", "cores": threads, "kind": "port",
                              "sample": desc},
             "e2e": {"value": value, "unit": "simplices/s", "h2d_bytes_per_step": 0,
@@ -464,12 +518,11 @@ def run_profile(args):
 
     lib = _native.require_gpu()
     w = prepare(args.config, 0)
-    dc = DeviceComplex(w, 0)
     stream = torch.cuda.current_stream().cuda_stream
     for _ in range(2):
-        step_single(lib, _native, w, dc, stream)
+        step_single(lib, _native, w, stream)
     torch.cuda.synchronize()
-    print("profile run done", dc.counts_full)
+    print("profile run done", [dc.counts_full for _, dc in w["items"]][:2])
 
 
 def main():

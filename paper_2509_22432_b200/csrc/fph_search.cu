@@ -941,13 +941,13 @@ __device__ void run_simplex(const Ctx& c, WarpSmem& W, const Team& tm, float* va
         atomicAdd(&stats[14], pairs);
         // warp-cycles per phase (A, B, C, finalize)
         for (int i = 0; i < 4; ++i) atomicAdd(&stats[19 + i], (unsigned long long)(clk[i + 1] - clk[i]));
-        if (a.dbg && tm.rank == 0) {
-            long long* d = a.dbg + (size_t)c.s * 8;
-            for (int i = 0; i < 4; ++i) d[i] = clk[i + 1] - clk[i];
-            d[4] = (long long)blocks;
-            d[5] = (long long)pruned;
-            d[6] = (long long)(staged + st[0] + st[1]);
-            d[7] = tm.size;
+        if (a.dbg && tm.rank == 0) {  // accumulated: the chained kernels each add their phase
+            unsigned long long* d = reinterpret_cast<unsigned long long*>(a.dbg + (size_t)c.s * 8);
+            for (int i = 0; i < 4; ++i) atomicAdd(d + i, (unsigned long long)(clk[i + 1] - clk[i]));
+            atomicAdd(d + 4, blocks);
+            atomicAdd(d + 5, pruned);
+            atomicAdd(d + 6, staged + st[0] + st[1]);
+            atomicMax(d + 7, (unsigned long long)tm.size);
         }
     }
     tm.sync();
@@ -1090,6 +1090,34 @@ __global__ void iota_kernel(int* out, int n) {
     if (i < n) out[i] = i;
 }
 
+__device__ __forceinline__ unsigned spread3(unsigned v) {  // 8 bits -> every third bit
+    v &= 0xffu;
+    v = (v | (v << 8)) & 0x0f00fu;
+    v = (v | (v << 4)) & 0x0c30c3u;
+    v = (v | (v << 2)) & 0x249249u;
+    return v;
+}
+
+// Schedule key of each simplex: the team-sized ones first (bucket 31), then
+// descending candidate count in factor-2 buckets; within a bucket the 24-bit
+// Morton code of the simplex's cell, so the warps working at the same time
+// read neighbouring parts of the cloud (L2 reuse; a 10M-point cloud does not
+// fit in L2).  Sorted descending on bits [0, 29).
+__global__ void order_key_kernel(Grid g, const SimplexGeom* __restrict__ geom,
+                                 const int* __restrict__ cand, int n, const long long* thr_dev,
+                                 long long thr_fixed, int shift, int* __restrict__ key) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const long long thr = thr_dev ? *thr_dev : thr_fixed;
+    const int c = cand[i];
+    const unsigned bucket = c > thr ? 31u : (unsigned)min(30, 31 - __clz(c + 1));
+    const SimplexGeom& G = geom[i];
+    const unsigned ix = (unsigned)cell_coord(G.cx, g.lox, g.inv_h, g.nx) >> shift;
+    const unsigned iy = (unsigned)cell_coord(G.cy, g.loy, g.inv_h, g.ny) >> shift;
+    const unsigned iz = (unsigned)cell_coord(G.cz, g.loz, g.inv_h, g.nz) >> shift;
+    key[i] = (int)((bucket << 24) | (spread3(iz) << 2) | (spread3(iy) << 1) | spread3(ix));
+}
+
 }  // namespace
 
 size_t search_smem_bytes(int P, int m) {
@@ -1106,26 +1134,6 @@ size_t search_smem_limit() {
 
 int launch_search(const FloodArgs& a, const SimplexGeom* d_geom, const int* d_cand,
                   cudaStream_t stream) {
-    // order simplices by candidate count, largest first: the longest
-    // searches start early and the tail is made of small ones
-    int *d_keys = nullptr, *d_order = nullptr, *d_iota = nullptr, *d_counter = nullptr;
-    FPH_CUDA_TRY(cudaMallocAsync(&d_keys, sizeof(int) * a.n, stream));
-    FPH_CUDA_TRY(cudaMallocAsync(&d_order, sizeof(int) * a.n, stream));
-    FPH_CUDA_TRY(cudaMallocAsync(&d_iota, sizeof(int) * a.n, stream));
-    iota_kernel<<<(a.n + 255) / 256, 256, 0, stream>>>(d_iota, a.n);
-    FPH_CUDA_TRY(cudaMallocAsync(&d_counter, sizeof(int), stream));
-    FPH_CUDA_TRY(cudaMemsetAsync(d_counter, 0, sizeof(int), stream));
-    size_t tmp_bytes = 0;
-    cub::DeviceRadixSort::SortPairsDescending(nullptr, tmp_bytes, d_cand, d_keys, d_iota, d_order,
-                                              a.n, kSortLo, 24, stream);
-    void* tmp = nullptr;
-    FPH_CUDA_TRY(cudaMallocAsync(&tmp, tmp_bytes, stream));
-    // key bits [kSortLo, 24): the order only schedules the work (largest
-    // first), so counts within 2^kSortLo of each other may come in any
-    // order and counts above 2^24 sort among themselves loosely -- two radix
-    // passes instead of three
-    FPH_CUDA_TRY(cub::DeviceRadixSort::SortPairsDescending(tmp, tmp_bytes, d_cand, d_keys, d_iota,
-                                                           d_order, a.n, kSortLo, 24, stream));
     int dev = 0, sms = 0, occ = 0;
     FPH_CUDA_TRY(cudaGetDevice(&dev));
     FPH_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
@@ -1174,6 +1182,35 @@ int launch_search(const FloodArgs& a, const SimplexGeom* d_geom, const int* d_ca
         team_thr_kernel<<<1, 1, 0, stream>>>(d_thr + 1, beta, blocks * kSW, d_thr);
         b.team_thr_dev = d_thr;
     }
+    // order: FPH_ORDER=0 (environment) sorts by candidate count alone,
+    // largest first (bits [8, 24)); the default adds spatial locality
+    // (order_key_kernel)
+    static const int order_mode = getenv("FPH_ORDER") ? atoi(getenv("FPH_ORDER")) : 1;
+    int *d_keys = nullptr, *d_order = nullptr, *d_iota = nullptr, *d_key_in = nullptr;
+    FPH_CUDA_TRY(cudaMallocAsync(&d_keys, sizeof(int) * a.n, stream));
+    FPH_CUDA_TRY(cudaMallocAsync(&d_order, sizeof(int) * a.n, stream));
+    FPH_CUDA_TRY(cudaMallocAsync(&d_iota, sizeof(int) * a.n, stream));
+    iota_kernel<<<(a.n + 255) / 256, 256, 0, stream>>>(d_iota, a.n);
+    int lo_bit = kSortLo, hi_bit = 24;
+    const int* sort_in = d_cand;
+    if (order_mode == 1) {
+        FPH_CUDA_TRY(cudaMallocAsync(&d_key_in, sizeof(int) * a.n, stream));
+        int nmax = max(a.g.nx, max(a.g.ny, a.g.nz)), bits = 0;
+        while ((1 << bits) < nmax) ++bits;
+        order_key_kernel<<<(a.n + 255) / 256, 256, 0, stream>>>(
+            a.g, d_geom, d_cand, a.n, b.team_thr_dev, (long long)a.team_threshold,
+            bits > 8 ? bits - 8 : 0, d_key_in);
+        sort_in = d_key_in;
+        lo_bit = 0;
+        hi_bit = 29;
+    }
+    size_t tmp_bytes = 0;
+    cub::DeviceRadixSort::SortPairsDescending(nullptr, tmp_bytes, sort_in, d_keys, d_iota, d_order,
+                                              a.n, lo_bit, hi_bit, stream);
+    void* tmp = nullptr;
+    FPH_CUDA_TRY(cudaMallocAsync(&tmp, tmp_bytes, stream));
+    FPH_CUDA_TRY(cub::DeviceRadixSort::SortPairsDescending(tmp, tmp_bytes, sort_in, d_keys, d_iota,
+                                                           d_order, a.n, lo_bit, hi_bit, stream));
     int nk = 0;
     while (nk < 4 && kern[nk]) ++nk;
     int* d_stage = nullptr;
@@ -1207,8 +1244,9 @@ int launch_search(const FloodArgs& a, const SimplexGeom* d_geom, const int* d_ca
         FPH_CUDA_TRY(cudaFreeAsync(tmp2, stream));
     }
     FPH_CUDA_TRY(cudaGetLastError());
-    for (void* p : {(void*)d_keys, (void*)d_order, (void*)d_iota, (void*)d_counter, tmp})
+    for (void* p : {(void*)d_keys, (void*)d_order, (void*)d_iota, tmp})
         FPH_CUDA_TRY(cudaFreeAsync(p, stream));
+    if (d_key_in) FPH_CUDA_TRY(cudaFreeAsync(d_key_in, stream));
     return FPH_OK;
 }
 

@@ -62,34 +62,48 @@ def _first_occurrences(pts: np.ndarray):
 
 
 def circumcenters(points: np.ndarray, cells: np.ndarray):
-    """Circumcenter and radius of each full-dimensional cell (inf if flat)."""
+    """Circumcenter and radius of each full-dimensional cell (inf if flat).
+
+    All cells at once: the (dim x dim) systems (e e^T) y = |e|^2 / 2 of the
+    edge vectors e from each cell's first vertex are solved as one stacked
+    LAPACK call; a singular (flat) cell gets center nan, radius inf.
+    """
     dim = points.shape[1]
-    centers = np.empty((cells.shape[0], dim))
-    radii = np.empty(cells.shape[0])
-    for i, cell in enumerate(cells):
-        v = points[cell]
-        e = v[1:] - v[0]
-        rhs = 0.5 * np.einsum("ij,ij->i", e, e)
-        try:
-            y = np.linalg.solve(e @ e.T, rhs)
-        except np.linalg.LinAlgError:
-            centers[i] = np.nan
-            radii[i] = np.inf
-            continue
-        c = v[0] + y @ e
-        centers[i] = c
-        radii[i] = float(np.linalg.norm(c - v[0]))
+    n = cells.shape[0]
+    centers = np.full((n, dim), np.nan)
+    radii = np.full(n, np.inf)
+    if n == 0:
+        return centers, radii
+    v = points[cells]                       # (n, dim + 1, dim)
+    e = v[:, 1:, :] - v[:, :1, :]           # (n, dim, dim)
+    rhs = 0.5 * np.einsum("nij,nij->ni", e, e)
+    gram = e @ np.swapaxes(e, 1, 2)
+    ok = np.ones(n, dtype=bool)
+    try:
+        y = np.linalg.solve(gram, rhs[..., None])[..., 0]
+    except np.linalg.LinAlgError:  # some cell is flat: solve the rest one by one
+        y = np.zeros((n, dim))
+        for i in range(n):
+            try:
+                y[i] = np.linalg.solve(gram[i], rhs[i])
+            except np.linalg.LinAlgError:
+                ok[i] = False
+    c = v[:, 0, :] + (y[:, None, :] @ e)[:, 0, :]
+    centers[ok] = c[ok]
+    radii[ok] = np.linalg.norm(c[ok] - v[ok, 0, :], axis=1)
     return centers, radii
 
 
 def _general_position_violated(pts: np.ndarray, cells: np.ndarray) -> bool:
+    """Some cell is flat, or its circumsphere (plus a 1e-9 relative slack)
+    holds more than dim + 1 landmarks: the triangulation is then an
+    arbitrary tie-break and the caller retries with a seeded jitter."""
     centers, radii = circumcenters(pts, cells)
     if not np.isfinite(radii).all():
         return True
-    tree = cKDTree(pts)
     slack = GP_TOL * max(1.0, float(np.abs(pts).max()))
-    need = pts.shape[1] + 1
-    return any(len(tree.query_ball_point(c, r + slack)) > need for c, r in zip(centers, radii))
+    counts = cKDTree(pts).query_ball_point(centers, radii + slack, return_length=True)
+    return bool((np.asarray(counts) > pts.shape[1] + 1).any())
 
 
 def _qhull_cells(work: np.ndarray):
@@ -99,22 +113,36 @@ def _qhull_cells(work: np.ndarray):
     return tri.simplices
 
 
+def _row_keys(rows: np.ndarray, base: int) -> np.ndarray:
+    """Injective int64 key of each sorted vertex row (lexicographic order)."""
+    key = np.zeros(rows.shape[0], dtype=np.int64)
+    for j in range(rows.shape[1]):
+        key = key * base + rows[:, j]
+    return key
+
+
 def _close_faces(cells: np.ndarray, dim: int):
+    """Every face of the top cells, per dimension (sorted rows, lexicographic),
+    and the facet links: links[k][i, j] = row in dimension k - 1 of simplex i
+    without its j-th vertex."""
+    base = int(cells.max()) + 1 if cells.size else 1
     by_dim = {}
     for k in range(dim + 1):
         if k == dim:
             faces = cells
         else:
             faces = np.concatenate([cells[:, list(c)] for c in combinations(range(dim + 1), k + 1)])
-        by_dim[k] = np.unique(faces, axis=0)
+        # unique rows via their keys (a 1-D sort; key order = lexicographic)
+        _, first = np.unique(_row_keys(faces, base), return_index=True)
+        by_dim[k] = faces[first]
     links = {}
     for k in range(1, dim + 1):
-        lower = {tuple(r): i for i, r in enumerate(by_dim[k - 1].tolist())}
-        rows = by_dim[k].tolist()
-        out = np.empty((len(rows), k + 1), dtype=np.int64)
-        for i, row in enumerate(rows):
-            for j in range(k + 1):
-                out[i, j] = lower[tuple(row[:j] + row[j + 1:])]
+        lower = _row_keys(by_dim[k - 1], base)  # ascending: rows are lexicographic
+        rows = by_dim[k]
+        out = np.empty((rows.shape[0], k + 1), dtype=np.int64)
+        for j in range(k + 1):
+            facet = np.delete(rows, j, axis=1)
+            out[:, j] = np.searchsorted(lower, _row_keys(facet, base))
         links[k] = out
     return by_dim, links
 
@@ -177,9 +205,10 @@ def circumsphere_check(triangulation: Triangulation, tolerance: float = 1e-7) ->
     cells = triangulation.top_cells
     centers, radii = circumcenters(pts, cells)
     bad = []
-    for i, cell in enumerate(cells):
-        if not np.isfinite(radii[i]):
-            continue
-        inside = np.flatnonzero(np.linalg.norm(pts - centers[i], axis=1) < radii[i] - tolerance)
-        bad.extend((i, int(p)) for p in inside if p not in cell)
+    tree = cKDTree(pts)
+    for i in np.flatnonzero(np.isfinite(radii)):
+        near = tree.query_ball_point(centers[i], max(radii[i] - tolerance, 0.0))
+        for p in sorted(near):
+            if p not in cells[i] and np.linalg.norm(pts[p] - centers[i]) < radii[i] - tolerance:
+                bad.append((int(i), int(p)))
     return bad

@@ -5,8 +5,8 @@ of each dimension are dealt round-robin (simplex j -> rank j % world), which
 balances the very uneven per-simplex costs statistically without a cost
 model.  Each rank values its shard with fph_flood_interior, the shards are
 all-gathered (NCCL over NVLink), and every rank runs the facet completion.
-Batches of independent clouds (farthest point sampling) are distributed
-whole: cloud b -> rank b % world.
+Batches of independent clouds are distributed whole (cloud b -> rank
+b % world, batch.flood_cloud_batch): no collective inside a cloud.
 """
 
 from __future__ import annotations
@@ -29,7 +29,7 @@ def gather_interleaved(mine, n_total: int, world: int, dist):
     """
     import torch
 
-    if world == 1:
+    if world == 1 and (dist is None or not dist.is_initialized()):
         return mine[:n_total]
     per = (n_total + world - 1) // world
     buf = torch.full((per,), float("nan"), dtype=mine.dtype, device=mine.device)
@@ -37,11 +37,6 @@ def gather_interleaved(mine, n_total: int, world: int, dist):
     parts = [torch.empty_like(buf) for _ in range(world)]
     dist.all_gather(parts, buf)
     return torch.stack(parts, dim=1).reshape(-1)[:n_total]
-
-
-def shard_clouds(batch: int, world: int, rank: int) -> np.ndarray:
-    """Cloud ids of a batch owned by `rank` (whole clouds, round-robin)."""
-    return shard_rows(batch, world, rank)
 
 
 def shard_interior(pts, lms, by_dim, top: int, m: int, subset: bool, rank: int, world: int,
@@ -62,11 +57,12 @@ def shard_interior(pts, lms, by_dim, top: int, m: int, subset: bool, rank: int, 
     outs = [None] + [torch.empty(max(len(shard_rows(int(counts[k]), world, rank)), 1),
                                  dtype=torch.float64, device=dev) for k in range(1, top + 1)]
     simp = [None] + [by_dim[k] for k in range(1, top + 1)]
-    s = stream if stream is not None else torch.cuda.current_stream(dev).cuda_stream
-    _native.check(lib.fph_flood_shard(
-        pts.data_ptr(), pts.shape[0], pts.shape[1], lms.data_ptr(), lms.shape[0], top,
-        counts.data_ptr(), _native.ptr_array(simp, None), rank, world, m, 1 if subset else 0,
-        _native.ptr_array(outs, None), _native.FPH_MEM_DEVICE, s))
+    with torch.cuda.device(dev):  # the library allocates on the current device
+        s = stream if stream is not None else torch.cuda.current_stream(dev).cuda_stream
+        _native.check(lib.fph_flood_shard(
+            pts.data_ptr(), pts.shape[0], pts.shape[1], lms.data_ptr(), lms.shape[0], top,
+            counts.data_ptr(), _native.ptr_array(simp, None), rank, world, m, 1 if subset else 0,
+            _native.ptr_array(outs, None), _native.FPH_MEM_DEVICE, s))
     return {k: outs[k][: len(shard_rows(int(counts[k]), world, rank))] for k in range(1, top + 1)}
 
 
@@ -83,19 +79,29 @@ def complete(interior: dict, facets: dict, n0: int, top: int, subset: bool, stre
     if not subset:
         raise ValueError("sharded runs need landmarks that are cloud points")
     out = {0: torch.zeros(n0, dtype=torch.float64, device=dev)}
-    for k in range(1, top + 1):
-        out[k] = torch.empty_like(interior[k])
-        _native.check(lib.fph_flood_complete(
-            interior[k].data_ptr(), facets[k].data_ptr(), interior[k].shape[0], k,
-            out[k - 1].data_ptr(), out[k].data_ptr(), s))
+    with torch.cuda.device(dev):
+        for k in range(1, top + 1):
+            out[k] = torch.empty_like(interior[k])
+            _native.check(lib.fph_flood_complete(
+                interior[k].data_ptr(), facets[k].data_ptr(), interior[k].shape[0], k,
+                out[k - 1].data_ptr(), out[k].data_ptr(), s))
     return out
 
 
-def flood_sq_values_sharded(pts, lms, by_dim, facets, top: int, m: int, dist, subset=True):
-    """Multi-GPU flood values: shard, all-gather (NCCL), complete on every rank."""
+def flood_sq_values_sharded(pts, lms, by_dim, facets, top: int, m: int, dist, subset=True,
+                            interior_fn=None, complete_fn=None):
+    """Multi-GPU flood values: this rank's share (fph_flood_shard), all-gather
+    of the interior terms (NCCL), facet completion on every rank.
+
+    interior_fn(rank, world) -> {k: 1-D tensor} and complete_fn(interior,
+    facets, n0, top, subset) -> {k: tensor} default to the device calls; the
+    CPU multi-process tests substitute host implementations."""
     world = dist.get_world_size() if dist is not None and dist.is_initialized() else 1
     rank = dist.get_rank() if world > 1 else 0
-    mine = shard_interior(pts, lms, by_dim, top, m, subset, rank, world)
+    if interior_fn is None:
+        def interior_fn(r, w):
+            return shard_interior(pts, lms, by_dim, top, m, subset, r, w)
+    mine = interior_fn(rank, world)
     interior = {k: gather_interleaved(mine[k], by_dim[k].shape[0], world, dist)
                 for k in range(1, top + 1)}
-    return complete(interior, facets, by_dim[0].shape[0], top, subset)
+    return (complete_fn or complete)(interior, facets, by_dim[0].shape[0], top, subset)

@@ -1,67 +1,67 @@
-"""Per-simplex cost anatomy of the bounded search on configs[1] triangles:
-cycles per phase vs candidate count (debug capture of fph_flood_interior)."""
+"""Per-simplex cost anatomy of the bounded search (debug capture of
+fph_flood_interior: warp-cycles per phase A, B, C, F, blocks searched /
+pruned, candidates staged, team size), binned by candidate count, plus the
+heaviest simplices -- the ones that bound a shard's time at high GPU counts.
 
+  python tools/simplex_costs.py [--config sphere_torus_1m] [--top 10]
+"""
+
+import argparse
 import json
 import os
 import sys
 
 import numpy as np
 
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
 
 
 def main():
-    from paper_2509_22432_b200 import _native, farthest_point_sampling
-    from paper_2509_22432_b200.datagen import gen_sphere_torus_mix
-    from paper_2509_22432_b200.delaunay import delaunay
+    import bench
+    from paper_2509_22432_b200 import _native
 
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="sphere_torus_1m")
+    ap.add_argument("--top", type=int, default=10)
+    args = ap.parse_args()
     lib = _native.require_gpu()
-    X = gen_sphere_torus_mix(1_000_000, seed=0).points
-    tri = delaunay(X[farthest_point_sampling(X, 2000)])
+    w = bench.prepare(args.config, 0)
+    X, tri = w["X"], w["tri"]
     lms = np.ascontiguousarray(tri.points)
-    out = {}
-    for k in (1, 2):
+    out = {"config": args.config}
+    clock_ghz = 1.965
+    for k in range(1, w["max_dim"] + 1):
         rows = tri.simplices_by_dim[k]
         s4 = np.full((rows.shape[0], 4), -1, dtype=np.int32)
         s4[:, : k + 1] = rows
         sq = np.empty(rows.shape[0])
         lib.fph_debug_simplex_cycles(1, None, 0, None)
-        _native.check(lib.fph_flood_interior(_native.ptr(X), X.shape[0], 3, _native.ptr(lms), lms.shape[0],
-                                             _native.ptr(s4), rows.shape[0], k, 20, 1, _native.ptr(sq),
-                                             _native.FPH_MEM_HOST, None))
+        _native.check(lib.fph_flood_interior(_native.ptr(X), X.shape[0], X.shape[1], _native.ptr(lms),
+                                             lms.shape[0], _native.ptr(s4), rows.shape[0], k, w["m"], 1,
+                                             _native.ptr(sq), _native.FPH_MEM_HOST, None))
         buf = np.empty(8 * rows.shape[0], dtype=np.int64)
         n = np.zeros(1, dtype=np.int64)
         lib.fph_debug_simplex_cycles(0, buf.ctypes.data, buf.size, n.ctypes.data)
         d = buf.reshape(-1, 8)
-        # candidate counts from the Ritter balls (host, for binning)
-        V = tri.points[rows]
-        best = np.full(len(rows), -1.0)
-        c = np.zeros((len(rows), 3))
-        for i in range(k + 1):
-            for j in range(i + 1, k + 1):
-                dd = ((V[:, i] - V[:, j]) ** 2).sum(1)
-                u = dd > best
-                best[u] = dd[u]
-                c[u] = 0.5 * (V[u, i] + V[u, j])
-        from scipy.spatial import cKDTree
-
-        r = np.sqrt(((V - c[:, None]) ** 2).sum(2).max(1))
-        C = cKDTree(X).query_ball_point(c, np.sqrt(2) * r, return_length=True)
         tot = d[:, :4].sum(1).astype(float)
-        edges = [0, 512, 2000, 5000, 20000, 50000, 131072, 10 ** 9]
-        rep = []
-        for lo, hi in zip(edges[:-1], edges[1:]):
-            m = (C > lo) & (C <= hi)
-            if m.any():
-                team = d[m, 7] > 1
-                rep.append({"C": f"({lo},{hi}]", "n": int(m.sum()),
-                            "cycles_share": float(tot[m].sum() / tot.sum()),
-                            "warp_cycles_mean": float(tot[m].mean()),
-                            "phase_share": [float(d[m, i].sum() / max(tot[m].sum(), 1)) for i in range(4)],
-                            "blocks_searched_mean": float(d[m, 4].mean()),
-                            "blocks_pruned_mean": float(d[m, 5].mean()),
-                            "staged_mean": float(d[m, 6].mean()), "team": int(team.sum())})
-        out[f"dim{k}"] = rep
+        staged = d[:, 6].astype(float)
+        order = np.argsort(-tot)
+        q = np.quantile(tot, [0.5, 0.9, 0.99, 0.999, 1.0])
+        top1 = order[: max(1, len(order) // 100)]
+        out[f"dim{k}"] = {
+            "n": int(len(rows)),
+            "warp_cycles_total": float(tot.sum()),
+            "quantiles_warp_cycles_p50_p90_p99_p999_max": [float(v) for v in q],
+            "max_simplex_us_single_warp": float(q[-1] / clock_ghz / 1e3),
+            "top1pct_share": float(tot[top1].sum() / tot.sum()),
+            "phase_share": [float(d[:, i].sum() / tot.sum()) for i in range(4)],
+            "team_simplices": int((d[:, 7] > 1).sum()),
+            "heaviest": [{"row": int(i), "warp_cycles": float(tot[i]),
+                          "phases": [int(v) for v in d[i, :4]], "blocks": int(d[i, 4]),
+                          "pruned": int(d[i, 5]), "staged": int(staged[i]), "team": int(d[i, 7])}
+                         for i in order[: args.top]],
+        }
     print(json.dumps(out, indent=1))
 
 
