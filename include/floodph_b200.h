@@ -230,6 +230,15 @@ int fph_debug_simplex_cycles(int32_t enable, int64_t* out, int64_t cap, int64_t*
 /* Measured FP32 (FFMA2) throughput of the current device, TFLOP/s. */
 double fph_fp32_peak_tflops(void);
 
+/*
+ * Tensor-core decision microbenchmarks: elements
+ * per second that can leave TMEM through tcgen05.ld and be min-reduced
+ * (all SMs), and (sample point, candidate) pairs per second of the FFMA2
+ * tile-min loop the flooding kernel runs.  0 on failure.
+ */
+double fph_tmem_min_rate(void);
+double fph_tilemin_rate(void);
+
 /* Kernel launches issued by this thread since the last reset (for bench accounting). */
 int64_t fph_launch_count(int32_t reset);
 

@@ -65,6 +65,8 @@ SIGNATURES = {
     "fph_flood_stats": (ctypes.c_int, [_vp, ctypes.c_int32]),
     "fph_debug_simplex_cycles": (ctypes.c_int, [ctypes.c_int32, _vp, ctypes.c_int64, _vp]),
     "fph_fp32_peak_tflops": (ctypes.c_double, []),
+    "fph_tmem_min_rate": (ctypes.c_double, []),
+    "fph_tilemin_rate": (ctypes.c_double, []),
     "fph_launch_count": (ctypes.c_int64, [ctypes.c_int32]),
 }
 

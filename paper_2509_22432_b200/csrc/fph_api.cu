@@ -297,6 +297,20 @@ double fph_fp32_peak_tflops(void) {
     return ffma2_peak_tflops(dev);
 }
 
+double fph_tmem_min_rate(void) {
+    if (ensure_device() != FPH_OK) return 0.0;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    return tmem_min_rate(dev);
+}
+
+double fph_tilemin_rate(void) {
+    if (ensure_device() != FPH_OK) return 0.0;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    return tilemin_rate(dev);
+}
+
 int fph_debug_simplex_cycles(int32_t enable, int64_t* out, int64_t cap, int64_t* n) {
     debug_enable(enable != 0);
     if (out && n) {

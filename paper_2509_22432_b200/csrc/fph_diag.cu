@@ -1,6 +1,17 @@
-// fph_diag.cu -- FP32 throughput microbenchmark: the roofline denominator
-// for the FFMA2-bound flooding kernel (MEASURED_PEAKS.json carries only HBM
-// and bf16 tensor peaks).  Independent fma.rn.f32x2 chains, 4 flop each.
+// fph_diag.cu -- microbenchmarks behind the roofline and design decisions.
+//
+//  * FP32 throughput (the denominator for the FFMA2-bound flooding kernel;
+//    MEASURED_PEAKS.json carries only HBM and bf16 tensor peaks):
+//    independent fma.rn.f32x2 chains, 4 flop each.
+//  * The tensor-core question (BASELINE north star: "a tensor-core
+//    |a|^2+|b|^2-2ab variant is kept only if it wins"): as a GEMM, the
+//    distance pass is [a, |a|^2] . [-2b, 1] with K = 4, and every one of the
+//    rows x candidates products must leave TMEM (tcgen05.ld) to be
+//    min-reduced.  tmem_min_rate() measures that epilogue alone -- TMEM load
+//    plus a 3-input min per element, all SMs -- and tilemin_rate() the FFMA2
+//    pass the kernel runs (shared-memory candidate pairs, 3 FFMA2 + 1 FMNMX3
+//    per two pairs).  If the epilogue alone is slower than the whole FFMA2
+//    pass, no tcgen05 variant can win, whatever its MMA rate.
 #include "fph_flood.cuh"
 
 namespace fph {
@@ -23,7 +34,143 @@ __global__ void __launch_bounds__(256) ffma2_burn(float* out, int iters, float s
     if (s == 12345.678f) out[0] = s;  // keep the chains alive
 }
 
+// Each CTA (128 threads = one warpgroup, one CTA per SM: it owns all 512
+// TMEM columns) repeatedly loads its 128 lanes x 512 columns of fp32 from
+// TMEM with tcgen05.ld.32x32b.x64 and min-reduces every element.
+__global__ void __launch_bounds__(128, 1) tmem_min_kernel(int iters, float* out) {
+    __shared__ uint32_t taddr_smem;
+    const int warp = threadIdx.x >> 5;
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(
+            (unsigned)__cvta_generic_to_shared(&taddr_smem)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;\n");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;\n");
+    const uint32_t taddr = taddr_smem + ((uint32_t)(32 * warp) << 16);
+    float m0 = INFINITY, m1 = INFINITY;
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll 1
+        for (int col = 0; col < 512; col += 64) {
+            uint32_t r[64];
+            asm volatile(
+                "tcgen05.ld.sync.aligned.32x32b.x64.b32 "
+                "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+                "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,"
+                "%32,%33,%34,%35,%36,%37,%38,%39,%40,%41,%42,%43,%44,%45,%46,%47,"
+                "%48,%49,%50,%51,%52,%53,%54,%55,%56,%57,%58,%59,%60,%61,%62,%63}, [%64];\n"
+                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]),
+                  "=r"(r[6]), "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]),
+                  "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]),
+                  "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+                  "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]),
+                  "=r"(r[30]), "=r"(r[31]), "=r"(r[32]), "=r"(r[33]), "=r"(r[34]), "=r"(r[35]),
+                  "=r"(r[36]), "=r"(r[37]), "=r"(r[38]), "=r"(r[39]), "=r"(r[40]), "=r"(r[41]),
+                  "=r"(r[42]), "=r"(r[43]), "=r"(r[44]), "=r"(r[45]), "=r"(r[46]), "=r"(r[47]),
+                  "=r"(r[48]), "=r"(r[49]), "=r"(r[50]), "=r"(r[51]), "=r"(r[52]), "=r"(r[53]),
+                  "=r"(r[54]), "=r"(r[55]), "=r"(r[56]), "=r"(r[57]), "=r"(r[58]), "=r"(r[59]),
+                  "=r"(r[60]), "=r"(r[61]), "=r"(r[62]), "=r"(r[63])
+                : "r"(taddr + col));
+            asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+            for (int i = 0; i < 64; i += 4) {
+                m0 = fmin3(m0, __uint_as_float(r[i]), __uint_as_float(r[i + 1]));
+                m1 = fmin3(m1, __uint_as_float(r[i + 2]), __uint_as_float(r[i + 3]));
+            }
+        }
+    }
+    if (fminf(m0, m1) == -12345.f) out[0] = m0;  // keep the loads alive
+    asm volatile("tcgen05.fence::before_thread_sync;\n");
+    __syncthreads();
+    if (warp == 0)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(taddr_smem));
+}
+
+// The flooding kernel's inner loop (tile_min in fph_search.cu): each lane
+// one sample point, candidates from a shared-memory tile in the pair layout,
+// 3 FFMA2 + 1 FMNMX3 per two (point, candidate) pairs, four chains.
+__global__ void __launch_bounds__(256) tilemin_kernel(int iters, float* out) {
+    __shared__ float4 tA[256], tB[256];
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) {
+        tA[i] = make_float4(i * 1e-3f, -i * 1e-3f, 0.5f, 0.25f);
+        tB[i] = make_float4(0.1f, 0.2f, i * 1e-4f, 1.f);
+    }
+    __syncthreads();
+    const float px = threadIdx.x * 1e-3f, py = 0.3f, pz = -0.2f;
+    const float2 bx = make_float2(px, px), by = make_float2(py, py), bz = make_float2(pz, pz);
+    float b0 = INFINITY, b1 = INFINITY, b2 = INFINITY, b3 = INFINITY;
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll 2
+        for (int p = 0; p < 256; p += 4) {
+            float2 u[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const float4 A = tA[p + i], B = tB[p + i];
+                u[i] = ffma2(bz, make_float2(B.x, B.y), make_float2(B.z, B.w));
+                u[i] = ffma2(by, make_float2(A.z, A.w), u[i]);
+                u[i] = ffma2(bx, make_float2(A.x, A.y), u[i]);
+            }
+            b0 = fmin3(b0, u[0].x, u[0].y);
+            b1 = fmin3(b1, u[1].x, u[1].y);
+            b2 = fmin3(b2, u[2].x, u[2].y);
+            b3 = fmin3(b3, u[3].x, u[3].y);
+        }
+    }
+    if (fminf(fminf(b0, b1), fminf(b2, b3)) == -12345.f) out[0] = b0;
+}
+
+template <class F>
+float best_ms(F launch) {
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    launch();  // warm up
+    float best = 1e30f;
+    for (int r = 0; r < 5; ++r) {
+        cudaEventRecord(a);
+        launch();
+        cudaEventRecord(b);
+        cudaEventSynchronize(b);
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, a, b);
+        if (ms < best) best = ms;
+    }
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    return best;
+}
+
 }  // namespace
+
+double tmem_min_rate(int device) {
+    int sms = 0;
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device) != cudaSuccess)
+        return 0.0;
+    float* d = nullptr;
+    if (cudaMalloc(&d, sizeof(float)) != cudaSuccess) return 0.0;
+    const int iters = 2000;
+    const float ms = best_ms([&] { tmem_min_kernel<<<sms, 128>>>(iters, d); });
+    cudaError_t e = cudaGetLastError();
+    cudaFree(d);
+    if (e != cudaSuccess) {
+        set_error("tmem_min_kernel: %s", cudaGetErrorString(e));
+        return 0.0;
+    }
+    return (double)sms * 128 * 512 * iters / (ms * 1e-3);  // elements per second
+}
+
+double tilemin_rate(int device) {
+    int sms = 0;
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device) != cudaSuccess)
+        return 0.0;
+    float* d = nullptr;
+    if (cudaMalloc(&d, sizeof(float)) != cudaSuccess) return 0.0;
+    const int iters = 4000, blocks = sms * 4;
+    const float ms = best_ms([&] { tilemin_kernel<<<blocks, 256>>>(iters, d); });
+    cudaFree(d);
+    return (double)blocks * 256 * 512 * iters / (ms * 1e-3);  // (point, candidate) pairs per second
+}
 
 double ffma2_peak_tflops(int device) {
     int sms = 0;

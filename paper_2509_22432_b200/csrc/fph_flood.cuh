@@ -71,6 +71,9 @@ struct FloodTuning {
 int flood_stats(double* out, int reset);
 void profile_push(cudaEvent_t a, cudaEvent_t b);
 double ffma2_peak_tflops(int device);
+// elements/s of tcgen05.ld + min over all SMs; pairs/s of the FFMA2 tile-min loop
+double tmem_min_rate(int device);
+double tilemin_rate(int device);
 
 int choose_ppt(int P);
 
