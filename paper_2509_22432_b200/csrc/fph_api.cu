@@ -128,6 +128,43 @@ struct HostCtx {
     }
 };
 
+// The search kernels read the grid's parameters from one constant-memory
+// slot per device (fph_search.cu c_grid).  A call that launches them holds
+// its device's slot from the copy of its grid into it until its kernels are
+// queued, and the next call's stream waits for an event recorded after them,
+// so the GPU never rewrites the slot under running kernels.
+struct DevSlot {
+    std::mutex mu;
+    cudaEvent_t free_ev = nullptr;
+};
+std::mutex g_slot_map_mu;
+std::map<int, DevSlot*> g_slots;
+
+struct GridSlot {
+    DevSlot* ds = nullptr;
+    cudaStream_t stream = nullptr;
+    int acquire(const Grid* d_grid, cudaStream_t s) {
+        int dev = 0;
+        FPH_CUDA_TRY(cudaGetDevice(&dev));
+        {
+            std::lock_guard<std::mutex> lock(g_slot_map_mu);
+            auto it = g_slots.find(dev);
+            if (it == g_slots.end()) it = g_slots.emplace(dev, new DevSlot).first;
+            ds = it->second;
+        }
+        ds->mu.lock();
+        stream = s;
+        if (ds->free_ev) FPH_CUDA_TRY(cudaStreamWaitEvent(s, ds->free_ev, 0));
+        return set_search_grid(d_grid, s);
+    }
+    ~GridSlot() {
+        if (!ds) return;
+        if (!ds->free_ev) cudaEventCreateWithFlags(&ds->free_ev, cudaEventDisableTiming);
+        if (ds->free_ev) cudaEventRecord(ds->free_ev, stream);
+        ds->mu.unlock();
+    }
+};
+
 // a host-memory call returns once its stream is drained (on errors too)
 int host_finish(const HostCtx& hc, int memory, int rc) {
     if (memory != FPH_MEM_HOST) return rc;
@@ -463,7 +500,9 @@ int fph_flood_interior(const double* points, int64_t n_points, int32_t dim,
         count_launches(4);
         double* d_out = out_sq;
         if (memory == FPH_MEM_HOST) FPH_TRY(sc.alloc(&d_out, n_simplices));
-        rc = flood_interior(gs.grid, lm3, d_s, (int)n_simplices, k, grid_resolution, subset_mode,
+        GridSlot slot;
+        FPH_TRY(slot.acquire(gs.d_grid, hc.stream));
+        rc = flood_interior(gs.d_grid, lm3, d_s, (int)n_simplices, k, grid_resolution, subset_mode,
                             d_out, current_tuning(), hc.stream);
         count_launches(4);
         if (rc == FPH_OK && memory == FPH_MEM_HOST)
@@ -512,7 +551,9 @@ int fph_flood_samples(const double* points, int64_t n_points, int32_t dim,
         count_launches(4);
         double* d_out = out_sq;
         if (memory == FPH_MEM_HOST) FPH_TRY(sc.alloc(&d_out, n_simplices));
-        rc = flood_interior(gs.grid, lm3, d_s, (int)n_simplices, k, 1, subset_mode, d_out,
+        GridSlot slot;
+        FPH_TRY(slot.acquire(gs.d_grid, hc.stream));
+        rc = flood_interior(gs.d_grid, lm3, d_s, (int)n_simplices, k, 1, subset_mode, d_out,
                             current_tuning(), hc.stream, smp3, n_samples);
         count_launches(4);
         if (rc == FPH_OK && memory == FPH_MEM_HOST)
@@ -526,7 +567,7 @@ int fph_flood_samples(const double* points, int64_t n_points, int32_t dim,
 // Interior terms of dimensions 1..max_dim, concurrently on side streams
 // forked from (and joined back into) `stream`.  With profiling on, the
 // flooding time recorded is the fork-to-join interval.
-static int run_interiors(const Grid& g, const double* lm3, int* const* s4, double* const* interior,
+static int run_interiors(const Grid* g, const double* lm3, int* const* s4, double* const* interior,
                          const int64_t* counts, int max_dim, int grid_resolution, int subset_mode,
                          FloodTuning tune, cudaStream_t stream) {
     cudaEvent_t fork = nullptr, done[4] = {nullptr, nullptr, nullptr, nullptr}, p0 = nullptr,
@@ -617,7 +658,9 @@ int fph_flood_shard(const double* points, int64_t n_points, int32_t dim,
             if (memory == FPH_MEM_HOST) FPH_TRY(sc.alloc(&d_out[k], (size_t)mine[k]));
         }
         // every dimension's share concurrently, as in fph_flood_filtration
-        if (rc == FPH_OK) rc = run_interiors(gs.grid, lm3, s4, d_out, mine, max_dim,
+        GridSlot slot;
+        if (rc == FPH_OK) rc = slot.acquire(gs.d_grid, hc.stream);
+        if (rc == FPH_OK) rc = run_interiors(gs.d_grid, lm3, s4, d_out, mine, max_dim,
                                             grid_resolution, subset_mode, tune, hc.stream);
         for (int k = 1; k <= max_dim && rc == FPH_OK; ++k)
             if (mine[k] > 0 && memory == FPH_MEM_HOST)
@@ -661,6 +704,8 @@ int fph_flood_filtration(const double* points, int64_t n_points, int32_t dim,
         FPH_TRY(grid_build(d_pts, (int)n_points, dim, 0.0, g_occupancy, hc.stream, &gs));
         count_launches(4);
         const FloodTuning tune = current_tuning();
+        GridSlot slot;
+        FPH_TRY(slot.acquire(gs.d_grid, hc.stream));
         double* d_vals[4] = {nullptr, nullptr, nullptr, nullptr};
         const int32_t* d_f[4] = {nullptr, nullptr, nullptr, nullptr};
         int* s4[4] = {nullptr, nullptr, nullptr, nullptr};
@@ -681,7 +726,7 @@ int fph_flood_filtration(const double* points, int64_t n_points, int32_t dim,
                     FPH_TRY(sc.alloc(&v4, (size_t)nk * 4));
                     vertex_ids_kernel<<<blocks_for(nk), 256, 0, hc.stream>>>(nk, v4);
                     count_launches(1);
-                    rc = flood_interior(gs.grid, lm3, v4, (int)nk, 0, grid_resolution, 0, d_out,
+                    rc = flood_interior(gs.d_grid, lm3, v4, (int)nk, 0, grid_resolution, 0, d_out,
                                         tune, hc.stream);
                     count_launches(4);
                 }
@@ -698,7 +743,7 @@ int fph_flood_filtration(const double* points, int64_t n_points, int32_t dim,
         // The interior terms of the dimensions >= 1 are independent: each runs
         // on its own stream so one dimension's kernels fill the other's tail;
         // the facet completion then runs in increasing dimension.
-        if (rc == FPH_OK) rc = run_interiors(gs.grid, lm3, s4, interior, counts, max_dim,
+        if (rc == FPH_OK) rc = run_interiors(gs.d_grid, lm3, s4, interior, counts, max_dim,
                                             grid_resolution, subset_mode, tune, hc.stream);
         for (int k = 1; k <= max_dim && rc == FPH_OK; ++k) {
             if (counts[k] == 0) continue;
@@ -752,7 +797,7 @@ int fph_candidate_mask(const double* points, int64_t n_points, int32_t dim,
         GridGuard gg{gs, hc.stream};
         FPH_TRY(grid_build(d_pts, (int)n_points, dim, 0.0, g_occupancy, hc.stream, &gs, true));
         FPH_CUDA_TRY(cudaMemsetAsync(d_off, 0, sizeof(long long), hc.stream));
-        FPH_TRY(candidate_counts(gs.grid, lm3, c4, (int)n_cells, k, d_off + 1, hc.stream));
+        FPH_TRY(candidate_counts(gs.d_grid, lm3, c4, (int)n_cells, k, d_off + 1, hc.stream));
         size_t tb = 0;
         cub::DeviceScan::InclusiveSum(nullptr, tb, d_off + 1, d_off + 1, (int)n_cells, hc.stream);
         unsigned char* tmp;
@@ -770,7 +815,7 @@ int fph_candidate_mask(const double* points, int64_t n_points, int32_t dim,
         }
         int* d_idx;
         FPH_TRY(sc.alloc(&d_idx, (size_t)total));
-        FPH_TRY(candidate_fill(gs.grid, lm3, c4, (int)n_cells, k, d_off, total, d_idx, hc.stream));
+        FPH_TRY(candidate_fill(gs.d_grid, lm3, c4, (int)n_cells, k, d_off, total, d_idx, hc.stream));
         count_launches(3);
         FPH_CUDA_TRY(cudaMemcpyAsync(out_indices, d_idx, sizeof(int) * total,
                                      cudaMemcpyDeviceToHost, hc.stream));

@@ -118,6 +118,7 @@ __global__ void setup_kernel(FloodArgs a, SimplexGeom* __restrict__ geom,
     int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     int lane = threadIdx.x & 31;
     if (warp >= a.n) return;
+    const Grid g = *a.gp;
     Verts V;
     load_verts(a, warp, V);
     SimplexGeom G;
@@ -129,7 +130,7 @@ __global__ void setup_kernel(FloodArgs a, SimplexGeom* __restrict__ geom,
     G.r = r;
     // sqrt(2) r: Lemma 4.2 masking radius; tiny relative slack for rounding
     G.rho = a.subset ? 1.4142135623730951 * r * (1.0 + 1e-9) : 0.0;
-    Box b = a.subset ? ball_box(a.g, c[0], c[1], c[2], G.rho) : full_box(a.g);
+    Box b = a.subset ? ball_box(g, c[0], c[1], c[2], G.rho) : full_box(g);
     G.box = b;
     int rows = b.rows();
     long long cand = 0;
@@ -137,21 +138,21 @@ __global__ void setup_kernel(FloodArgs a, SimplexGeom* __restrict__ geom,
         // bounded search: the count only steers sampling and scheduling, so
         // an estimate suffices -- fp32 row clipping, every `step`-th row
         const int step = rows > 512 ? 4 : (rows > 128 ? 2 : 1);
-        const RowClipF cf = make_clip_f(a.g, c[0], c[1], c[2], G.rho);
+        const RowClipF cf = make_clip_f(g, c[0], c[1], c[2], G.rho);
 #pragma unroll 4
         for (int rr = lane * step; rr < rows; rr += 32 * step) {
             int2 run;
             if (a.subset) {
-                run = row_run_f(a.g, b, rr, cf);
+                run = row_run_f(g, b, rr, cf);
             } else {
-                const int base = ((b.z0 + rr / b.ny_b()) * a.g.ny + b.y0 + rr % b.ny_b()) * a.g.nx;
-                run = make_int2(a.g.cell_start[base + b.x0], a.g.cell_start[base + b.x1 + 1]);
+                const int base = ((b.z0 + rr / b.ny_b()) * g.ny + b.y0 + rr % b.ny_b()) * g.nx;
+                run = make_int2(g.cell_start[base + b.x0], g.cell_start[base + b.x1 + 1]);
             }
             cand += (long long)(run.y - run.x) * step;
         }
     } else {
         for (int rr = lane; rr < rows; rr += 32) {
-            int2 run = row_run(a.g, b, rr, c[0], c[1], c[2], G.rho, a.subset != 0);
+            int2 run = row_run(g, b, rr, c[0], c[1], c[2], G.rho, a.subset != 0);
             cand += run.y - run.x;
         }
     }
@@ -220,14 +221,14 @@ __device__ __forceinline__ void compute_tile(SmemPass& S, int n, int g, int G, b
 
 // Exact float64 nearest-neighbour squared distance of p over the grid cells
 // of the ball |x - p| <= R (cooperative over the CTA).
-__device__ __noinline__ double refine_point(const FloodArgs& a, SmemPass& S, const double p[3], double R) {
-    Box b = ball_box(a.g, p[0], p[1], p[2], R);
+__device__ __noinline__ double refine_point(const Grid& g, SmemPass& S, const double p[3], double R) {
+    Box b = ball_box(g, p[0], p[1], p[2], R);
     int rows = b.rows();
     double best = INFINITY;
     unsigned long long scanned = 0;
     for (int rb = 0; rb < rows; rb += kThreads) {
         int r = rb + threadIdx.x;
-        int2 run = r < rows ? row_run(a.g, b, r, p[0], p[1], p[2], R, true) : make_int2(0, 0);
+        int2 run = r < rows ? row_run(g, b, r, p[0], p[1], p[2], R, true) : make_int2(0, 0);
         int total;
         int off = block_excl(run.y - run.x, S.warp_buf, total);
         S.row_off[threadIdx.x] = off;
@@ -242,7 +243,7 @@ __device__ __noinline__ double refine_point(const FloodArgs& a, SmemPass& S, con
                 if (S.row_off[mid] <= f) lo = mid; else hi = mid;
             }
             int idx = S.row_beg[lo] + f - S.row_off[lo];
-            best = fmin(best, sq64(a.g.x[idx], a.g.y[idx], a.g.z[idx], p[0], p[1], p[2]));
+            best = fmin(best, sq64(g.x[idx], g.y[idx], g.z[idx], p[0], p[1], p[2]));
         }
         __syncthreads();
     }
@@ -324,7 +325,7 @@ __device__ __noinline__ double finalize(const FloodArgs& a, SmemPass& S, int s, 
                 sample_row(a, V, s, jj, nullptr, p);
                 double R2 = fmax((double)vv + 2.0 * (double)EE, 0.0);
                 double R = sqrt(R2) * (1.0 + 1e-6) + 1e-300;
-                double m64 = refine_point(a, S, p, R);
+                double m64 = refine_point(*a.gp, S, p, R);
                 M = fmax(M, m64);
             }
             __syncthreads();
@@ -338,6 +339,7 @@ __global__ void __launch_bounds__(kThreads, 2) pass_kernel(FloodArgs a, const Si
                                                         const int* task_off, int* task_counter,
                                                         int* done) {
     __shared__ SmemPass S;
+    const Grid grid = *a.gp;
     const int total_tasks = task_off[a.n];
     for (;;) {
         if (threadIdx.x == 0) S.task = atomicAdd(task_counter, 1);
@@ -387,7 +389,7 @@ __global__ void __launch_bounds__(kThreads, 2) pass_kernel(FloodArgs a, const Si
         unsigned long long n_staged = 0, n_scanned = 0;
         for (int rb = row_lo; rb < row_hi; rb += kThreads) {
             int r = rb + threadIdx.x;
-            int2 run = r < row_hi ? row_run(a.g, G.box, r, G.cx, G.cy, G.cz, G.rho, a.subset != 0)
+            int2 run = r < row_hi ? row_run(grid, G.box, r, G.cx, G.cy, G.cz, G.rho, a.subset != 0)
                                   : make_int2(0, 0);
             int total;
             int off = block_excl(run.y - run.x, S.warp_buf, total);
@@ -407,9 +409,9 @@ __global__ void __launch_bounds__(kThreads, 2) pass_kernel(FloodArgs a, const Si
                         if (S.row_off[mid] <= f) l = mid; else h = mid;
                     }
                     int idx = S.row_beg[l] + f - S.row_off[l];
-                    ax = __double2float_rn(__dsub_rn(a.g.x[idx], G.cx));
-                    ay = __double2float_rn(__dsub_rn(a.g.y[idx], G.cy));
-                    az = __double2float_rn(__dsub_rn(a.g.z[idx], G.cz));
+                    ax = __double2float_rn(__dsub_rn(grid.x[idx], G.cx));
+                    ay = __double2float_rn(__dsub_rn(grid.y[idx], G.cy));
+                    az = __double2float_rn(__dsub_rn(grid.z[idx], G.cz));
                     aw = fmaf(az, az, fmaf(ay, ay, ax * ax));
                     keep = aw <= thr;
                 }
@@ -672,13 +674,13 @@ long long interior_rows(int k, int m) {
 // per-point fp32 scratch per chunk of simplices (n x P floats)
 constexpr double kPerpointBudget = 2.0 * (1 << 30);
 
-int flood_range(const Grid& g, const double* d_landmarks3, const int* d_simplices, int n, int k,
+int flood_range(const Grid* d_grid, const double* d_landmarks3, const int* d_simplices, int n, int k,
                 int m, int subset, double* d_out_sq, const FloodTuning& tune, cudaStream_t stream,
                 const double* d_explicit, const Template& T) {
     const int P = T.P;
     const int ppt = choose_ppt(P);
     FloodArgs a{};
-    a.g = g;
+    a.gp = d_grid;
     a.landmarks = d_landmarks3;
     a.simplices = d_simplices;
     a.n = n;
@@ -787,7 +789,7 @@ int flood_range(const Grid& g, const double* d_landmarks3, const int* d_simplice
 
 }  // namespace
 
-int flood_interior(const Grid& g, const double* d_landmarks3, const int* d_simplices, int n,
+int flood_interior(const Grid* d_grid, const double* d_landmarks3, const int* d_simplices, int n,
                    int k, int m, int subset, double* d_out_sq, const FloodTuning& tune,
                    cudaStream_t stream, const double* d_explicit, int explicit_rows) {
     if (n == 0) return FPH_OK;
@@ -818,7 +820,7 @@ int flood_interior(const Grid& g, const double* d_landmarks3, const int* d_simpl
         std::max(1ll, std::min((long long)n, (long long)(kPerpointBudget / (4.0 * T.P))));
     for (long long off = 0; off < n; off += chunk) {
         const int cnt = (int)std::min(chunk, n - off);
-        FPH_TRY(flood_range(g, d_landmarks3, d_simplices + off * 4, cnt, k, m, subset,
+        FPH_TRY(flood_range(d_grid, d_landmarks3, d_simplices + off * 4, cnt, k, m, subset,
                             d_out_sq + off, tune, stream,
                             d_explicit ? d_explicit + off * (long long)T.P * 3 : nullptr, T));
     }

@@ -18,7 +18,7 @@ struct SimplexGeom {
 constexpr int kMaxResolution = 65535;
 
 struct FloodArgs {
-    Grid g;
+    const Grid* gp;           // grid parameters (device memory, fph_grid.cu)
     const double* landmarks;  // n_landmarks x 3 (z = 0 for planar clouds)
     const int* simplices;     // n x 4, vertex ids, unused slots -1
     int n, k, m, P;
@@ -52,6 +52,9 @@ int debug_fetch(long long* out, long long cap, long long* n);
 // algorithm 1 (fph_search.cu): warp-per-simplex bounded search
 int launch_search(const FloodArgs& a, const SimplexGeom* d_geom, const int* d_cand,
                   cudaStream_t stream);
+// copy a device grid's parameters into the search kernels' constant slot,
+// ordered on `stream` (the caller holds the device's GridSlot)
+int set_search_grid(const Grid* d_grid, cudaStream_t stream);
 // dynamic shared memory of the search kernel for P rows at resolution m, and
 // the device limit it must fit
 size_t search_smem_bytes(int P, int m);
@@ -79,7 +82,7 @@ int choose_ppt(int P);
 
 // Squared flood value over the relative-interior grid rows of every
 // simplex (k = 0: the vertex itself), exactly as the reference computes it.
-int flood_interior(const Grid& g, const double* d_landmarks3, const int* d_simplices, int n,
+int flood_interior(const Grid* d_grid, const double* d_landmarks3, const int* d_simplices, int n,
                    int k, int m, int subset, double* d_out_sq, const FloodTuning& tune,
                    cudaStream_t stream, const double* d_explicit = nullptr, int explicit_rows = 0);
 
@@ -97,9 +100,9 @@ int fps_batched(const double* d_x, const double* d_y, const double* d_z, int bat
 
 // candidate masks (fph_mask.cu): per simplex, the count / the ascending cloud
 // indices of the points in its masking ball (needs a grid with idx)
-int candidate_counts(const Grid& g, const double* d_lm3, const int* d_cells4, int n, int k,
+int candidate_counts(const Grid* d_grid, const double* d_lm3, const int* d_cells4, int n, int k,
                      long long* d_counts, cudaStream_t stream);
-int candidate_fill(const Grid& g, const double* d_lm3, const int* d_cells4, int n, int k,
+int candidate_fill(const Grid* d_grid, const double* d_lm3, const int* d_cells4, int n, int k,
                    const long long* d_offsets, long long total, int* d_idx, cudaStream_t stream);
 
 }  // namespace fph

@@ -11,6 +11,7 @@
 #include <cub/cub.cuh>
 
 #include <cmath>
+#include <algorithm>
 #include <cstdio>
 
 #include "fph_grid.cuh"
@@ -68,11 +69,64 @@ __global__ void bbox_kernel(const double* __restrict__ pts, int n, int dim,
     }
 }
 
+// Grid parameters from the box, on the device (one thread): cell edge
+// h = (volume x occupancy / n)^(1/dim) (each extent clamped below at 1e-3 of
+// the largest), grown by 1.25x until the cell count fits the host-allocated
+// capacity.  The host never reads the box back, so nothing waits for it.
+__global__ void grid_params_kernel(const unsigned long long* __restrict__ bbox, int n, int dim,
+                                   double cell_size, double occupancy, long long cap,
+                                   Grid out, Grid* __restrict__ g) {
+    double lo[3] = {0.0, 0.0, 0.0}, hi[3] = {0.0, 0.0, 0.0};
+    for (int a = 0; a < dim; ++a) {
+        lo[a] = ord2d(bbox[a]);
+        hi[a] = ord2d(bbox[3 + a]);
+    }
+    double h = cell_size;
+    if (!(h > 0.0)) {
+        double emax = 0.0;
+        for (int a = 0; a < dim; ++a) emax = fmax(emax, hi[a] - lo[a]);
+        if (!(emax > 0.0)) {
+            h = 1.0;
+        } else {
+            double vol = 1.0;
+            for (int a = 0; a < dim; ++a) vol *= fmax(hi[a] - lo[a], emax * 1e-3);
+            h = pow(vol * occupancy / (double)n, 1.0 / dim);
+            if (!(h > 0.0)) h = emax;
+        }
+    }
+    int nc[3] = {1, 1, 1};
+    for (int attempt = 0; attempt < 256; ++attempt) {
+        double total = 1.0;
+        for (int a = 0; a < dim; ++a) {
+            const double c = floor((hi[a] - lo[a]) / h) + 1.0;
+            nc[a] = (int)fmin(c, (double)(1 << 24));
+            total *= nc[a];
+        }
+        if (total <= (double)cap) break;
+        h *= 1.25;
+    }
+    out.n = n;  // `out` arrives with the host-set fields (the pointers)
+    out.nx = nc[0];
+    out.ny = nc[1];
+    out.nz = dim == 3 ? nc[2] : 1;
+    out.lox = lo[0];
+    out.loy = lo[1];
+    out.loz = dim == 3 ? lo[2] : 0.0;
+    out.h = h;
+    out.inv_h = 1.0 / h;
+    double scale = 0.0;
+    for (int a = 0; a < dim; ++a) scale = fmax(scale, fmax(fabs(lo[a]), fabs(hi[a])));
+    out.margin = 1e-9 * (scale + h);
+    *g = out;
+}
+
 // cell id per point + histogram (counting sort pass 1)
-__global__ void cell_id_kernel(const double* __restrict__ pts, int n, int dim, Grid g,
-                               int* __restrict__ keys, int* __restrict__ counts) {
+__global__ void cell_id_kernel(const double* __restrict__ pts, int n, int dim,
+                               const Grid* __restrict__ gp, int* __restrict__ keys,
+                               int* __restrict__ counts) {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
+    const Grid g = *gp;
     const double* p = pts + (size_t)i * dim;
     int ix = cell_coord(p[0], g.lox, g.inv_h, g.nx);
     int iy = cell_coord(p[1], g.loy, g.inv_h, g.ny);
@@ -103,117 +157,68 @@ __global__ void scatter_kernel(const double* __restrict__ pts, int n, int dim,
 
 }  // namespace
 
-double grid_cell_size(const double lo[3], const double hi[3], int dim, long long n,
-                      double occupancy) {
-    double ext[3];
-    double emax = 0.0;
-    for (int a = 0; a < dim; ++a) {
-        ext[a] = hi[a] - lo[a];
-        emax = fmax(emax, ext[a]);
-    }
-    if (!(emax > 0.0)) return 1.0;
-    double vol = 1.0;
-    for (int a = 0; a < dim; ++a) vol *= fmax(ext[a], emax * 1e-3);
-    double h = pow(vol * occupancy / (double)(n > 0 ? n : 1), 1.0 / dim);
-    return h > 0.0 ? h : emax;
-}
-
 int grid_build(const double* d_pts, int n, int dim, double cell_size, double occupancy,
                cudaStream_t stream, GridStore* gs, bool keep_index) {
     if (n < 1 || (dim != 2 && dim != 3)) {
         set_error("grid_build: need n >= 1 and dim in {2, 3}");
         return FPH_EARG;
     }
-    unsigned long long hb[6];
-    unsigned long long* d_bbox = nullptr;
-    FPH_CUDA_TRY(cudaMallocAsync(&d_bbox, 6 * sizeof(unsigned long long), stream));
-    // ordered-int identities: mins start at ~0, maxes at 0 (no host copy)
-    FPH_CUDA_TRY(cudaMemsetAsync(d_bbox, 0xff, 3 * sizeof(unsigned long long), stream));
-    FPH_CUDA_TRY(cudaMemsetAsync(d_bbox + 3, 0, 3 * sizeof(unsigned long long), stream));
-    int blocks = (n + 255) / 256;
-    if (blocks > 592) blocks = 592;
-    bbox_kernel<<<blocks, 256, 0, stream>>>(d_pts, n, dim, d_bbox);
-    FPH_CUDA_TRY(cudaMemcpyAsync(hb, d_bbox, sizeof(hb), cudaMemcpyDeviceToHost, stream));
-    FPH_CUDA_TRY(cudaStreamSynchronize(stream));
-    FPH_CUDA_TRY(cudaFreeAsync(d_bbox, stream));
-    double lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
-    for (int a = 0; a < dim; ++a) {
-        lo[a] = ord2d(hb[a]);
-        hi[a] = ord2d(hb[3 + a]);
-    }
-    double h = cell_size > 0.0 ? cell_size : grid_cell_size(lo, hi, dim, n, occupancy);
-    const double max_cells = 1 << 27;
-    int nc[3] = {1, 1, 1};
-    for (int attempt = 0; attempt < 64; ++attempt) {
-        double total = 1.0;
-        for (int a = 0; a < dim; ++a) {
-            double c = floor((hi[a] - lo[a]) / h) + 1.0;
-            nc[a] = (int)fmin(c, 1 << 24);
-            total *= nc[a];
-        }
-        if (total <= max_cells) break;
-        h *= 1.25;
-    }
-    Grid g{};
-    g.n = n;
-    g.nx = nc[0];
-    g.ny = nc[1];
-    g.nz = dim == 3 ? nc[2] : 1;
-    g.lox = lo[0];
-    g.loy = lo[1];
-    g.loz = dim == 3 ? lo[2] : 0.0;
-    g.h = h;
-    g.inv_h = 1.0 / h;
-    double scale = 0.0;
-    for (int a = 0; a < dim; ++a) scale = fmax(scale, fmax(fabs(lo[a]), fabs(hi[a])));
-    g.margin = 1e-9 * (scale + h);
-    long long ncells = (long long)g.nx * g.ny * g.nz;
-
     gs->free_all(stream);
+    // cell capacity: about n / occupancy cells for a cloud filling its box;
+    // rounding adds at most ~30% for realistic shapes, and the device grows h
+    // until the grid fits (coarser cells stay exact, only slower)
+    const long long cap = std::min<long long>(
+        1ll << 27, (long long)(2.0 * n / (occupancy > 0 ? occupancy : 2.0)) + 4096);
+    Scratch sc(stream);
+    unsigned long long* d_bbox = nullptr;
     int *keys = nullptr, *counts = nullptr, *cursor = nullptr;
-    FPH_CUDA_TRY(cudaMallocAsync(&keys, sizeof(int) * n, stream));
-    FPH_CUDA_TRY(cudaMallocAsync(&counts, sizeof(int) * (ncells + 1), stream));
-    FPH_CUDA_TRY(cudaMallocAsync(&cursor, sizeof(int) * ncells, stream));
+    FPH_TRY(sc.alloc(&d_bbox, 6));
+    FPH_TRY(sc.alloc(&keys, n));
+    FPH_TRY(sc.alloc(&counts, cap + 1));
+    FPH_TRY(sc.alloc(&cursor, cap));
     FPH_CUDA_TRY(cudaMallocAsync(&gs->x, sizeof(double) * n, stream));
     FPH_CUDA_TRY(cudaMallocAsync(&gs->y, sizeof(double) * n, stream));
     FPH_CUDA_TRY(cudaMallocAsync(&gs->z, sizeof(double) * n, stream));
-    FPH_CUDA_TRY(cudaMallocAsync(&gs->cell_start, sizeof(int) * (ncells + 1), stream));
+    FPH_CUDA_TRY(cudaMallocAsync(&gs->cell_start, sizeof(int) * (cap + 1), stream));
+    FPH_CUDA_TRY(cudaMallocAsync(&gs->d_grid, sizeof(Grid), stream));
     if (keep_index) FPH_CUDA_TRY(cudaMallocAsync(&gs->idx, sizeof(int) * n, stream));
-    FPH_CUDA_TRY(cudaMemsetAsync(counts, 0, sizeof(int) * (ncells + 1), stream));
-    FPH_CUDA_TRY(cudaMemsetAsync(cursor, 0, sizeof(int) * ncells, stream));
-    cell_id_kernel<<<(n + 255) / 256, 256, 0, stream>>>(d_pts, n, dim, g, keys, counts);
-    size_t tmp_bytes = 0;
-    cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, counts, gs->cell_start, ncells + 1, stream);
-    void* tmp = nullptr;
-    FPH_CUDA_TRY(cudaMallocAsync(&tmp, tmp_bytes, stream));
-    FPH_CUDA_TRY(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, counts, gs->cell_start, ncells + 1,
-                                               stream));
-    scatter_kernel<<<(n + 255) / 256, 256, 0, stream>>>(d_pts, n, dim, keys, gs->cell_start, cursor,
-                                                        gs->x, gs->y, gs->z, gs->idx);
-    FPH_CUDA_TRY(cudaGetLastError());
-    FPH_CUDA_TRY(cudaFreeAsync(tmp, stream));
-    FPH_CUDA_TRY(cudaFreeAsync(keys, stream));
-    FPH_CUDA_TRY(cudaFreeAsync(counts, stream));
-    FPH_CUDA_TRY(cudaFreeAsync(cursor, stream));
+    Grid g{};
     g.x = gs->x;
     g.y = gs->y;
     g.z = gs->z;
     g.cell_start = gs->cell_start;
     g.idx = gs->idx;
-    gs->grid = g;
-    gs->ncells = ncells;
+    FPH_CUDA_TRY(cudaMemsetAsync(d_bbox, 0xff, 3 * sizeof(unsigned long long), stream));
+    FPH_CUDA_TRY(cudaMemsetAsync(d_bbox + 3, 0, 3 * sizeof(unsigned long long), stream));
+    FPH_CUDA_TRY(cudaMemsetAsync(counts, 0, sizeof(int) * (cap + 1), stream));
+    FPH_CUDA_TRY(cudaMemsetAsync(cursor, 0, sizeof(int) * cap, stream));
+    int blocks = (n + 255) / 256;
+    if (blocks > 592) blocks = 592;
+    bbox_kernel<<<blocks, 256, 0, stream>>>(d_pts, n, dim, d_bbox);
+    grid_params_kernel<<<1, 1, 0, stream>>>(d_bbox, n, dim, cell_size, occupancy, cap, g,
+                                            gs->d_grid);
+    cell_id_kernel<<<(n + 255) / 256, 256, 0, stream>>>(d_pts, n, dim, gs->d_grid, keys, counts);
+    size_t tmp_bytes = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, counts, gs->cell_start, (int)(cap + 1),
+                                  stream);
+    unsigned char* tmp = nullptr;
+    FPH_TRY(sc.alloc(&tmp, tmp_bytes));
+    FPH_CUDA_TRY(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, counts, gs->cell_start,
+                                               (int)(cap + 1), stream));
+    scatter_kernel<<<(n + 255) / 256, 256, 0, stream>>>(d_pts, n, dim, keys, gs->cell_start, cursor,
+                                                        gs->x, gs->y, gs->z, gs->idx);
+    FPH_CUDA_TRY(cudaGetLastError());
+    gs->cap = cap;
     return FPH_OK;
 }
 
 void GridStore::free_all(cudaStream_t stream) {
-    if (x) cudaFreeAsync(x, stream);
-    if (y) cudaFreeAsync(y, stream);
-    if (z) cudaFreeAsync(z, stream);
-    if (cell_start) cudaFreeAsync(cell_start, stream);
-    if (idx) cudaFreeAsync(idx, stream);
+    for (void* p : {(void*)x, (void*)y, (void*)z, (void*)cell_start, (void*)idx, (void*)d_grid})
+        if (p) cudaFreeAsync(p, stream);
     x = y = z = nullptr;
     cell_start = nullptr;
     idx = nullptr;
+    d_grid = nullptr;
 }
 
 }  // namespace fph

@@ -45,12 +45,13 @@ __device__ __forceinline__ MaskBall mask_ball(const double* lm3, const int* cell
 // kFill = false: out_count[s] = number of cloud points in the ball of s;
 // kFill = true: their cloud indices (unordered) at out_idx[offsets[s] ...]
 template <bool kFill>
-__global__ void mask_kernel(Grid g, const double* __restrict__ lm3, const int* __restrict__ cells,
-                            int n, int k, long long* __restrict__ out_count,
+__global__ void mask_kernel(const Grid* __restrict__ gp, const double* __restrict__ lm3,
+                            const int* __restrict__ cells, int n, int k, long long* __restrict__ out_count,
                             const long long* __restrict__ offsets, int* __restrict__ out_idx) {
     const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (warp >= n) return;
+    const Grid g = *gp;
     const MaskBall b = mask_ball(lm3, cells, warp, k);
     const Box box = ball_box(g, b.c[0], b.c[1], b.c[2], b.rad);
     const int rows = box.rows();
@@ -72,7 +73,7 @@ __global__ void mask_kernel(Grid g, const double* __restrict__ lm3, const int* _
 
 }  // namespace
 
-int candidate_counts(const Grid& g, const double* d_lm3, const int* d_cells4, int n, int k,
+int candidate_counts(const Grid* g, const double* d_lm3, const int* d_cells4, int n, int k,
                      long long* d_counts, cudaStream_t stream) {
     if (n == 0) return FPH_OK;
     mask_kernel<false><<<(unsigned)(((long long)n * 32 + 255) / 256), 256, 0, stream>>>(
@@ -81,7 +82,7 @@ int candidate_counts(const Grid& g, const double* d_lm3, const int* d_cells4, in
     return FPH_OK;
 }
 
-int candidate_fill(const Grid& g, const double* d_lm3, const int* d_cells4, int n, int k,
+int candidate_fill(const Grid* g, const double* d_lm3, const int* d_cells4, int n, int k,
                    const long long* d_offsets, long long total, int* d_idx,
                    cudaStream_t stream) {
     if (n == 0 || total == 0) return FPH_OK;

@@ -44,6 +44,15 @@ constexpr int kSThreads = 32 * kSW;
 #define FPH_SEARCH_MINB 2
 #endif
 constexpr int kWT = FPH_WT;     // candidates per warp tile
+
+// The grid's parameters for the search kernels.  The grid is built on the
+// device (fph_grid.cu computes its box and cell size there, so the host
+// never waits for them); before the kernels of a call are queued its
+// parameters are copied here device-to-device on the call's stream
+// (set_search_grid), where every access is a constant-bank operand, as
+// kernel parameters are.  fph_api.cu serialises the calls of a device
+// around this slot (GridSlot).
+__constant__ Grid c_grid;
 constexpr int kMaxBlk = 160;    // blocks ordered best-first per simplex
 
 struct WarpSmem {
@@ -191,16 +200,14 @@ __device__ __forceinline__ float vertex_bound(const Ctx& c, const PointF& q) {
 // exclusive offsets go to shared memory so any lane can map a flattened
 // candidate position to its point index.
 struct Rows {
-    const Grid* g;
     Box box;
     RowClipF cf;
     bool clip;
 };
 
-__device__ __forceinline__ Rows make_rows(const Grid& g, double qx, double qy, double qz,
-                                          double R) {
+__device__ __forceinline__ Rows make_rows(double qx, double qy, double qz, double R) {
+    const Grid& g = c_grid;
     Rows r;
-    r.g = &g;
     r.clip = R < 1e300;
     r.box = r.clip ? ball_box(g, qx, qy, qz, R) : full_box(g);
     if (r.clip) r.cf = make_clip_f(g, qx, qy, qz, R);
@@ -224,11 +231,12 @@ __device__ __forceinline__ Batch row_batch(const Rows& rw, WarpSmem& W, int rb) 
     int2 run = make_int2(0, 0);
     if (r < rows) {
         if (rw.clip) {
-            run = row_run_f(*rw.g, rw.box, r, rw.cf);
+            run = row_run_f(c_grid, rw.box, r, rw.cf);
         } else {
-            const int base = ((rw.box.z0 + r / rw.box.ny_b()) * rw.g->ny + rw.box.y0 +
-                              r % rw.box.ny_b()) * rw.g->nx;
-            run = make_int2(rw.g->cell_start[base + rw.box.x0], rw.g->cell_start[base + rw.box.x1 + 1]);
+            const int base = ((rw.box.z0 + r / rw.box.ny_b()) * c_grid.ny + rw.box.y0 +
+                              r % rw.box.ny_b()) * c_grid.nx;
+            run = make_int2(c_grid.cell_start[base + rw.box.x0],
+                            c_grid.cell_start[base + rw.box.x1 + 1]);
         }
     }
     const int len = run.y - run.x;
@@ -279,7 +287,7 @@ __device__ __forceinline__ int cand_index(const WarpSmem& W, int nne, int f) {
 
 __device__ __forceinline__ void load_rel(const Ctx& c, int idx, float& ax, float& ay, float& az,
                                          float& aw) {
-    const Grid& g = c.a->g;
+    const Grid& g = c_grid;
     ax = __double2float_rn(__dsub_rn(g.x[idx], c.G.cx));
     ay = __double2float_rn(__dsub_rn(g.y[idx], c.G.cy));
     az = __double2float_rn(__dsub_rn(g.z[idx], c.G.cz));
@@ -473,7 +481,7 @@ __device__ void reps_pass(const Ctx& c, WarpSmem& W, int stride, float* vals, co
                           unsigned long long& pairs, unsigned long long& staged) {
     const int lane = threadIdx.x & 31;
     const FloodArgs& a = *c.a;
-    const Rows rw = make_rows(a.g, c.G.cx, c.G.cy, c.G.cz, a.subset ? c.G.rho : 1e301);
+    const Rows rw = make_rows(c.G.cx, c.G.cy, c.G.cz, a.subset ? c.G.rho : 1e301);
     const int rows = rw.box.rows();
     int tile_n = 0;
     long long fbase = 0;  // this warp's own enumeration: any subset is a valid sample
@@ -524,8 +532,8 @@ __device__ float point_min32(const Ctx& c, WarpSmem& W, const PointF& q, double 
     const int lane = threadIdx.x & 31;
     const double qx = c.G.cx + (double)q.bx, qy = c.G.cy + (double)q.by,
                  qz = c.G.cz + (double)q.bz;
-    const double Rrow = R * (1.0 + 1e-4) + 1e-5 * ((double)q.B + R) + c.a->g.margin;
-    const Rows rw = make_rows(c.a->g, qx, qy, qz, Rrow);
+    const double Rrow = R * (1.0 + 1e-4) + 1e-5 * ((double)q.B + R) + c_grid.margin;
+    const Rows rw = make_rows(qx, qy, qz, Rrow);
     const int rows = rw.box.rows();
     float best = INFINITY;
     for (int rb = tm.rank * 32; rb < rows; rb += tm.size * 32) {
@@ -549,9 +557,9 @@ __device__ float point_min32(const Ctx& c, WarpSmem& W, const PointF& q, double 
 __device__ double point_min64(const Ctx& c, WarpSmem& W, const double p[3], double R,
                               const Team& tm, unsigned long long& scanned) {
     const int lane = threadIdx.x & 31;
-    const Rows rw = make_rows(c.a->g, p[0], p[1], p[2], R);
+    const Rows rw = make_rows(p[0], p[1], p[2], R);
     const int rows = rw.box.rows();
-    const Grid& g = c.a->g;
+    const Grid& g = c_grid;
     double best = INFINITY;
     for (int rb = tm.rank * 32; rb < rows; rb += tm.size * 32) {
         const Batch bt = row_batch(rw, W, rb);
@@ -617,9 +625,9 @@ __device__ void search_block(const Ctx& c, WarpSmem& W, int nb, float* vals, flo
     float best = INFINITY;
     for (int pass = 0; pass < 2; ++pass) {
         const bool full = !(R < 1e300);
-        const double Rrow = full ? 1e301 : R * (1.0 + 1e-4) + 1e-5 * (cbn + R) + a.g.margin;
+        const double Rrow = full ? 1e301 : R * (1.0 + 1e-4) + 1e-5 * (cbn + R) + c_grid.margin;
         const float rout2 = full ? INFINITY : (float)(R * R);
-        const Rows rw = make_rows(a.g, qx, qy, qz, Rrow);
+        const Rows rw = make_rows(qx, qy, qz, Rrow);
         const int rows = rw.box.rows();
         int stride = 1;
         // a region expected to hold few candidates (the simplex's count
@@ -1103,11 +1111,15 @@ __device__ __forceinline__ unsigned spread3(unsigned v) {  // 8 bits -> every th
 // Morton code of the simplex's cell, so the warps working at the same time
 // read neighbouring parts of the cloud (L2 reuse; a 10M-point cloud does not
 // fit in L2).  Sorted descending on bits [0, 29).
-__global__ void order_key_kernel(Grid g, const SimplexGeom* __restrict__ geom,
+__global__ void order_key_kernel(const Grid* __restrict__ gp, const SimplexGeom* __restrict__ geom,
                                  const int* __restrict__ cand, int n, const long long* thr_dev,
-                                 long long thr_fixed, int shift, int* __restrict__ key) {
+                                 long long thr_fixed, int* __restrict__ key) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
+    const Grid g = *gp;
+    const int nmax = max(g.nx, max(g.ny, g.nz));
+    const int bits = 32 - __clz(max(nmax - 1, 1));
+    const int shift = bits > 8 ? bits - 8 : 0;
     const long long thr = thr_dev ? *thr_dev : thr_fixed;
     const int c = cand[i];
     const unsigned bucket = c > thr ? 31u : (unsigned)min(30, 31 - __clz(c + 1));
@@ -1119,6 +1131,12 @@ __global__ void order_key_kernel(Grid g, const SimplexGeom* __restrict__ geom,
 }
 
 }  // namespace
+
+int set_search_grid(const Grid* d_grid, cudaStream_t stream) {
+    FPH_CUDA_TRY(cudaMemcpyToSymbolAsync(c_grid, d_grid, sizeof(Grid), 0, cudaMemcpyDeviceToDevice,
+                                         stream));
+    return FPH_OK;
+}
 
 size_t search_smem_bytes(int P, int m) {
     return (P <= kValsCap ? kSmemVals : sizeof(SearchSmem)) + sizeof(double) * (size_t)(m + 1);
@@ -1195,11 +1213,8 @@ int launch_search(const FloodArgs& a, const SimplexGeom* d_geom, const int* d_ca
     const int* sort_in = d_cand;
     if (order_mode == 1) {
         FPH_CUDA_TRY(cudaMallocAsync(&d_key_in, sizeof(int) * a.n, stream));
-        int nmax = max(a.g.nx, max(a.g.ny, a.g.nz)), bits = 0;
-        while ((1 << bits) < nmax) ++bits;
         order_key_kernel<<<(a.n + 255) / 256, 256, 0, stream>>>(
-            a.g, d_geom, d_cand, a.n, b.team_thr_dev, (long long)a.team_threshold,
-            bits > 8 ? bits - 8 : 0, d_key_in);
+            a.gp, d_geom, d_cand, a.n, b.team_thr_dev, (long long)a.team_threshold, d_key_in);
         sort_in = d_key_in;
         lo_bit = 0;
         hi_bit = 29;

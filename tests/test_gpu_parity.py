@@ -450,3 +450,41 @@ def test_near_ties_lattice_cloud(algo_switch):
         got = flood_sq_values(X, tri, 6, True)
         for k in range(4):
             assert np.array_equal(got[k], want[k]), (algo, k)
+
+
+def test_concurrent_host_threads_share_the_device():
+    """Four host threads value different complexes on one device at once
+    (host-memory calls on the library stream and device-memory calls on
+    their own torch streams): the grid-parameter slot the search kernels
+    read is serialised per device, so every result stays bit-exact."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    import torch
+
+    from paper_2509_22432_b200.batch import DeviceComplex, flood_sq_device
+
+    names = ["rand3d_m4", "torus10k_m20", "rand3d_m30", "dup3d_m5", "circle_m64", "rand2d_m6"]
+
+    def host_call(name):
+        z = G.load("flood", name)
+        tri = C.triangulation(z["tri_points"], G.simplices_by_dim(z))
+        subset = str(z["landmark_mode"]) == "subset"
+        sq = flood_sq_values(z["points"], tri, int(z["grid_resolution"]), subset)
+        return all(np.array_equal(np.sqrt(sq[k]), want) for k, want in G.values_by_dim(z).items())
+
+    def device_call(name):
+        z = G.load("flood", name)
+        tri = C.triangulation(z["tri_points"], G.simplices_by_dim(z))
+        dev = torch.device("cuda:0")
+        s = torch.cuda.Stream(dev)
+        with torch.cuda.stream(s):
+            X = torch.from_numpy(np.ascontiguousarray(z["points"])).to(dev)
+            dc = DeviceComplex(tri, dev)
+            got = [v.cpu().numpy() for v in flood_sq_device(X, dc, int(z["grid_resolution"]))]
+        s.synchronize()
+        return all(np.array_equal(np.sqrt(got[k]), want) for k, want in G.values_by_dim(z).items())
+
+    with ThreadPoolExecutor(4) as pool:
+        futs = [pool.submit(host_call if i % 2 else device_call, names[i % len(names)])
+                for i in range(16)]
+        assert all(f.result() for f in futs)
