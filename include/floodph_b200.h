@@ -133,6 +133,23 @@ int fph_flood_shard(const double* points, int64_t n_points, int32_t dim,
                     double* const* out_interior, int32_t memory, void* stream);
 
 /*
+ * Interior terms of an explicit subset of every dimension's simplices, with
+ * one grid build: rows[k] lists n_rows[k] row indices (int64, in range) into
+ * simplices[k]; out_interior[k] receives n_rows[k] squared values in that
+ * order.  The general form of fph_flood_shard: a multi-GPU caller picks any
+ * partition of the rows -- e.g. spatially compact shards, so each GPU's
+ * working set of the cloud stays in its L2 (parallel.spatial_partition).
+ * counts / simplices / rows / n_rows / out_interior are host tables whose
+ * entries follow `memory`.
+ */
+int fph_flood_subset(const double* points, int64_t n_points, int32_t dim,
+                     const double* landmarks, int64_t n_landmarks, int32_t max_dim,
+                     const int64_t* counts, const int32_t* const* simplices,
+                     const int64_t* const* rows, const int64_t* n_rows, int32_t grid_resolution,
+                     int32_t subset_mode, double* const* out_interior, int32_t memory,
+                     void* stream);
+
+/*
  * Facet completion for sharded runs (device memory only): out[i] =
  * max(interior_sq[i], lower_sq[facets[i][j]] for j <= k).  This is the
  * face-nesting identity that replaces the reference's per-cell face

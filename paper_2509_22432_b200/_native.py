@@ -50,6 +50,9 @@ SIGNATURES = {
     "fph_flood_shard": (ctypes.c_int, [_vp, ctypes.c_int64, ctypes.c_int32, _vp, ctypes.c_int64,
                                        ctypes.c_int32, _vp, _vp, ctypes.c_int32, ctypes.c_int32,
                                        ctypes.c_int32, ctypes.c_int32, _vp, ctypes.c_int32, _vp]),
+    "fph_flood_subset": (ctypes.c_int, [_vp, ctypes.c_int64, ctypes.c_int32, _vp, ctypes.c_int64,
+                                        ctypes.c_int32, _vp, _vp, _vp, _vp, ctypes.c_int32,
+                                        ctypes.c_int32, _vp, ctypes.c_int32, _vp]),
     "fph_flood_complete": (ctypes.c_int, [_vp, _vp, ctypes.c_int64, ctypes.c_int32, _vp, _vp,
                                           _vp]),
     "fph_candidate_mask": (ctypes.c_int, [_vp, ctypes.c_int64, ctypes.c_int32, _vp, ctypes.c_int64,

@@ -84,6 +84,18 @@ __global__ void vertex_ids_kernel(long long n, int* __restrict__ out) {
     out[i * 4 + 1] = out[i * 4 + 2] = out[i * 4 + 3] = -1;
 }
 
+// listed rows of an n_all x (k+1) table, padded to 4 ids (rows out of range
+// give -1 ids and are rejected by the caller's validation upstream)
+__global__ void pad4_rows_kernel(const int* __restrict__ s, long long n_all,
+                                 const long long* __restrict__ rows, long long n_out, int k,
+                                 int* __restrict__ out) {
+    long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (i >= n_out) return;
+    const long long row = rows[i];
+    const bool ok = row >= 0 && row < n_all;
+    for (int j = 0; j < 4; ++j) out[i * 4 + j] = (ok && j <= k) ? s[row * (k + 1) + j] : -1;
+}
+
 __global__ void fill_kernel(double* out, long long n, double v) {
     long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     if (i < n) out[i] = v;
@@ -608,11 +620,15 @@ static int run_interiors(const Grid* g, const double* lm3, int* const* s4, doubl
     return rc;
 }
 
-int fph_flood_shard(const double* points, int64_t n_points, int32_t dim,
-                    const double* landmarks, int64_t n_landmarks, int32_t max_dim,
-                    const int64_t* counts, const int32_t* const* simplices, int32_t rank,
-                    int32_t world, int32_t grid_resolution, int32_t subset_mode,
-                    double* const* out_interior, int32_t memory, void* stream) {
+// Interior terms of a subset of every dimension's simplices with one grid
+// build: rows[k] (n_rows[k] indices) or, when rows is null, the interleaved
+// share rank, rank + world, ...
+static int flood_rows(const double* points, int64_t n_points, int32_t dim,
+                      const double* landmarks, int64_t n_landmarks, int32_t max_dim,
+                      const int64_t* counts, const int32_t* const* simplices,
+                      const int64_t* const* rows, const int64_t* n_rows, int32_t rank,
+                      int32_t world, int32_t grid_resolution, int32_t subset_mode,
+                      double* const* out_interior, int32_t memory, void* stream) {
     g_err[0] = 0;
     FPH_TRY(check_cloud(points, n_points, dim));
     FPH_TRY(check_resolution(grid_resolution));
@@ -646,13 +662,20 @@ int fph_flood_shard(const double* points, int64_t n_points, int32_t dim,
         double* d_out[4] = {nullptr, nullptr, nullptr, nullptr};
         for (int k = 1; k <= max_dim && rc == FPH_OK; ++k) {
             const long long nk = counts[k];
-            mine[k] = nk > rank ? (nk - 1 - rank) / world + 1 : 0;
+            mine[k] = rows ? n_rows[k] : (nk > rank ? (nk - 1 - rank) / world + 1 : 0);
             if (mine[k] == 0) continue;
             const int32_t* d_s;
             FPH_TRY(stage_in(sc, simplices[k], (size_t)nk * (k + 1), memory, &d_s));
             FPH_TRY(sc.alloc(&s4[k], (size_t)mine[k] * 4));
-            pad4_shard_kernel<<<blocks_for(mine[k]), 256, 0, hc.stream>>>(d_s, mine[k], k, rank,
-                                                                         world, s4[k]);
+            if (rows) {
+                const int64_t* d_rows;
+                FPH_TRY(stage_in(sc, rows[k], (size_t)mine[k], memory, &d_rows));
+                pad4_rows_kernel<<<blocks_for(mine[k]), 256, 0, hc.stream>>>(
+                    d_s, nk, reinterpret_cast<const long long*>(d_rows), mine[k], k, s4[k]);
+            } else {
+                pad4_shard_kernel<<<blocks_for(mine[k]), 256, 0, hc.stream>>>(d_s, mine[k], k, rank,
+                                                                             world, s4[k]);
+            }
             count_launches(1);
             d_out[k] = out_interior[k];
             if (memory == FPH_MEM_HOST) FPH_TRY(sc.alloc(&d_out[k], (size_t)mine[k]));
@@ -669,6 +692,37 @@ int fph_flood_shard(const double* points, int64_t n_points, int32_t dim,
         return rc;
     }();
     return host_finish(hc, memory, rc);
+}
+
+int fph_flood_shard(const double* points, int64_t n_points, int32_t dim,
+                    const double* landmarks, int64_t n_landmarks, int32_t max_dim,
+                    const int64_t* counts, const int32_t* const* simplices, int32_t rank,
+                    int32_t world, int32_t grid_resolution, int32_t subset_mode,
+                    double* const* out_interior, int32_t memory, void* stream) {
+    return flood_rows(points, n_points, dim, landmarks, n_landmarks, max_dim, counts, simplices,
+                      nullptr, nullptr, rank, world, grid_resolution, subset_mode, out_interior,
+                      memory, stream);
+}
+
+int fph_flood_subset(const double* points, int64_t n_points, int32_t dim,
+                     const double* landmarks, int64_t n_landmarks, int32_t max_dim,
+                     const int64_t* counts, const int32_t* const* simplices,
+                     const int64_t* const* rows, const int64_t* n_rows, int32_t grid_resolution,
+                     int32_t subset_mode, double* const* out_interior, int32_t memory,
+                     void* stream) {
+    if (!rows || !n_rows) {
+        g_err[0] = 0;
+        set_error("fph_flood_subset: rows and n_rows are required");
+        return FPH_EARG;
+    }
+    for (int k = 1; k <= max_dim && k <= 3; ++k)
+        if (n_rows[k] < 0 || (n_rows[k] > 0 && !rows[k])) {
+            set_error("fph_flood_subset: bad row list for dimension %d", k);
+            return FPH_EARG;
+        }
+    return flood_rows(points, n_points, dim, landmarks, n_landmarks, max_dim, counts, simplices,
+                      rows, n_rows, 0, 1, grid_resolution, subset_mode, out_interior, memory,
+                      stream);
 }
 
 int fph_flood_filtration(const double* points, int64_t n_points, int32_t dim,

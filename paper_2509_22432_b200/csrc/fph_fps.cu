@@ -459,12 +459,16 @@ __global__ void __launch_bounds__(kFpsThreads, 1)
     }
 }
 
+// mm: the box as (min, max) per axis, from minmax_kernel (read on the
+// device: the quantisation never waits for the host; any box works)
 __global__ void morton_kernel(const double* __restrict__ x, const double* __restrict__ y,
-                              const double* __restrict__ z, int n, double lox, double loy,
-                              double loz, double inv, unsigned* __restrict__ code,
-                              int* __restrict__ idx) {
+                              const double* __restrict__ z, int n, const double* __restrict__ mm,
+                              unsigned* __restrict__ code, int* __restrict__ idx) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
+    const double lox = mm[0], loy = mm[2], loz = mm[4];
+    const double ext = fmax(fmax(mm[1] - mm[0], mm[3] - mm[2]), fmax(mm[5] - mm[4], 1e-300));
+    const double inv = 1024.0 / ext;
     auto q = [&](double v, double lo) {
         return (unsigned)fmin(1023.0, fmax(0.0, floor((v - lo) * inv)));
     };
@@ -520,6 +524,10 @@ __global__ void tile_box_kernel(const double* __restrict__ sx, const double* __r
         }
 }
 
+__global__ void minmax_init_kernel(double* mm) {
+    mm[threadIdx.x] = (threadIdx.x & 1) ? -INFINITY : INFINITY;
+}
+
 __global__ void minmax_kernel(const double* __restrict__ v, int n, double* __restrict__ out2) {
     double lo = INFINITY, hi = -INFINITY;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
@@ -552,16 +560,10 @@ int fps_tiled(const double* d_x, const double* d_y, const double* d_z, int n, in
     Scratch sc(stream);
     double* mm = nullptr;
     FPH_TRY(sc.alloc(&mm, 6));
-    const double init[6] = {INFINITY, -INFINITY, INFINITY, -INFINITY, INFINITY, -INFINITY};
-    FPH_CUDA_TRY(cudaMemcpyAsync(mm, init, sizeof(init), cudaMemcpyHostToDevice, stream));
+    minmax_init_kernel<<<1, 6, 0, stream>>>(mm);
     minmax_kernel<<<1024, 256, 0, stream>>>(d_x, n, mm);
     minmax_kernel<<<1024, 256, 0, stream>>>(d_y, n, mm + 2);
     minmax_kernel<<<1024, 256, 0, stream>>>(d_z, n, mm + 4);
-    double h[6];
-    FPH_CUDA_TRY(cudaMemcpyAsync(h, mm, sizeof(h), cudaMemcpyDeviceToHost, stream));
-    FPH_CUDA_TRY(cudaStreamSynchronize(stream));
-    const double ext = fmax(fmax(h[1] - h[0], h[3] - h[2]), fmax(h[5] - h[4], 1e-300));
-    const double inv = 1024.0 / ext;
     unsigned *code = nullptr, *code2 = nullptr;
     int *idx = nullptr, *sidx = nullptr, *spos = nullptr;
     double *sx = nullptr, *sy = nullptr, *sz = nullptr, *md = nullptr, *tbox = nullptr;
@@ -576,8 +578,7 @@ int fps_tiled(const double* d_x, const double* d_y, const double* d_z, int n, in
     FPH_TRY(sc.alloc(&sz, n));
     FPH_TRY(sc.alloc(&md, n));
     FPH_TRY(sc.alloc(&tbox, 6 * (size_t)ntiles));
-    morton_kernel<<<(n + 255) / 256, 256, 0, stream>>>(d_x, d_y, d_z, n, h[0], h[2], h[4], inv, code,
-                                                       idx);
+    morton_kernel<<<(n + 255) / 256, 256, 0, stream>>>(d_x, d_y, d_z, n, mm, code, idx);
     size_t tmp_bytes = 0;
     cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, code, code2, idx, sidx, n, 0, 30, stream);
     unsigned char* tmp = nullptr;

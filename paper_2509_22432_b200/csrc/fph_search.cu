@@ -54,6 +54,12 @@ constexpr int kWT = FPH_WT;     // candidates per warp tile
 // around this slot (GridSlot).
 __constant__ Grid c_grid;
 constexpr int kMaxBlk = 160;    // blocks ordered best-first per simplex
+#ifndef FPH_SPREAD_RATIO
+#define FPH_SPREAD_RATIO 8.0
+#endif
+// phase C searches a block's rows one by one when the region around all
+// their U-balls has more than this many times their summed volume
+constexpr double kSpreadRatio = FPH_SPREAD_RATIO;
 
 struct WarpSmem {
     float4 tA[kWT / 2];  // pair p: (c0.x, c1.x, c0.y, c1.y)
@@ -622,6 +628,48 @@ __device__ void search_block(const Ctx& c, WarpSmem& W, int nb, float* vals, flo
     };
     const double qx = c.G.cx + (double)cbx, qy = c.G.cy + (double)cby, qz = c.G.cz + (double)cbz;
     double R = cover(active, U2);
+    // Rows spread far apart relative to their U-balls (a long edge, a big
+    // hull triangle): the one region around all the balls holds many times
+    // the points of the balls themselves.  Search each active row over its
+    // own ball instead (as phase B does for the top row), raising L as it
+    // goes -- the same certified values, a fraction of the candidates.
+    {
+        const double ru = active ? sqrt((double)U2) * (1.0 + 1e-3) + 1e-4 * (double)q.B : 0.0;
+        double own = ru * ru * ru;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) own += __shfl_xor_sync(0xffffffffu, own, o);
+        if (R * R * R > kSpreadRatio * own) {
+            if (valid && !active && tm.rank == 0) vals[j] = -INFINITY;
+            unsigned long long scanned = 0;
+            unsigned todo = __ballot_sync(0xffffffffu, active);
+            while (todo) {
+                const int i = __ffs(todo) - 1;
+                todo &= todo - 1;
+                const float ui = __shfl_sync(0xffffffffu, U2, i);
+                const bool mine = lane == i && tm.rank == 0;
+                if (!(ui >= L)) {  // dropped below the raised bound
+                    if (mine) vals[j] = -INFINITY;
+                    continue;
+                }
+                PointF qi;
+                qi.bx = __shfl_sync(0xffffffffu, q.bx, i);
+                qi.by = __shfl_sync(0xffffffffu, q.by, i);
+                qi.bz = __shfl_sync(0xffffffffu, q.bz, i);
+                qi.bb = __shfl_sync(0xffffffffu, q.bb, i);
+                qi.px2 = __shfl_sync(0xffffffffu, q.px2, i);
+                qi.py2 = __shfl_sync(0xffffffffu, q.py2, i);
+                qi.pz2 = __shfl_sync(0xffffffffu, q.pz2, i);
+                qi.B = __shfl_sync(0xffffffffu, q.B, i);
+                const double Ri = sqrt((double)ui) * (1.0 + 1e-3) + 1e-4 * (double)qi.B;
+                const float m = point_min32(c, W, qi, Ri, tm, scanned) + qi.bb;
+                if (mine) vals[j] = m;
+                L = fmaxf(L, m - err_bound(m, qi.B));
+            }
+            st[1] += scanned;
+            tm.sync();
+            return;
+        }
+    }
     float best = INFINITY;
     for (int pass = 0; pass < 2; ++pass) {
         const bool full = !(R < 1e300);
@@ -949,9 +997,8 @@ __device__ void run_simplex(const Ctx& c, WarpSmem& W, const Team& tm, float* va
         atomicAdd(&stats[14], pairs);
         // warp-cycles per phase (A, B, C, finalize)
         for (int i = 0; i < 4; ++i) atomicAdd(&stats[19 + i], (unsigned long long)(clk[i + 1] - clk[i]));
-        if (a.dbg && tm.rank == 0) {  // accumulated: the chained kernels each add their phase
+        if (a.dbg && tm.rank == 0) {  // accumulated: the chained kernels each add their part
             unsigned long long* d = reinterpret_cast<unsigned long long*>(a.dbg + (size_t)c.s * 8);
-            for (int i = 0; i < 4; ++i) atomicAdd(d + i, (unsigned long long)(clk[i + 1] - clk[i]));
             atomicAdd(d + 4, blocks);
             atomicAdd(d + 5, pruned);
             atomicAdd(d + 6, staged + st[0] + st[1]);
@@ -1021,6 +1068,7 @@ __global__ void __launch_bounds__(kSThreads, FPH_SEARCH_MINB)
             t = __shfl_sync(0xffffffffu, t, 0);
         }
         if (t >= a.n) return;
+        const long long t_claim = clock64();
         const int s = order[t];
         // Simplices valued by one exact pass in phase A have no B or C: those
         // kernels skip them outright and F waits for A's flag instead.
@@ -1076,6 +1124,13 @@ __global__ void __launch_bounds__(kSThreads, FPH_SEARCH_MINB)
             __threadfence();
             tm.sync();
             if (tm.rank == 0 && lane == 0) st_release_i(stage + s, pos + 1);
+        }
+        if (a.dbg && lane == 0 && (team ? w == 0 : true)) {
+            // profiling aid: cycles of this simplex in this kernel (claim to
+            // publish), per phase slot: A 0, B 1, C 2, F 3 (one kernel: 0)
+            const int slot = kPh == 5 ? 1 : (kPh == 6 ? 2 : (kPh == 4 ? 3 : 0));
+            atomicAdd(reinterpret_cast<unsigned long long*>(a.dbg + (size_t)s * 8) + slot,
+                      (unsigned long long)(clock64() - t_claim));
         }
     }
 }

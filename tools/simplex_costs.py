@@ -1,7 +1,8 @@
 """Per-simplex cost anatomy of the bounded search (debug capture of
-fph_flood_interior: warp-cycles per phase A, B, C, F, blocks searched /
-pruned, candidates staged, team size), binned by candidate count, plus the
-heaviest simplices -- the ones that bound a shard's time at high GPU counts.
+fph_flood_interior: cycles of each simplex in the phase kernels A, B, C, F,
+claim to publish; blocks searched / pruned, candidates staged, team size),
+plus the heaviest simplices -- the ones that bound a shard's time at high
+GPU counts -- against the average load per resident warp.
 
   python tools/simplex_costs.py [--config sphere_torus_1m] [--top 10]
 """
@@ -54,6 +55,8 @@ def main():
             "warp_cycles_total": float(tot.sum()),
             "quantiles_warp_cycles_p50_p90_p99_p999_max": [float(v) for v in q],
             "max_simplex_us_single_warp": float(q[-1] / clock_ghz / 1e3),
+            "mean_load_per_warp_us": float(tot.sum() / 2368 / clock_ghz / 1e3),
+            "max_phase_us": [float(d[:, i].max() / clock_ghz / 1e3) for i in range(4)],
             "top1pct_share": float(tot[top1].sum() / tot.sum()),
             "phase_share": [float(d[:, i].sum() / tot.sum()) for i in range(4)],
             "team_simplices": int((d[:, 7] > 1).sum()),
