@@ -176,20 +176,36 @@ def step_single(lib, native, w, stream):
 
 
 def step_sharded(lib, native, w, stream):
-    """N > 1: this rank's interleaved share of every dimension in one
-    fph_flood_shard call (grid built once), NCCL all-gather back into row
-    order, then facet completion on every rank."""
-    import torch
+    """N > 1: this rank's spatially compact share of every dimension in one
+    fph_flood_subset call (grid built once; the shares are Morton-ordered
+    cuts of the simplex centers, computed once per complex in prepare),
+    NCCL all-gather back into row order, then facet completion on every
+    rank."""
     import torch.distributed as dist
 
-    from paper_2509_22432_b200.parallel import flood_sq_values_sharded
+    from paper_2509_22432_b200.parallel import flood_sq_values_spatial
 
     Xd, dc = w["items"][0]
-    vert_ids = torch.arange(dc.counts_full[0], dtype=torch.int32, device=dc.dev)
-    by_dim = {0: vert_ids, **dc.simp}
-    vals = flood_sq_values_sharded(Xd, dc.lm, by_dim, dc.facets, dc.top, w["m"], dist)
+    by_dim = {0: w["vert_ids"], **dc.simp}
+    vals = flood_sq_values_spatial(Xd, dc.lm, by_dim, dc.facets, dc.top, w["m"], dist, w["parts"])
     for k in range(dc.top + 1):
         dc.out[k][: vals[k].shape[0]] = vals[k]
+
+
+def shard_parts(w, world):
+    """Every rank computes the same spatial partition of each dimension's
+    simplices (parallel.spatial_partition: Morton order of the Ritter
+    centers cut into equal counts)."""
+    import torch
+
+    from paper_2509_22432_b200.parallel import simplex_centers, spatial_partition
+
+    tri, dc = w["tri"], w["items"][0][1]
+    w["vert_ids"] = torch.arange(dc.counts_full[0], dtype=torch.int32, device=dc.dev)
+    w["parts"] = {k: [torch.from_numpy(p).to(dc.dev) for p in
+                      spatial_partition(simplex_centers(tri.points, tri.simplices_by_dim[k]), None,
+                                        world)]
+                  for k in range(1, dc.top + 1)}
 
 
 def run_ours(args):
@@ -200,14 +216,24 @@ def run_ours(args):
     world, rank, local = _dist()
     torch.cuda.set_device(local)
     if world > 1 or args.force_sharded:
+        import socket
+
         import torch.distributed as dist
 
+        if "RANK" not in os.environ:  # --force-sharded without torchrun: a world of one
+            with socket.socket() as sk:
+                sk.bind(("127.0.0.1", 0))
+                port = sk.getsockname()[1]
+            os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK="0",
+                              WORLD_SIZE="1", LOCAL_RANK="0")
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
     lib = _native.require_gpu()
     w = prepare(args.config, local, rank)
     stream = torch.cuda.current_stream().cuda_stream
     sharded = (world > 1 or args.force_sharded) and not w["batch"]
     step = step_sharded if sharded else step_single
+    if sharded:
+        shard_parts(w, world)
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=w["dev"])  # > 126 MB L2
     for _ in range(args.warmup):
         step(lib, _native, w, stream)
@@ -262,7 +288,7 @@ def run_ours(args):
                            "parallelism": f"whole clouds per GPU x{world}, no collective"})
         else:
             config.update({"counts": dc0.counts_full,
-                           "parallelism": f"simplex shards x{world}, cloud replicated"})
+                           "parallelism": f"spatial simplex shards x{world}, cloud replicated"})
         result = {
             "metric": "flood-filtration simplices/s",
             "value": value,

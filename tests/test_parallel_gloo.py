@@ -140,3 +140,47 @@ def test_flood_sq_values_sharded_end_to_end(world):
         assert np.array_equal(np.asarray(results[r][0]), np.zeros(by_dim[0].shape[0]))
         for k in range(1, 4):
             assert np.array_equal(np.sqrt(np.asarray(results[r][k])), vals[k]), (r, k)
+
+
+def _worker_partitioned(rank, world, port, payload, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2509_22432_b200.parallel import gather_partitioned, spatial_partition
+
+        parts = [torch.from_numpy(p) for p in spatial_partition(payload["centers"], None, world)]
+        full = payload["values"]
+        mine = torch.from_numpy(full[parts[rank].numpy()])
+        got = gather_partitioned(mine, parts, full.shape[0], world, dist).numpy()
+        q.put((rank, bool(np.array_equal(got, full))))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_spatial_partition_gather(world):
+    """Spatially compact shards (Morton cuts of the simplex centers, the same
+    on every rank) gathered back into row order over gloo."""
+    from paper_2509_22432_b200.parallel import simplex_centers, spatial_partition
+    from tests import _golden as G
+
+    z = G.load("flood", "torus10k_m20")
+    rows = z["simplices_2"]
+    centers = simplex_centers(z["tri_points"], rows)
+    parts = spatial_partition(centers, None, world)
+    assert np.array_equal(np.sort(np.concatenate(parts)), np.arange(rows.shape[0]))
+    assert max(len(p) for p in parts) - min(len(p) for p in parts) <= 1
+    payload = {"centers": centers, "values": z["values_2"] ** 2}
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_partitioned, args=(r, world, port, payload, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    results = dict(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert all(results.values())
