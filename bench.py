@@ -320,7 +320,8 @@ def run_ours(args):
         if e2e:
             result["e2e"] = e2e
         result["roofline"] = roofline(lib, stats, ms, args.steps, clocks.summary(),
-                                      brute_pairs=brute_pairs(lib, _native, w, stream))
+                                      brute_pairs=brute_pairs(lib, _native, w, stream),
+                                      config=args.config)
         result["work_per_step"] = {"fp32_pairs": stats[0] / args.steps,
                                    "candidates_staged": stats[1] / args.steps,
                                    "candidates_scanned": stats[2] / args.steps,
@@ -348,42 +349,68 @@ def run_ours(args):
     return result
 
 
-def roofline(lib, stats, step_ms, steps, clocks, brute_pairs=None):
+def roofline(lib, stats, step_ms, steps, clocks, brute_pairs=None, config="sphere_torus_1m"):
     """Flooding kernel (search_kernel, algorithm 1): FP32-pipe bound.  Work =
     6 flop (three FMAs of |a|^2 - 2 a.b) per (sample point, candidate) pair
     actually evaluated, counted on the device; time = CUDA events around
     every flooding-kernel launch on its stream during the timed steps.
     `effective` rates the same time against the reference algorithm's pair
     count (every sample point x every cloud point of the Lemma-4.2 ball),
-    i.e. what a brute-force kernel would have had to sustain."""
+    i.e. what a brute-force kernel would have had to sustain.  DRAM traffic,
+    achieved HBM GB/s and FP32-pipe utilisation of the whole step come from
+    the committed ncu range capture of one real step (caches not flushed)."""
     pairs, pass_ms = stats[0], stats[6]
     sec = pass_ms * 1e-3
     achieved = 6.0 * pairs / sec / 1e12 if pass_ms > 0 else 0.0
     peak = float(lib.fph_fp32_peak_tflops())
     out = {"bound": "fp32", "kernel": "search_kernel", "achieved": achieved, "peak": peak,
-           "unit": "TFLOP/s", "frac": achieved / peak if peak else None, "traffic": _traffic(),
-           "traffic_note": "dram__bytes_read.sum + dram__bytes_write.sum per step over the flooding "
-                           "kernel's launches, from profiles/r01/ncu_search_full_final.json",
-           "peak_source": "measured FFMA2 microbenchmark on this GPU (fph_fp32_peak_tflops); "
-                          "MEASURED_PEAKS.json has no FP32 figure",
+           "unit": "TFLOP/s", "frac": achieved / peak if peak else None, "traffic": None,
+           "peak_source": "measured FFMA2 microbenchmark on this GPU (fph_fp32_peak_tflops, "
+                          "csrc/fph_diag.cu); MEASURED_PEAKS.json has no FP32 figure",
            "kernel_ms_per_step": pass_ms / steps, "kernel_share_of_step": pass_ms / steps / step_ms}
+    cap = _step_capture(config)
+    if cap:
+        traffic = cap["dram_bytes_per_step"]
+        peaks = _peaks()
+        cycles = step_ms * 1e-3 * 1.965e9 * 148 * 4  # SMSP-cycles in the step at max clock
+        out.update({
+            "traffic": traffic,
+            "traffic_note": "dram__bytes_read.sum + dram__bytes_write.sum of ONE whole step from "
+                            f"{cap['_path']} (ncu --replay-mode app-range, --cache-control none)",
+            "algorithmic_bytes": _algorithmic_bytes(config),
+            "hbm_gbs_achieved": traffic / (step_ms * 1e-3) / 1e9,
+            "hbm_gbs_peak": peaks.get("hbm_gbs"),
+            "hbm_frac": (traffic / (step_ms * 1e-3) / 1e9 / peaks["hbm_gbs"]) if peaks.get("hbm_gbs") else None,
+            "fp32_pipe_util": cap["sm_inst_executed_pipe_fma"] / cycles,
+            "fp32_pipe_note": "sm__inst_executed_pipe_fma of the captured step / (SMSP cycles of "
+                              "the event-timed step at 1965 MHz); ncu's own "
+                              "sm__pipe_fma_cycles_active over the (launch-gap inflated) range: "
+                              f"{cap['sm_pipe_fma_cycles_active_pct_of_range']:.1f}%",
+        })
     if brute_pairs:
         out["reference_algorithm_pairs_per_step"] = brute_pairs
         out["effective_tflops_vs_reference_algorithm"] = 6.0 * brute_pairs / (sec / steps) / 1e12
     return out
 
 
-def _traffic():
-    """DRAM bytes (read + write) per step of the flooding kernel's launches,
-    from the committed `ncu --set full` capture of this bench command
-    (profiles/r01/ncu_search_full_final.json); None if it is absent."""
-    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01",
-                        "ncu_search_full_final.json")
+def _step_capture(config):
+    path = os.path.join(ROOT, "profiles", "r02", f"ncu_step_range_{config}.json")
     try:
         with open(path) as fh:
-            return float(json.load(fh)["dram_bytes_per_step"])
-    except (OSError, KeyError, ValueError):
+            cap = json.load(fh)
+    except (OSError, ValueError):
         return None
+    cap["_path"] = os.path.relpath(path, ROOT)
+    return cap
+
+
+def _algorithmic_bytes(config):
+    """Bytes a step must move at least: read the float64 cloud once, write
+    its grid-sorted copy once, read the landmarks and complex, write the
+    values (DESIGN.md, "Roofline")."""
+    kind, n, nl, m, max_dim = CONFIGS[config]
+    dim = 2 if kind == "circle" else 3
+    return 2 * n * dim * 8
 
 
 def brute_pairs(lib, native, w, stream):
@@ -551,6 +578,26 @@ def run_profile(args):
     print("profile run done", [dc.counts_full for _, dc in w["items"]][:2])
 
 
+def run_profile_range(args):
+    import torch
+
+    from paper_2509_22432_b200 import _native
+
+    lib = _native.require_gpu()
+    w = prepare(args.config, 0)
+    stream = torch.cuda.current_stream().cuda_stream
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=w["dev"])
+    for _ in range(3):
+        step_single(lib, _native, w, stream)
+    flush.zero_()
+    torch.cuda.synchronize()
+    torch.cuda.profiler.start()
+    step_single(lib, _native, w, stream)
+    torch.cuda.synchronize()
+    torch.cuda.profiler.stop()
+    print("profile range done", [dc.counts_full for _, dc in w["items"]][:1])
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -564,11 +611,16 @@ def main():
                     help="run the multi-GPU (shard + NCCL all-gather + completion) step even at N=1")
     ap.add_argument("--profile", action="store_true",
                     help="minimal run for ncu: setup, 1 warm-up step, 1 step, no e2e/cpu")
+    ap.add_argument("--profile-range", action="store_true",
+                    help="for ncu --replay-mode app-range: warm-up steps, an L2 flush, then ONE step "
+                         "between cudaProfilerStart/Stop (the whole PDL-chained step as one range)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
     if args.profile:
         return run_profile(args)
+    if args.profile_range:
+        return run_profile_range(args)
     # stdout carries exactly one JSON line: anything libraries print there
     # (NCCL's version banner, CUDA/driver notices) goes to stderr instead
     sys.stdout.flush()
