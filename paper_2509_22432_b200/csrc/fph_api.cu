@@ -259,6 +259,23 @@ FloodTuning current_tuning() {
     return t;
 }
 
+// grid_build, timed with events when profiling is on (fph_flood_stats [23])
+int build_grid_timed(const double* d_pts, int n, int dim, cudaStream_t stream, GridStore* gs,
+                     bool keep_index = false) {
+    cudaEvent_t a = nullptr, b = nullptr;
+    if (g_profile) {
+        FPH_CUDA_TRY(cudaEventCreate(&a));
+        FPH_CUDA_TRY(cudaEventCreate(&b));
+        FPH_CUDA_TRY(cudaEventRecord(a, stream));
+    }
+    FPH_TRY(grid_build(d_pts, n, dim, 0.0, g_occupancy, stream, gs, keep_index));
+    if (g_profile) {
+        FPH_CUDA_TRY(cudaEventRecord(b, stream));
+        profile_push_grid(a, b);
+    }
+    return FPH_OK;
+}
+
 int check_resolution(int m) {
     if (m < 1 || m > kMaxResolution) {
         set_error("grid_resolution must be in [1, %d], got %d", kMaxResolution, m);
@@ -508,7 +525,7 @@ int fph_flood_interior(const double* points, int64_t n_points, int32_t dim,
         count_launches(1);
         GridStore gs;
         GridGuard gg{gs, hc.stream};
-        FPH_TRY(grid_build(d_pts, (int)n_points, dim, 0.0, g_occupancy, hc.stream, &gs));
+        FPH_TRY(build_grid_timed(d_pts, (int)n_points, dim, hc.stream, &gs));
         count_launches(4);
         double* d_out = out_sq;
         if (memory == FPH_MEM_HOST) FPH_TRY(sc.alloc(&d_out, n_simplices));
@@ -559,7 +576,7 @@ int fph_flood_samples(const double* points, int64_t n_points, int32_t dim,
         count_launches(2);
         GridStore gs;
         GridGuard gg{gs, hc.stream};
-        FPH_TRY(grid_build(d_pts, (int)n_points, dim, 0.0, g_occupancy, hc.stream, &gs));
+        FPH_TRY(build_grid_timed(d_pts, (int)n_points, dim, hc.stream, &gs));
         count_launches(4);
         double* d_out = out_sq;
         if (memory == FPH_MEM_HOST) FPH_TRY(sc.alloc(&d_out, n_simplices));
@@ -654,7 +671,7 @@ static int flood_rows(const double* points, int64_t n_points, int32_t dim,
         count_launches(1);
         GridStore gs;
         GridGuard gg{gs, hc.stream};
-        FPH_TRY(grid_build(d_pts, (int)n_points, dim, 0.0, g_occupancy, hc.stream, &gs));
+        FPH_TRY(build_grid_timed(d_pts, (int)n_points, dim, hc.stream, &gs));
         count_launches(4);
         const FloodTuning tune = current_tuning();
         int64_t mine[4] = {0, 0, 0, 0};
@@ -755,7 +772,7 @@ int fph_flood_filtration(const double* points, int64_t n_points, int32_t dim,
         count_launches(1);
         GridStore gs;
         GridGuard gg{gs, hc.stream};
-        FPH_TRY(grid_build(d_pts, (int)n_points, dim, 0.0, g_occupancy, hc.stream, &gs));
+        FPH_TRY(build_grid_timed(d_pts, (int)n_points, dim, hc.stream, &gs));
         count_launches(4);
         const FloodTuning tune = current_tuning();
         GridSlot slot;

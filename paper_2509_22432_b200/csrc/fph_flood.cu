@@ -516,10 +516,11 @@ int choose_ppt(int P) {
 }
 
 // ---------------------------------------------------------- profiling
-static std::vector<std::pair<cudaEvent_t, cudaEvent_t>> g_pass_events;
-static double g_pass_ms = 0.0;
+static std::vector<std::pair<cudaEvent_t, cudaEvent_t>> g_pass_events, g_grid_events;
+static double g_pass_ms = 0.0, g_grid_ms = 0.0;
 
 void profile_push(cudaEvent_t a, cudaEvent_t b) { g_pass_events.emplace_back(a, b); }
+void profile_push_grid(cudaEvent_t a, cudaEvent_t b) { g_grid_events.emplace_back(a, b); }
 
 int flood_stats(double* out, int reset) {
     for (auto& e : g_pass_events) {
@@ -531,14 +532,25 @@ int flood_stats(double* out, int reset) {
         cudaEventDestroy(e.second);
     }
     g_pass_events.clear();
+    for (auto& e : g_grid_events) {
+        FPH_CUDA_TRY(cudaEventSynchronize(e.second));
+        float ms = 0.f;
+        FPH_CUDA_TRY(cudaEventElapsedTime(&ms, e.first, e.second));
+        g_grid_ms += ms;
+        cudaEventDestroy(e.first);
+        cudaEventDestroy(e.second);
+    }
+    g_grid_events.clear();
     unsigned long long h[kStats];
     FPH_CUDA_TRY(cudaMemcpyFromSymbol(h, g_stats, sizeof(h)));
     for (int i = 0; i < kStats; ++i) out[i] = (double)h[i];
     out[6] = g_pass_ms;
+    out[23] = g_grid_ms;
     if (reset) {
         unsigned long long z[kStats] = {};
         FPH_CUDA_TRY(cudaMemcpyToSymbol(g_stats, z, sizeof(z)));
         g_pass_ms = 0.0;
+        g_grid_ms = 0.0;
     }
     return FPH_OK;
 }

@@ -73,6 +73,7 @@ struct FloodTuning {
 // out[0..5]: work counters (see g_stats), out[6]: pass-kernel ms
 int flood_stats(double* out, int reset);
 void profile_push(cudaEvent_t a, cudaEvent_t b);
+void profile_push_grid(cudaEvent_t a, cudaEvent_t b);
 double ffma2_peak_tflops(int device);
 // elements/s of tcgen05.ld + min over all SMs; pairs/s of the FFMA2 tile-min loop
 double tmem_min_rate(int device);

@@ -27,6 +27,7 @@
 // above is taken with it, so the result is the reference's float64 value.
 #include <cub/cub.cuh>
 
+#include <algorithm>
 #include <cstdlib>
 
 #include "fph_dev.cuh"
@@ -1000,7 +1001,7 @@ __device__ void run_simplex(const Ctx& c, WarpSmem& W, const Team& tm, float* va
         if (a.dbg && tm.rank == 0) {  // accumulated: the chained kernels each add their part
             unsigned long long* d = reinterpret_cast<unsigned long long*>(a.dbg + (size_t)c.s * 8);
             atomicAdd(d + 4, blocks);
-            atomicAdd(d + 5, pruned);
+            atomicMax(d + 5, (unsigned long long)c.cnt);  // the candidate count
             atomicAdd(d + 6, staged + st[0] + st[1]);
             atomicMax(d + 7, (unsigned long long)tm.size);
         }
@@ -1136,13 +1137,36 @@ __global__ void __launch_bounds__(kSThreads, FPH_SEARCH_MINB)
 }
 
 // Auto team threshold: a simplex is searched by a whole CTA when its
-// candidates exceed beta x (all candidates / resident warps) -- one warp
-// would otherwise still be busy with it long after the others ran dry.
+// predicted cost exceeds beta x (the whole launch's predicted cost / resident
+// warps) -- one warp would otherwise still be busy with it long after the
+// others ran dry.  Cost grows sublinearly with the candidate count C
+// (measured log-log slopes 0.24..0.52, tools/simplex_costs.py), modelled as
+// C^p; the threshold is returned in candidates: (beta sum C^p / warps)^(1/p).
 constexpr double kTeamBeta = 2.0;
 constexpr long long kTeamMin = 32768;
+#ifndef FPH_TEAM_POW
+#define FPH_TEAM_POW 1.0
+#endif
 
-__global__ void team_thr_kernel(const long long* sum, double beta, int warps, long long* thr) {
-    const double t = beta * (double)*sum / (double)(warps > 0 ? warps : 1);
+__global__ void pow_sum_kernel(const int* __restrict__ cand, int n, double p, double* sum) {
+    __shared__ double part[8];
+    double v = 0.0;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+        v += p == 1.0 ? (double)cand[i] : pow((double)cand[i], p);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t += part[i];
+        atomicAdd(sum, t);
+    }
+}
+
+__global__ void team_thr_kernel(const double* sum, double beta, double p, int warps,
+                                long long* thr) {
+    const double t = pow(beta * *sum / (double)(warps > 0 ? warps : 1), 1.0 / p);
     *thr = t > (double)kTeamMin ? (long long)t : kTeamMin;
 }
 
@@ -1242,17 +1266,18 @@ int launch_search(const FloodArgs& a, const SimplexGeom* d_geom, const int* d_ca
     b.lower = d_lower;
     b.wt_off = (int)(sv ? kSmemVals : sizeof(SearchSmem));
     long long* d_thr = nullptr;
-    void* tmp2 = nullptr;
     if (a.team_threshold <= 0) {
         // threshold from the total candidate count, computed on the device so
         // the concurrent streams never wait for the host
         const double beta = a.team_threshold < 0 ? -a.team_threshold / 100.0 : kTeamBeta;
+        static const double team_pow =
+            getenv("FPH_TEAM_POW") ? atof(getenv("FPH_TEAM_POW")) : FPH_TEAM_POW;
         FPH_CUDA_TRY(cudaMallocAsync(&d_thr, 2 * sizeof(long long), stream));
-        size_t tb = 0;
-        cub::DeviceReduce::Sum(nullptr, tb, d_cand, d_thr + 1, a.n, stream);
-        FPH_CUDA_TRY(cudaMallocAsync(&tmp2, tb, stream));
-        FPH_CUDA_TRY(cub::DeviceReduce::Sum(tmp2, tb, d_cand, d_thr + 1, a.n, stream));
-        team_thr_kernel<<<1, 1, 0, stream>>>(d_thr + 1, beta, blocks * kSW, d_thr);
+        double* d_sum = reinterpret_cast<double*>(d_thr + 1);
+        FPH_CUDA_TRY(cudaMemsetAsync(d_sum, 0, sizeof(double), stream));
+        pow_sum_kernel<<<std::min(148, (a.n + 255) / 256), 256, 0, stream>>>(d_cand, a.n, team_pow,
+                                                                          d_sum);
+        team_thr_kernel<<<1, 1, 0, stream>>>(d_sum, beta, team_pow, blocks * kSW, d_thr);
         b.team_thr_dev = d_thr;
     }
     // order: FPH_ORDER=0 (environment) sorts by candidate count alone,
@@ -1309,10 +1334,7 @@ int launch_search(const FloodArgs& a, const SimplexGeom* d_geom, const int* d_ca
     FPH_CUDA_TRY(cudaFreeAsync(d_counters, stream));
     if (d_stage) FPH_CUDA_TRY(cudaFreeAsync(d_stage, stream));
     if (d_lower) FPH_CUDA_TRY(cudaFreeAsync(d_lower, stream));
-    if (d_thr) {
-        FPH_CUDA_TRY(cudaFreeAsync(d_thr, stream));
-        FPH_CUDA_TRY(cudaFreeAsync(tmp2, stream));
-    }
+    if (d_thr) FPH_CUDA_TRY(cudaFreeAsync(d_thr, stream));
     FPH_CUDA_TRY(cudaGetLastError());
     for (void* p : {(void*)d_keys, (void*)d_order, (void*)d_iota, tmp})
         FPH_CUDA_TRY(cudaFreeAsync(p, stream));

@@ -64,6 +64,8 @@ def main():
     lib = _native.require_gpu()
     stats = np.zeros(24)
 
+    grid_ms = []
+
     def interiors_ms(fn, keep=None):
         """(call ms, fork-to-join ms of the interior kernels inside it)"""
         lib.fph_set_profiling(1)
@@ -73,6 +75,7 @@ def main():
         lib.fph_set_profiling(0)
         if keep is not None:
             keep.append(out)
+        grid_ms.append(stats[23] / (args.reps + 1))
         return t, stats[6] / (args.reps + 1)
 
     t1, _ = timed(lambda: flood_sq_device(Xd, dc, w["m"]))
@@ -132,6 +135,7 @@ def main():
     print(json.dumps({"config": args.config, "simplices": dc.n_simplices, "single_gpu_ms": t1,
                       "single_call_interiors_ms": one_int, "fixed_share_ms": fixed,
                       "fixed_share_interiors_ms": fixed_int,
+                      "grid_build_ms": grid_ms[0] if grid_ms else None,
                       "gather_us_assumed": GATHER_US, "worlds": rows}))
 
 

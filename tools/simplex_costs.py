@@ -5,6 +5,9 @@ plus the heaviest simplices -- the ones that bound a shard's time at high
 GPU counts -- against the average load per resident warp.
 
   python tools/simplex_costs.py [--config sphere_torus_1m] [--top 10]
+
+(record fields: cycles A, B, C, F; blocks searched; candidate count;
+candidates staged; team size)
 """
 
 import argparse
@@ -60,9 +63,17 @@ def main():
             "top1pct_share": float(tot[top1].sum() / tot.sum()),
             "phase_share": [float(d[:, i].sum() / tot.sum()) for i in range(4)],
             "team_simplices": int((d[:, 7] > 1).sum()),
+            "cost_vs_cand_loglog_slope": float(np.polyfit(np.log(np.maximum(d[:, 5], 1)),
+                                                          np.log(np.maximum(tot, 1)), 1)[0]),
+            "cost_per_cand_by_cand_decile": [
+                float(np.median(tot[(d[:, 5] >= lo) & (d[:, 5] <= hi)] /
+                                np.maximum(d[(d[:, 5] >= lo) & (d[:, 5] <= hi), 5], 1)))
+                for lo, hi in zip(np.quantile(d[:, 5], np.linspace(0, 0.9, 10)),
+                                  np.quantile(d[:, 5], np.linspace(0.1, 1.0, 10)))],
+            "heaviest_cand_rank_pct": [float((d[:, 5] < d[i, 5]).mean() * 100) for i in order[:10]],
             "heaviest": [{"row": int(i), "warp_cycles": float(tot[i]),
                           "phases": [int(v) for v in d[i, :4]], "blocks": int(d[i, 4]),
-                          "pruned": int(d[i, 5]), "staged": int(staged[i]), "team": int(d[i, 7])}
+                          "cand": int(d[i, 5]), "staged": int(staged[i]), "team": int(d[i, 7])}
                          for i in order[: args.top]],
         }
     print(json.dumps(out, indent=1))
