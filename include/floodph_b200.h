@@ -237,10 +237,13 @@ int fph_set_profiling(int32_t on);
 int fph_flood_stats(double* out, int32_t reset);
 
 /*
- * Profiling aid: enable (1) / disable (0) per-simplex capture in the
- * bounded search; out (cap int64s) receives the last flood_interior call's
- * 8 values per simplex (cycles of phases A, B, C, finalize; blocks
- * searched; blocks pruned; candidates staged; team size), n their count.
+ * Profiling aid.  n != NULL: first waits for the device and returns the
+ * capture so far in out (cap int64s; out NULL: size only, *n = values
+ * available) as blocks [k, count, count x 16 values], one block per flooding
+ * launch; then enable (1, clearing the capture) / disable (0) capturing.
+ * Per simplex: cycles in the phase kernels A, B, C, F (claim to publish);
+ * blocks searched; candidate count; candidates staged; team size; global
+ * timer (ns) start and end in A, B, C, F.
  */
 int fph_debug_simplex_cycles(int32_t enable, int64_t* out, int64_t cap, int64_t* n);
 

@@ -378,12 +378,13 @@ double fph_tilemin_rate(void) {
 }
 
 int fph_debug_simplex_cycles(int32_t enable, int64_t* out, int64_t cap, int64_t* n) {
-    debug_enable(enable != 0);
-    if (out && n) {
+    g_err[0] = 0;
+    if (n) {  // fetch first (waits for the device), then switch
         long long nn = 0;
-        debug_fetch(reinterpret_cast<long long*>(out), cap, &nn);
+        FPH_TRY(debug_fetch(reinterpret_cast<long long*>(out), out ? cap : 0, &nn));
         *n = nn;
     }
+    debug_enable(enable != 0);
     return FPH_OK;
 }
 

@@ -555,12 +555,38 @@ int flood_stats(double* out, int reset) {
     return FPH_OK;
 }
 
+// Debug capture (profiling aid): per flood_range launch with the search
+// kernels, kDbgFields values per simplex (search_kernel fills them); the
+// device buffers are kept until debug_fetch, which waits for the device and
+// returns blocks [k, n, n x kDbgFields values] -- no stream sync in between,
+// so the captured run keeps its concurrency.
+struct DebugRec {
+    long long* d;
+    int n, k;
+};
 static bool g_debug = false;
+static std::vector<DebugRec> g_debug_pending;
 static std::vector<long long> g_debug_buf;
-void debug_enable(bool on) { g_debug = on; }
+void debug_enable(bool on) {
+    g_debug = on;
+    if (on) g_debug_buf.clear();
+}
 int debug_fetch(long long* out, long long cap, long long* n) {
+    if (!g_debug_pending.empty()) {
+        FPH_CUDA_TRY(cudaDeviceSynchronize());
+        for (const DebugRec& r : g_debug_pending) {
+            const size_t base = g_debug_buf.size();
+            g_debug_buf.resize(base + 2 + (size_t)kDbgFields * r.n);
+            g_debug_buf[base] = r.k;
+            g_debug_buf[base + 1] = r.n;
+            FPH_CUDA_TRY(cudaMemcpy(g_debug_buf.data() + base + 2, r.d,
+                                    sizeof(long long) * kDbgFields * r.n, cudaMemcpyDeviceToHost));
+            FPH_CUDA_TRY(cudaFree(r.d));
+        }
+        g_debug_pending.clear();
+    }
     *n = (long long)g_debug_buf.size();
-    std::copy(g_debug_buf.begin(), g_debug_buf.begin() + std::min<long long>(cap, *n), out);
+    if (out) std::copy(g_debug_buf.begin(), g_debug_buf.begin() + std::min<long long>(cap, *n), out);
     return FPH_OK;
 }
 
@@ -686,12 +712,33 @@ long long interior_rows(int k, int m) {
 // per-point fp32 scratch per chunk of simplices (n x P floats)
 constexpr double kPerpointBudget = 2.0 * (1 << 30);
 
-int flood_range(const Grid* d_grid, const double* d_landmarks3, const int* d_simplices, int n, int k,
-                int m, int subset, double* d_out_sq, const FloodTuning& tune, cudaStream_t stream,
-                const double* d_explicit, const Template& T) {
-    const int P = T.P;
-    const int ppt = choose_ppt(P);
+// One chunk of simplices of one dimension, queued in two steps
+// (range_prepare: allocations, setup_kernel, the search set-up; range_run:
+// the flooding kernels and the frees).
+struct RangePlan {
     FloodArgs a{};
+    bool search = false, profile = false;
+    int ppt = 1;
+    cudaStream_t stream = nullptr;
+    SimplexGeom* d_geom = nullptr;
+    int *d_ntasks = nullptr, *d_task_off = nullptr, *d_counter = nullptr, *d_done = nullptr;
+    int* d_cand = nullptr;
+    float* d_perpoint = nullptr;
+    void* tmp = nullptr;
+    SearchPlan sp;
+};
+
+int range_prepare(const Grid* d_grid, const double* d_landmarks3, const int* d_simplices, int n,
+                  int k, int m, int subset, double* d_out_sq, const FloodTuning& tune,
+                  cudaStream_t stream, const double* d_explicit, const Template& T,
+                  RangePlan* plan) {
+    RangePlan& rp = *plan;
+    rp = RangePlan{};
+    rp.stream = stream;
+    rp.profile = tune.profile;
+    const int P = T.P;
+    rp.ppt = choose_ppt(P);
+    FloodArgs& a = rp.a;
     a.gp = d_grid;
     a.landmarks = d_landmarks3;
     a.simplices = d_simplices;
@@ -700,14 +747,14 @@ int flood_range(const Grid* d_grid, const double* d_landmarks3, const int* d_sim
     a.m = m;
     a.P = P;
     a.subset = subset;
-    a.chunk_pts = kThreads * ppt;
+    a.chunk_pts = kThreads * rp.ppt;
     a.pairs_per_task = tune.pairs_per_task > 0 ? tune.pairs_per_task : (double)(1 << 21);
     a.out_sq = d_out_sq;
     a.explicit_pts = d_explicit;
     // the bounded search keeps the (m + 1) weights in shared memory; a
     // resolution too large for that takes the brute-force kernel
-    const bool search = tune.algo >= 1 && search_smem_bytes(P, m) <= search_smem_limit();
-    a.nblk = search ? T.nblk : 0;
+    rp.search = tune.algo >= 1 && search_smem_bytes(P, m) <= search_smem_limit();
+    a.nblk = rp.search ? T.nblk : 0;
     a.reps_target = tune.reps_target > 0 ? tune.reps_target : 384;
     a.team_threshold = tune.team_threshold;
     a.team_thr_dev = nullptr;
@@ -716,94 +763,98 @@ int flood_range(const Grid* d_grid, const double* d_landmarks3, const int* d_sim
     a.tmpl = T.rows;
     a.blk_off = T.blk_off;
 
-    SimplexGeom* d_geom = nullptr;
-    int *d_ntasks = nullptr, *d_task_off = nullptr, *d_counter = nullptr, *d_done = nullptr;
-    float* d_perpoint = nullptr;
-    FPH_CUDA_TRY(cudaMallocAsync(&d_geom, sizeof(SimplexGeom) * n, stream));
-    FPH_CUDA_TRY(cudaMallocAsync(&d_ntasks, sizeof(int) * (n + 1), stream));
-    FPH_CUDA_TRY(cudaMallocAsync(&d_task_off, sizeof(int) * (n + 1), stream));
-    FPH_CUDA_TRY(cudaMallocAsync(&d_counter, sizeof(int), stream));
-    FPH_CUDA_TRY(cudaMallocAsync(&d_done, sizeof(int) * n, stream));
-    FPH_CUDA_TRY(cudaMallocAsync(&d_perpoint, sizeof(float) * (size_t)n * P, stream));
-    FPH_CUDA_TRY(cudaMemsetAsync(d_counter, 0, sizeof(int), stream));
-    FPH_CUDA_TRY(cudaMemsetAsync(d_done, 0, sizeof(int) * n, stream));
-    FPH_CUDA_TRY(cudaMemsetAsync(d_ntasks + n, 0, sizeof(int), stream));
+    FPH_CUDA_TRY(cudaMallocAsync(&rp.d_geom, sizeof(SimplexGeom) * n, stream));
+    FPH_CUDA_TRY(cudaMallocAsync(&rp.d_ntasks, sizeof(int) * (n + 1), stream));
+    FPH_CUDA_TRY(cudaMallocAsync(&rp.d_task_off, sizeof(int) * (n + 1), stream));
+    FPH_CUDA_TRY(cudaMallocAsync(&rp.d_counter, sizeof(int), stream));
+    FPH_CUDA_TRY(cudaMallocAsync(&rp.d_done, sizeof(int) * n, stream));
+    FPH_CUDA_TRY(cudaMallocAsync(&rp.d_perpoint, sizeof(float) * (size_t)n * P, stream));
+    FPH_CUDA_TRY(cudaMemsetAsync(rp.d_counter, 0, sizeof(int), stream));
+    FPH_CUDA_TRY(cudaMemsetAsync(rp.d_done, 0, sizeof(int) * n, stream));
+    FPH_CUDA_TRY(cudaMemsetAsync(rp.d_ntasks + n, 0, sizeof(int), stream));
     const long long npp = (long long)n * P;
-    if (!search)
+    if (!rp.search)
         init_perpoint_kernel<<<(unsigned)((npp + 255) / 256), 256, 0, stream>>>(
-            reinterpret_cast<unsigned*>(d_perpoint), npp);
-    int* d_cand = nullptr;
-    if (search) FPH_CUDA_TRY(cudaMallocAsync(&d_cand, sizeof(int) * n, stream));
-    a.cand_count = d_cand;
+            reinterpret_cast<unsigned*>(rp.d_perpoint), npp);
+    if (rp.search) FPH_CUDA_TRY(cudaMallocAsync(&rp.d_cand, sizeof(int) * n, stream));
+    a.cand_count = rp.d_cand;
     FPH_CUDA_TRY(cudaGetSymbolAddress((void**)&a.stats, g_stats));
-    a.perpoint = d_perpoint;
+    a.perpoint = rp.d_perpoint;
 
-    setup_kernel<<<(n * 32 + 255) / 256, 256, 0, stream>>>(a, d_geom, d_ntasks);
-    void* tmp = nullptr;
-    if (!search) {
+    setup_kernel<<<(n * 32 + 255) / 256, 256, 0, stream>>>(a, rp.d_geom, rp.d_ntasks);
+    if (!rp.search) {
         size_t tmp_bytes = 0;
-        cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, d_ntasks, d_task_off, n + 1, stream);
-        FPH_CUDA_TRY(cudaMallocAsync(&tmp, tmp_bytes, stream));
-        FPH_CUDA_TRY(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, d_ntasks, d_task_off, n + 1,
-                                                   stream));
+        cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, rp.d_ntasks, rp.d_task_off, n + 1, stream);
+        FPH_CUDA_TRY(cudaMallocAsync(&rp.tmp, tmp_bytes, stream));
+        FPH_CUDA_TRY(cub::DeviceScan::ExclusiveSum(rp.tmp, tmp_bytes, rp.d_ntasks, rp.d_task_off,
+                                                   n + 1, stream));
     }
+    long long* d_dbg = nullptr;
+    if (rp.search && g_debug) {
+        FPH_CUDA_TRY(cudaMalloc(&d_dbg, sizeof(long long) * kDbgFields * n));
+        FPH_CUDA_TRY(cudaMemsetAsync(d_dbg, 0, sizeof(long long) * kDbgFields * n, stream));
+        g_debug_pending.push_back({d_dbg, n, k});
+    }
+    a.dbg = d_dbg;
+    if (rp.search) FPH_TRY(search_prepare(a, rp.d_geom, a.cand_count, stream, &rp.sp));
+    FPH_CUDA_TRY(cudaGetLastError());
+    return FPH_OK;
+}
 
-    int dev = 0, sms = 0, occ = 0;
+int range_run(RangePlan& rp) {
+    cudaStream_t stream = rp.stream;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
-    if (tune.profile) {
+    if (rp.profile) {
         FPH_CUDA_TRY(cudaEventCreate(&ev0));
         FPH_CUDA_TRY(cudaEventCreate(&ev1));
         FPH_CUDA_TRY(cudaEventRecord(ev0, stream));
     }
-    FPH_CUDA_TRY(cudaGetDevice(&dev));
-    FPH_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    long long* d_dbg = nullptr;
-    if (search && g_debug) {
-        FPH_CUDA_TRY(cudaMallocAsync(&d_dbg, sizeof(long long) * 8 * n, stream));
-        FPH_CUDA_TRY(cudaMemsetAsync(d_dbg, 0, sizeof(long long) * 8 * n, stream));
-    }
-    a.dbg = d_dbg;
-    if (search) {
-        FPH_TRY(launch_search(a, d_geom, a.cand_count, stream));
-        if (d_dbg) {
-            g_debug_buf.assign((size_t)8 * n, 0);
-            FPH_CUDA_TRY(cudaMemcpyAsync(g_debug_buf.data(), d_dbg, sizeof(long long) * 8 * n,
-                                         cudaMemcpyDeviceToHost, stream));
-            FPH_CUDA_TRY(cudaStreamSynchronize(stream));
-            FPH_CUDA_TRY(cudaFreeAsync(d_dbg, stream));
-        }
-    } else switch (ppt) {
+    if (rp.search) {
+        FPH_TRY(search_run(rp.sp, true));
+    } else {
+        int dev = 0, sms = 0, occ = 0;
+        FPH_CUDA_TRY(cudaGetDevice(&dev));
+        FPH_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        const FloodArgs& a = rp.a;
+        switch (rp.ppt) {
 #define FPH_LAUNCH(PPTV)                                                                     \
     case PPTV:                                                                               \
         FPH_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pass_kernel<PPTV>,  \
                                                                    kThreads, 0));            \
         pass_kernel<PPTV><<<sms * (occ > 0 ? occ : 1), kThreads, 0, stream>>>(               \
-            a, d_geom, d_task_off, d_counter, d_done);                                       \
+            a, rp.d_geom, rp.d_task_off, rp.d_counter, rp.d_done);                           \
         break;
-        FPH_LAUNCH(1)
-        FPH_LAUNCH(2)
-        FPH_LAUNCH(4)
-        FPH_LAUNCH(8)
+            FPH_LAUNCH(1)
+            FPH_LAUNCH(2)
+            FPH_LAUNCH(4)
+            FPH_LAUNCH(8)
 #undef FPH_LAUNCH
+        }
     }
     FPH_CUDA_TRY(cudaGetLastError());
-    if (tune.profile) {
+    if (rp.profile) {
         FPH_CUDA_TRY(cudaEventRecord(ev1, stream));
         profile_push(ev0, ev1);
     }
-    for (void* p : {(void*)d_geom, (void*)d_ntasks, (void*)d_task_off, (void*)d_counter,
-                    (void*)d_done, (void*)d_perpoint})
-        FPH_CUDA_TRY(cudaFreeAsync(p, stream));
-    if (tmp) FPH_CUDA_TRY(cudaFreeAsync(tmp, stream));
-    if (d_cand) FPH_CUDA_TRY(cudaFreeAsync(d_cand, stream));
+    for (void* p : {(void*)rp.d_geom, (void*)rp.d_ntasks, (void*)rp.d_task_off,
+                    (void*)rp.d_counter, (void*)rp.d_done, (void*)rp.d_perpoint, rp.tmp,
+                    (void*)rp.d_cand})
+        if (p) FPH_CUDA_TRY(cudaFreeAsync(p, stream));
+    rp = RangePlan{};
     return FPH_OK;
 }
 
 }  // namespace
 
-int flood_interior(const Grid* d_grid, const double* d_landmarks3, const int* d_simplices, int n,
-                   int k, int m, int subset, double* d_out_sq, const FloodTuning& tune,
-                   cudaStream_t stream, const double* d_explicit, int explicit_rows) {
+struct FloodJob {
+    std::vector<RangePlan> ranges;
+};
+
+int flood_interior_prepare(const Grid* d_grid, const double* d_landmarks3, const int* d_simplices,
+                           int n, int k, int m, int subset, double* d_out_sq,
+                           const FloodTuning& tune, cudaStream_t stream, FloodJob** job,
+                           const double* d_explicit, int explicit_rows) {
+    *job = nullptr;
     if (n == 0) return FPH_OK;
     if (d_explicit && explicit_rows < 1) {
         set_error("flood_interior: explicit samples need at least one row per simplex");
@@ -827,16 +878,50 @@ int flood_interior(const Grid* d_grid, const double* d_landmarks3, const int* d_
     Template T;
     FPH_TRY(get_template(k, m, d_explicit ? explicit_rows : 0, &T));
     // simplices in chunks whose per-row scratch fits the budget (only very
-    // high resolutions ever need more than one)
+    // high resolutions ever need more than one; their chunks run in turn)
     const long long chunk =
         std::max(1ll, std::min((long long)n, (long long)(kPerpointBudget / (4.0 * T.P))));
+    FloodJob* jb = new FloodJob;
     for (long long off = 0; off < n; off += chunk) {
         const int cnt = (int)std::min(chunk, n - off);
-        FPH_TRY(flood_range(d_grid, d_landmarks3, d_simplices + off * 4, cnt, k, m, subset,
-                            d_out_sq + off, tune, stream,
-                            d_explicit ? d_explicit + off * (long long)T.P * 3 : nullptr, T));
+        jb->ranges.emplace_back();
+        const int rc = range_prepare(d_grid, d_landmarks3, d_simplices + off * 4, cnt, k, m, subset,
+                                     d_out_sq + off, tune, stream,
+                                     d_explicit ? d_explicit + off * (long long)T.P * 3 : nullptr,
+                                     T, &jb->ranges.back());
+        if (rc != FPH_OK) {
+            delete jb;
+            return rc;
+        }
+        if (off + chunk < n) {  // later chunks reuse nothing: run this one now
+            const int rr = range_run(jb->ranges.back());
+            if (rr != FPH_OK) {
+                delete jb;
+                return rr;
+            }
+            jb->ranges.pop_back();
+        }
     }
+    *job = jb;
     return FPH_OK;
+}
+
+int flood_interior_run(FloodJob* job) {
+    if (!job) return FPH_OK;
+    int rc = FPH_OK;
+    for (RangePlan& rp : job->ranges)
+        if (rc == FPH_OK) rc = range_run(rp);
+    delete job;
+    return rc;
+}
+
+int flood_interior(const Grid* d_grid, const double* d_landmarks3, const int* d_simplices, int n,
+                   int k, int m, int subset, double* d_out_sq, const FloodTuning& tune,
+                   cudaStream_t stream, const double* d_explicit, int explicit_rows) {
+    FloodJob* job = nullptr;
+    FPH_TRY(flood_interior_prepare(d_grid, d_landmarks3, d_simplices, n, k, m, subset, d_out_sq,
+                                   tune, stream, &job, d_explicit, explicit_rows));
+    return flood_interior_run(job);
 }
 
 // value(s) = max(interior(s), max_j value(facet_j(s))) -- the face-nesting

@@ -45,11 +45,34 @@ struct FloodArgs {
     long long exact_cand[4];  // bounded search: exact pass when candidates <= this, per dim
 };
 
-// debug capture of the last flood_interior call (per-simplex phase cycles)
+// debug capture of flood_interior calls (per-simplex phase cycles, times):
+// per simplex [cycles A, B, C, F; blocks; candidates; staged; team size;
+// globaltimer start, end of A, B, C, F]
+constexpr int kDbgFields = 16;
 void debug_enable(bool on);
 int debug_fetch(long long* out, long long cap, long long* n);
 
-// algorithm 1 (fph_search.cu): warp-per-simplex bounded search
+// algorithm 1 (fph_search.cu): warp-per-simplex bounded search.  Queued in
+// two steps so a caller can put every dimension's set-up (team threshold,
+// schedule sort) on the GPU before any dimension's persistent search kernels
+// take the SMs: search_prepare, then search_run.
+using SearchKernelFn = void (*)(const FloodArgs, const SimplexGeom*, const int*, int*, int*, int);
+struct SearchPlan {
+    FloodArgs b{};
+    const SimplexGeom* d_geom = nullptr;
+    cudaStream_t stream = nullptr;
+    SearchKernelFn kern[4] = {nullptr, nullptr, nullptr, nullptr};
+    int nk = 0, blocks = 0, smem = 0;
+    float* d_lower = nullptr;
+    long long* d_thr = nullptr;
+    int *d_keys = nullptr, *d_order = nullptr, *d_iota = nullptr, *d_key_in = nullptr;
+    int *d_counters = nullptr, *d_stage = nullptr;
+    void* tmp = nullptr;
+};
+int search_prepare(const FloodArgs& a, const SimplexGeom* d_geom, const int* d_cand,
+                   cudaStream_t stream, SearchPlan* plan);
+int search_run(SearchPlan& plan, bool release);
+int search_release(SearchPlan& plan);
 int launch_search(const FloodArgs& a, const SimplexGeom* d_geom, const int* d_cand,
                   cudaStream_t stream);
 // copy a device grid's parameters into the search kernels' constant slot,
@@ -80,6 +103,18 @@ double tmem_min_rate(int device);
 double tilemin_rate(int device);
 
 int choose_ppt(int P);
+
+// The same in two steps: prepare queues the allocations, the setup kernel
+// and the schedule sort; run queues the flooding kernels and frees.  (Queuing
+// every dimension's set-up first, and all dimensions' kernels as one PDL chain
+// on one stream, were both measured: no gain over concurrent per-dimension
+// streams, docs/experiments.md.)
+struct FloodJob;
+int flood_interior_prepare(const Grid* d_grid, const double* d_landmarks3, const int* d_simplices,
+                           int n, int k, int m, int subset, double* d_out_sq,
+                           const FloodTuning& tune, cudaStream_t stream, FloodJob** job,
+                           const double* d_explicit = nullptr, int explicit_rows = 0);
+int flood_interior_run(FloodJob* job);
 
 // Squared flood value over the relative-interior grid rows of every
 // simplex (k = 0: the vertex itself), exactly as the reference computes it.

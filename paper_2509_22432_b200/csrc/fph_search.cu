@@ -61,6 +61,11 @@ constexpr int kMaxBlk = 160;    // blocks ordered best-first per simplex
 // phase C searches a block's rows one by one when the region around all
 // their U-balls has more than this many times their summed volume
 constexpr double kSpreadRatio = FPH_SPREAD_RATIO;
+#ifndef FPH_SAMPLE_PASSES
+#define FPH_SAMPLE_PASSES 1
+#endif
+// phase C: sampling passes a large block region may get before its exact pass
+constexpr int kSamplePasses = FPH_SAMPLE_PASSES;
 
 struct WarpSmem {
     float4 tA[kWT / 2];  // pair p: (c0.x, c1.x, c0.y, c1.y)
@@ -672,6 +677,7 @@ __device__ void search_block(const Ctx& c, WarpSmem& W, int nb, float* vals, flo
         }
     }
     float best = INFINITY;
+    int samples = 0;
     for (int pass = 0; pass < 2; ++pass) {
         const bool full = !(R < 1e300);
         const double Rrow = full ? 1e301 : R * (1.0 + 1e-4) + 1e-5 * (cbn + R) + c_grid.margin;
@@ -760,6 +766,9 @@ __device__ void search_block(const Ctx& c, WarpSmem& W, int nb, float* vals, flo
                 active = active && U2 >= L;
                 if (!__any_sync(0xffffffffu, active)) break;
                 R = cover(active, U2);
+                // the tightened balls may still span a large region: count
+                // and sample it again before the exact pass
+                if (++samples < kSamplePasses) pass = -1;
             }
             continue;
         }
@@ -999,7 +1008,7 @@ __device__ void run_simplex(const Ctx& c, WarpSmem& W, const Team& tm, float* va
         // warp-cycles per phase (A, B, C, finalize)
         for (int i = 0; i < 4; ++i) atomicAdd(&stats[19 + i], (unsigned long long)(clk[i + 1] - clk[i]));
         if (a.dbg && tm.rank == 0) {  // accumulated: the chained kernels each add their part
-            unsigned long long* d = reinterpret_cast<unsigned long long*>(a.dbg + (size_t)c.s * 8);
+            unsigned long long* d = reinterpret_cast<unsigned long long*>(a.dbg + (size_t)c.s * kDbgFields);
             atomicAdd(d + 4, blocks);
             atomicMax(d + 5, (unsigned long long)c.cnt);  // the candidate count
             atomicAdd(d + 6, staged + st[0] + st[1]);
@@ -1070,6 +1079,8 @@ __global__ void __launch_bounds__(kSThreads, FPH_SEARCH_MINB)
         }
         if (t >= a.n) return;
         const long long t_claim = clock64();
+        long long g_claim = 0;
+        if (a.dbg) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_claim));
         const int s = order[t];
         // Simplices valued by one exact pass in phase A have no B or C: those
         // kernels skip them outright and F waits for A's flag instead.
@@ -1128,10 +1139,16 @@ __global__ void __launch_bounds__(kSThreads, FPH_SEARCH_MINB)
         }
         if (a.dbg && lane == 0 && (team ? w == 0 : true)) {
             // profiling aid: cycles of this simplex in this kernel (claim to
-            // publish), per phase slot: A 0, B 1, C 2, F 3 (one kernel: 0)
+            // publish) and its global-timer interval, per phase slot: A 0,
+            // B 1, C 2, F 3 (one kernel: 0)
             const int slot = kPh == 5 ? 1 : (kPh == 6 ? 2 : (kPh == 4 ? 3 : 0));
-            atomicAdd(reinterpret_cast<unsigned long long*>(a.dbg + (size_t)s * 8) + slot,
+            long long* d = a.dbg + (size_t)s * kDbgFields;
+            atomicAdd(reinterpret_cast<unsigned long long*>(d) + slot,
                       (unsigned long long)(clock64() - t_claim));
+            unsigned long long t_end;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
+            d[8 + 2 * slot] = g_claim;
+            d[9 + 2 * slot] = (long long)t_end;
         }
     }
 }
@@ -1147,26 +1164,49 @@ constexpr long long kTeamMin = 32768;
 #ifndef FPH_TEAM_POW
 #define FPH_TEAM_POW 1.0
 #endif
+#ifndef FPH_TEAM_GAMMA
+#define FPH_TEAM_GAMMA 0.0
+#endif
 
+// sum of C^p (sum[0]) and the largest C (as a double in sum[1])
 __global__ void pow_sum_kernel(const int* __restrict__ cand, int n, double p, double* sum) {
     __shared__ double part[8];
+    __shared__ int mpart[8];
     double v = 0.0;
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    int mx = 0;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
         v += p == 1.0 ? (double)cand[i] : pow((double)cand[i], p);
+        mx = max(mx, cand[i]);
+    }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = v;
+    for (int o = 16; o > 0; o >>= 1) {
+        v += __shfl_xor_sync(0xffffffffu, v, o);
+        mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+        part[threadIdx.x >> 5] = v;
+        mpart[threadIdx.x >> 5] = mx;
+    }
     __syncthreads();
     if (threadIdx.x == 0) {
         double t = 0.0;
-        for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t += part[i];
+        int m = 0;
+        for (int i = 0; i < (int)(blockDim.x >> 5); ++i) {
+            t += part[i];
+            m = max(m, mpart[i]);
+        }
         atomicAdd(sum, t);
+        atomicMax(reinterpret_cast<int*>(sum + 1), m);
     }
 }
 
-__global__ void team_thr_kernel(const double* sum, double beta, double p, int warps,
+// gamma > 0 also gives a team to every simplex above gamma x the largest
+// count: the few heaviest simplices bound a launch's critical path
+__global__ void team_thr_kernel(const double* sum, double beta, double p, double gamma, int warps,
                                 long long* thr) {
-    const double t = pow(beta * *sum / (double)(warps > 0 ? warps : 1), 1.0 / p);
+    double t = pow(beta * sum[0] / (double)(warps > 0 ? warps : 1), 1.0 / p);
+    const int mx = *reinterpret_cast<const int*>(sum + 1);
+    if (gamma > 0.0) t = fmin(t, gamma * (double)mx);
     *thr = t > (double)kTeamMin ? (long long)t : kTeamMin;
 }
 
@@ -1229,13 +1269,17 @@ size_t search_smem_limit() {
     return (size_t)lim;
 }
 
-int launch_search(const FloodArgs& a, const SimplexGeom* d_geom, const int* d_cand,
-                  cudaStream_t stream) {
+int search_prepare(const FloodArgs& a, const SimplexGeom* d_geom, const int* d_cand,
+                   cudaStream_t stream, SearchPlan* plan) {
+    SearchPlan& p = *plan;
+    p = SearchPlan{};
+    p.stream = stream;
+    p.d_geom = d_geom;
     int dev = 0, sms = 0, occ = 0;
     FPH_CUDA_TRY(cudaGetDevice(&dev));
     FPH_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     const bool sv = a.P <= kValsCap;
-    const int smem = (int)search_smem_bytes(a.P, a.m);
+    p.smem = (int)search_smem_bytes(a.P, a.m);
     // Complexes of >= 10 000 simplices run the phases as four kernels, A | B |
     // C | F, each with its own register allocation (phase C alone lost a third
     // of its cycles that way), chained per simplex by programmatic dependent
@@ -1246,100 +1290,110 @@ int launch_search(const FloodArgs& a, const SimplexGeom* d_geom, const int* d_ca
     long long split_min = 10000;
     if (const char* e = getenv("FPH_SPLIT_MIN_SIMPLICES")) split_min = atoll(e);
     const bool chain = a.n >= split_min;
-    using K = void (*)(const FloodArgs, const SimplexGeom*, const int*, int*, int*, int);
-    K kern[4] = {nullptr, nullptr, nullptr, nullptr};
-    float* d_lower = nullptr;
     if (chain) {
-        kern[0] = sv ? search_kernel<true, 1> : search_kernel<false, 1>;
-        kern[1] = sv ? search_kernel<true, 5> : search_kernel<false, 5>;
-        kern[2] = sv ? search_kernel<true, 6> : search_kernel<false, 6>;
-        kern[3] = sv ? search_kernel<true, 4> : search_kernel<false, 4>;
-        FPH_CUDA_TRY(cudaMallocAsync(&d_lower, sizeof(float) * a.n, stream));
+        p.kern[0] = sv ? search_kernel<true, 1> : search_kernel<false, 1>;
+        p.kern[1] = sv ? search_kernel<true, 5> : search_kernel<false, 5>;
+        p.kern[2] = sv ? search_kernel<true, 6> : search_kernel<false, 6>;
+        p.kern[3] = sv ? search_kernel<true, 4> : search_kernel<false, 4>;
+        FPH_CUDA_TRY(cudaMallocAsync(&p.d_lower, sizeof(float) * a.n, stream));
     } else {
-        kern[0] = sv ? search_kernel<true, 0> : search_kernel<false, 0>;
+        p.kern[0] = sv ? search_kernel<true, 0> : search_kernel<false, 0>;
     }
-    FPH_CUDA_TRY(cudaFuncSetAttribute(kern[0], cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    FPH_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern[0], kSThreads, smem));
+    FPH_CUDA_TRY(cudaFuncSetAttribute(p.kern[0], cudaFuncAttributeMaxDynamicSharedMemorySize, p.smem));
+    FPH_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, p.kern[0], kSThreads, p.smem));
     int blocks = sms * (occ > 0 ? occ : 1);
-    blocks = blocks < (a.n + kSW - 1) / kSW ? blocks : (a.n + kSW - 1) / kSW;
-    FloodArgs b = a;
-    b.lower = d_lower;
-    b.wt_off = (int)(sv ? kSmemVals : sizeof(SearchSmem));
-    long long* d_thr = nullptr;
+    p.blocks = blocks < (a.n + kSW - 1) / kSW ? blocks : (a.n + kSW - 1) / kSW;
+    p.b = a;
+    p.b.lower = p.d_lower;
+    p.b.wt_off = (int)(sv ? kSmemVals : sizeof(SearchSmem));
     if (a.team_threshold <= 0) {
         // threshold from the total candidate count, computed on the device so
         // the concurrent streams never wait for the host
         const double beta = a.team_threshold < 0 ? -a.team_threshold / 100.0 : kTeamBeta;
         static const double team_pow =
             getenv("FPH_TEAM_POW") ? atof(getenv("FPH_TEAM_POW")) : FPH_TEAM_POW;
-        FPH_CUDA_TRY(cudaMallocAsync(&d_thr, 2 * sizeof(long long), stream));
-        double* d_sum = reinterpret_cast<double*>(d_thr + 1);
-        FPH_CUDA_TRY(cudaMemsetAsync(d_sum, 0, sizeof(double), stream));
+        static const double team_gamma =
+            getenv("FPH_TEAM_GAMMA") ? atof(getenv("FPH_TEAM_GAMMA")) : FPH_TEAM_GAMMA;
+        FPH_CUDA_TRY(cudaMallocAsync(&p.d_thr, 3 * sizeof(long long), stream));
+        double* d_sum = reinterpret_cast<double*>(p.d_thr + 1);
+        FPH_CUDA_TRY(cudaMemsetAsync(d_sum, 0, 2 * sizeof(double), stream));
         pow_sum_kernel<<<std::min(148, (a.n + 255) / 256), 256, 0, stream>>>(d_cand, a.n, team_pow,
                                                                           d_sum);
-        team_thr_kernel<<<1, 1, 0, stream>>>(d_sum, beta, team_pow, blocks * kSW, d_thr);
-        b.team_thr_dev = d_thr;
+        team_thr_kernel<<<1, 1, 0, stream>>>(d_sum, beta, team_pow, team_gamma, p.blocks * kSW,
+                                             p.d_thr);
+        p.b.team_thr_dev = p.d_thr;
     }
     // order: FPH_ORDER=0 (environment) sorts by candidate count alone,
     // largest first (bits [8, 24)); the default adds spatial locality
     // (order_key_kernel)
     static const int order_mode = getenv("FPH_ORDER") ? atoi(getenv("FPH_ORDER")) : 1;
-    int *d_keys = nullptr, *d_order = nullptr, *d_iota = nullptr, *d_key_in = nullptr;
-    FPH_CUDA_TRY(cudaMallocAsync(&d_keys, sizeof(int) * a.n, stream));
-    FPH_CUDA_TRY(cudaMallocAsync(&d_order, sizeof(int) * a.n, stream));
-    FPH_CUDA_TRY(cudaMallocAsync(&d_iota, sizeof(int) * a.n, stream));
-    iota_kernel<<<(a.n + 255) / 256, 256, 0, stream>>>(d_iota, a.n);
+    FPH_CUDA_TRY(cudaMallocAsync(&p.d_keys, sizeof(int) * a.n, stream));
+    FPH_CUDA_TRY(cudaMallocAsync(&p.d_order, sizeof(int) * a.n, stream));
+    FPH_CUDA_TRY(cudaMallocAsync(&p.d_iota, sizeof(int) * a.n, stream));
+    iota_kernel<<<(a.n + 255) / 256, 256, 0, stream>>>(p.d_iota, a.n);
     int lo_bit = kSortLo, hi_bit = 24;
     const int* sort_in = d_cand;
     if (order_mode == 1) {
-        FPH_CUDA_TRY(cudaMallocAsync(&d_key_in, sizeof(int) * a.n, stream));
+        FPH_CUDA_TRY(cudaMallocAsync(&p.d_key_in, sizeof(int) * a.n, stream));
         order_key_kernel<<<(a.n + 255) / 256, 256, 0, stream>>>(
-            a.gp, d_geom, d_cand, a.n, b.team_thr_dev, (long long)a.team_threshold, d_key_in);
-        sort_in = d_key_in;
+            a.gp, d_geom, d_cand, a.n, p.b.team_thr_dev, (long long)a.team_threshold, p.d_key_in);
+        sort_in = p.d_key_in;
         lo_bit = 0;
         hi_bit = 29;
     }
     size_t tmp_bytes = 0;
-    cub::DeviceRadixSort::SortPairsDescending(nullptr, tmp_bytes, sort_in, d_keys, d_iota, d_order,
-                                              a.n, lo_bit, hi_bit, stream);
-    void* tmp = nullptr;
-    FPH_CUDA_TRY(cudaMallocAsync(&tmp, tmp_bytes, stream));
-    FPH_CUDA_TRY(cub::DeviceRadixSort::SortPairsDescending(tmp, tmp_bytes, sort_in, d_keys, d_iota,
-                                                           d_order, a.n, lo_bit, hi_bit, stream));
-    int nk = 0;
-    while (nk < 4 && kern[nk]) ++nk;
-    int* d_stage = nullptr;
-    int* d_counters = nullptr;
-    FPH_CUDA_TRY(cudaMallocAsync(&d_counters, sizeof(int) * 4, stream));
-    FPH_CUDA_TRY(cudaMemsetAsync(d_counters, 0, sizeof(int) * 4, stream));
-    if (nk > 1) {
-        FPH_CUDA_TRY(cudaMallocAsync(&d_stage, sizeof(int) * a.n, stream));
-        FPH_CUDA_TRY(cudaMemsetAsync(d_stage, 0, sizeof(int) * a.n, stream));
+    cub::DeviceRadixSort::SortPairsDescending(nullptr, tmp_bytes, sort_in, p.d_keys, p.d_iota,
+                                              p.d_order, a.n, lo_bit, hi_bit, stream);
+    FPH_CUDA_TRY(cudaMallocAsync(&p.tmp, tmp_bytes, stream));
+    FPH_CUDA_TRY(cub::DeviceRadixSort::SortPairsDescending(p.tmp, tmp_bytes, sort_in, p.d_keys,
+                                                           p.d_iota, p.d_order, a.n, lo_bit,
+                                                           hi_bit, stream));
+    while (p.nk < 4 && p.kern[p.nk]) ++p.nk;
+    FPH_CUDA_TRY(cudaMallocAsync(&p.d_counters, sizeof(int) * 4, stream));
+    FPH_CUDA_TRY(cudaMemsetAsync(p.d_counters, 0, sizeof(int) * 4, stream));
+    if (p.nk > 1) {
+        FPH_CUDA_TRY(cudaMallocAsync(&p.d_stage, sizeof(int) * a.n, stream));
+        FPH_CUDA_TRY(cudaMemsetAsync(p.d_stage, 0, sizeof(int) * a.n, stream));
     }
-    for (int i = 0; i < nk; ++i) {
-        FPH_CUDA_TRY(cudaFuncSetAttribute(kern[i], cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    FPH_CUDA_TRY(cudaGetLastError());
+    return FPH_OK;
+}
+
+int search_run(SearchPlan& p, bool release) {
+    for (int i = 0; i < p.nk; ++i) {
+        FPH_CUDA_TRY(cudaFuncSetAttribute(p.kern[i], cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          p.smem));
         cudaLaunchConfig_t cfg = {};
-        cfg.gridDim = dim3(blocks);
+        cfg.gridDim = dim3(p.blocks);
         cfg.blockDim = dim3(kSThreads);
-        cfg.dynamicSmemBytes = smem;
-        cfg.stream = stream;
+        cfg.dynamicSmemBytes = p.smem;
+        cfg.stream = p.stream;
         cudaLaunchAttribute attr[1];
         attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
         attr[0].val.programmaticStreamSerializationAllowed = 1;
         cfg.attrs = attr;
-        cfg.numAttrs = (i > 0 && d_stage) ? 1 : 0;
-        FPH_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern[i], b, d_geom, (const int*)d_order, d_counters + i,
-                                        d_stage, i));
+        // PDL between the chain's phases (per-simplex stage flags order them)
+        cfg.numAttrs = (i > 0 && p.d_stage) ? 1 : 0;
+        FPH_CUDA_TRY(cudaLaunchKernelEx(&cfg, p.kern[i], p.b, p.d_geom, (const int*)p.d_order,
+                                        p.d_counters + i, p.d_stage, i));
     }
-    FPH_CUDA_TRY(cudaFreeAsync(d_counters, stream));
-    if (d_stage) FPH_CUDA_TRY(cudaFreeAsync(d_stage, stream));
-    if (d_lower) FPH_CUDA_TRY(cudaFreeAsync(d_lower, stream));
-    if (d_thr) FPH_CUDA_TRY(cudaFreeAsync(d_thr, stream));
     FPH_CUDA_TRY(cudaGetLastError());
-    for (void* p : {(void*)d_keys, (void*)d_order, (void*)d_iota, tmp})
-        FPH_CUDA_TRY(cudaFreeAsync(p, stream));
-    if (d_key_in) FPH_CUDA_TRY(cudaFreeAsync(d_key_in, stream));
+    return release ? search_release(p) : FPH_OK;
+}
+
+int search_release(SearchPlan& p) {
+    for (void* q : {(void*)p.d_counters, (void*)p.d_stage, (void*)p.d_lower, (void*)p.d_thr,
+                    (void*)p.d_keys, (void*)p.d_order, (void*)p.d_iota, p.tmp, (void*)p.d_key_in})
+        if (q) FPH_CUDA_TRY(cudaFreeAsync(q, p.stream));
+    p = SearchPlan{};
     return FPH_OK;
+}
+
+int launch_search(const FloodArgs& a, const SimplexGeom* d_geom, const int* d_cand,
+                  cudaStream_t stream) {
+    SearchPlan p;
+    FPH_TRY(search_prepare(a, d_geom, d_cand, stream, &p));
+    return search_run(p, true);
 }
 
 }  // namespace fph

@@ -44,10 +44,11 @@ def main():
         _native.check(lib.fph_flood_interior(_native.ptr(X), X.shape[0], X.shape[1], _native.ptr(lms),
                                              lms.shape[0], _native.ptr(s4), rows.shape[0], k, w["m"], 1,
                                              _native.ptr(sq), _native.FPH_MEM_HOST, None))
-        buf = np.empty(8 * rows.shape[0], dtype=np.int64)
         n = np.zeros(1, dtype=np.int64)
+        lib.fph_debug_simplex_cycles(0, None, 0, n.ctypes.data)
+        buf = np.empty(int(n[0]), dtype=np.int64)
         lib.fph_debug_simplex_cycles(0, buf.ctypes.data, buf.size, n.ctypes.data)
-        d = buf.reshape(-1, 8)
+        d = buf[2: 2 + 16 * int(buf[1])].reshape(-1, 16)
         tot = d[:, :4].sum(1).astype(float)
         staged = d[:, 6].astype(float)
         order = np.argsort(-tot)
