@@ -9,13 +9,7 @@ import pytest
 
 from paper_2509_22432_b200.delaunay import circumsphere_check, delaunay
 from paper_2509_22432_b200.filtration import FilteredComplex, FloodConfig, filtration_order
-from paper_2509_22432_b200.persistence import (
-    BoundaryMatrix,
-    _pairs,
-    betti_at,
-    boundary_matrix,
-    reduce_and_extract,
-)
+from paper_2509_22432_b200.persistence import betti_at, boundary_matrix, reduce_and_extract
 from tests import _complex as C
 from tests import _golden as G
 
@@ -53,15 +47,16 @@ def _flood_complex(name):
 
 
 @pytest.mark.parametrize("name", ["rand2d_m6", "rand3d_m4", "circle_m64", "torus10k_m20"])
-@pytest.mark.parametrize("clearing", [True, False])
-def test_native_persistence_equals_python_reduction(name, clearing):
+def test_generic_and_triangulation_inputs_agree(name):
+    """The same complex reduced from the triangulation's facet links and from
+    a plain FilteredComplex (facets found by vertex lookup), with and without
+    the clearing optimisation: identical diagrams."""
     fc = _flood_complex(name)
-    bm = boundary_matrix(fc)
-    assert bm.native is not None
-    native = reduce_and_extract(bm, fc, clearing=clearing)
     plain = FilteredComplex(fc.simplices, fc.order, meta={})
-    py = reduce_and_extract(boundary_matrix(plain), plain, clearing=clearing)
-    assert native.bars == py.bars
+    want = reduce_and_extract(boundary_matrix(fc), fc)
+    for clearing in (True, False):
+        assert reduce_and_extract(boundary_matrix(fc), fc, clearing=clearing).bars == want.bars
+        assert reduce_and_extract(boundary_matrix(plain), plain, clearing=clearing).bars == want.bars
 
 
 def test_filtration_order_matches_reference_sort():
@@ -142,3 +137,31 @@ def test_face_order_violation_detected():
 
     with pytest.raises(IntegrityError):
         boundary_matrix(bad)
+
+
+def test_missing_facet_detected():
+    simplices = [((0,), 0, 0.0), ((1,), 0, 0.0), ((0, 1), 1, 1.0), ((0, 2), 1, 2.0)]
+    fc = FilteredComplex(simplices, np.arange(4), meta={})
+    from paper_2509_22432_b200.errors import IntegrityError
+
+    with pytest.raises(IntegrityError, match="absent"):
+        boundary_matrix(fc)
+
+
+def test_generic_complex_not_grouped_by_dimension():
+    """A user-built complex listing simplices out of dimension order reduces
+    like the same complex grouped by dimension."""
+    grouped = [((0,), 0, 0.0), ((1,), 0, 0.0), ((2,), 0, 0.0),
+               ((0, 1), 1, 1.0), ((0, 2), 1, 2.0), ((1, 2), 1, 3.0), ((0, 1, 2), 2, 4.0)]
+    shuffled = [grouped[i] for i in (3, 0, 6, 1, 5, 2, 4)]
+
+    def fc_of(simplices):
+        keys = [(v, d, s) for s, d, v in simplices]
+        ranks = sorted(range(len(keys)), key=lambda i: keys[i])
+        order = np.empty(len(keys), dtype=np.int64)
+        order[ranks] = np.arange(len(keys))
+        return FilteredComplex(simplices, order, meta={})
+
+    a, b = fc_of(grouped), fc_of(shuffled)
+    assert reduce_and_extract(boundary_matrix(a), a).bars == reduce_and_extract(boundary_matrix(b), b).bars
+    assert reduce_and_extract(boundary_matrix(a), a).in_dim(1) == [(3.0, 4.0)]
