@@ -241,9 +241,6 @@ def run_ours(args):
     if world > 1:
         torch.distributed.barrier()
     lib.fph_launch_count(1)
-    stats = np.zeros(24)
-    lib.fph_set_profiling(1)
-    lib.fph_flood_stats(stats.ctypes.data, 1)
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     with ClockSampler(local) as clocks:
@@ -254,7 +251,20 @@ def run_ours(args):
             step(lib, _native, w, stream)
             ends[i].record()
         torch.cuda.synchronize()
-    launches = int(lib.fph_launch_count(0))
+        launches = int(lib.fph_launch_count(0))
+        # the same step captured into a CUDA graph and replayed (single-call
+        # steps; values checked equal to the uncaptured step's)
+        graph = (graph_step(lib, _native, w, flush, args)
+                 if (step is step_single and not args.no_graph) else None)
+    # an extra profiled pass (CUDA events around the flooding kernels, work
+    # counters) for the roofline, outside the timed steps
+    stats = np.zeros(24)
+    lib.fph_set_profiling(1)
+    lib.fph_flood_stats(stats.ctypes.data, 1)
+    for _ in range(args.steps):
+        flush.zero_()
+        step(lib, _native, w, stream)
+    torch.cuda.synchronize()
     lib.fph_flood_stats(stats.ctypes.data, 1)
     lib.fph_set_profiling(0)
     sharded_ok = None
@@ -264,16 +274,18 @@ def run_ours(args):
         step_single(lib, _native, w, stream)
         torch.cuda.synchronize()
         sharded_ok = all(torch.equal(a[: c], b[: c]) for a, b, c in zip(got, dc.out, dc.counts_full))
-    ms = sum(s.elapsed_time(e) for s, e in zip(starts, ends)) / args.steps
+    ms_eager = sum(s.elapsed_time(e) for s, e in zip(starts, ends)) / args.steps
+    use_graph = bool(graph) and graph.get("values_equal_uncaptured") is True
+    ms = graph["ms_per_step"] if use_graph else ms_eager
     n_simplices = sum(dc.n_simplices for _, dc in w["items"])
     if not sharded and world > 1:  # weak scaling: every rank its own clouds
         t = torch.tensor([float(n_simplices)], dtype=torch.float64, device=w["dev"])
         torch.distributed.all_reduce(t)
         n_simplices = int(t.item())
     if world > 1:
-        t = torch.tensor([ms], device=w["dev"])
+        t = torch.tensor([ms, ms_eager], device=w["dev"])
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        ms = float(t.item())
+        ms, ms_eager = float(t[0].item()), float(t[1].item())
     value = n_simplices / (ms / 1e3)
 
     result = None
@@ -297,6 +309,9 @@ def run_ours(args):
             "steps": args.steps,
             "warmup": args.warmup,
             "ms_per_step": ms,
+            "ms_per_step_eager": ms_eager,
+            "launch": ("CUDA graph of the step, replayed (values equal to the eager step's)"
+                       if use_graph else "eager C-ABI calls"),
             "higher_is_better": True,
             "scaling": "weak" if w["batch"] else "strong",
             "vs_baseline": None,
@@ -317,6 +332,8 @@ def run_ours(args):
         }
         if sharded_ok is not None:
             result["sharded_equals_single_gpu_values"] = sharded_ok
+        if graph:
+            result["cuda_graph"] = graph
         if e2e:
             result["e2e"] = e2e
         result["roofline"] = roofline(lib, stats, ms, args.steps, clocks.summary(),
@@ -411,6 +428,42 @@ def _algorithmic_bytes(config):
     kind, n, nl, m, max_dim = CONFIGS[config]
     dim = 2 if kind == "circle" else 3
     return 2 * n * dim * 8
+
+
+def graph_step(lib, native, w, flush, args):
+    """The same step captured once into a CUDA graph (device-memory calls on
+    a capturing stream: grid build, every dimension's kernels on their forked
+    streams, completion) and replayed: time per replay (events, L2 flushed)
+    and whether the replayed values equal an uncaptured step's."""
+    import torch
+
+    try:
+        ref = [dc.out[k][: dc.counts_full[k]].clone() for _, dc in w["items"]
+               for k in range(dc.top + 1)]
+        s = torch.cuda.Stream(device=w["dev"])
+        g = torch.cuda.CUDAGraph()
+        torch.cuda.synchronize()
+        with torch.cuda.graph(g, stream=s, capture_error_mode="thread_local"):
+            step_single(lib, native, w, s.cuda_stream)
+        for _ in range(2):
+            g.replay()
+        torch.cuda.synchronize()
+        times = []
+        for _ in range(args.steps):
+            flush.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            g.replay()
+            e1.record()
+            torch.cuda.synchronize()
+            times.append(e0.elapsed_time(e1))
+        got = [dc.out[k][: dc.counts_full[k]] for _, dc in w["items"] for k in range(dc.top + 1)]
+        same = all(torch.equal(a, b) for a, b in zip(ref, got))
+        n = sum(dc.n_simplices for _, dc in w["items"])
+        ms = float(np.mean(times))
+        return {"ms_per_step": ms, "value": n / (ms / 1e3), "values_equal_uncaptured": same}
+    except Exception as e:  # report, never fail the bench line
+        return {"error": f"{type(e).__name__}: {e}"[:300]}
 
 
 def brute_pairs(lib, native, w, stream):
@@ -607,6 +660,7 @@ def main():
     ap.add_argument("--config", choices=sorted(CONFIGS), default="sphere_torus_1m")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-graph", action="store_true", help="skip the CUDA-graph replay measurement")
     ap.add_argument("--force-sharded", action="store_true",
                     help="run the multi-GPU (shard + NCCL all-gather + completion) step even at N=1")
     ap.add_argument("--profile", action="store_true",

@@ -166,15 +166,24 @@ struct GridSlot {
         }
         ds->mu.lock();
         stream = s;
-        if (ds->free_ev) FPH_CUDA_TRY(cudaStreamWaitEvent(s, ds->free_ev, 0));
+        // under stream capture (a CUDA graph of the step) the graph's own
+        // order stands in for the event: replays of a captured call must not
+        // overlap other library calls on the device
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        FPH_CUDA_TRY(cudaStreamIsCapturing(s, &cs));
+        capturing = cs != cudaStreamCaptureStatusNone;
+        if (ds->free_ev && !capturing) FPH_CUDA_TRY(cudaStreamWaitEvent(s, ds->free_ev, 0));
         return set_search_grid(d_grid, s);
     }
     ~GridSlot() {
         if (!ds) return;
-        if (!ds->free_ev) cudaEventCreateWithFlags(&ds->free_ev, cudaEventDisableTiming);
-        if (ds->free_ev) cudaEventRecord(ds->free_ev, stream);
+        if (!capturing) {
+            if (!ds->free_ev) cudaEventCreateWithFlags(&ds->free_ev, cudaEventDisableTiming);
+            if (ds->free_ev) cudaEventRecord(ds->free_ev, stream);
+        }
         ds->mu.unlock();
     }
+    bool capturing = false;
 };
 
 // a host-memory call returns once its stream is drained (on errors too)
