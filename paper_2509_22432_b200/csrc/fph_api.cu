@@ -256,8 +256,9 @@ int check_cloud(const double* points, int64_t n, int32_t dim) {
     return FPH_OK;
 }
 
-FloodTuning current_tuning() {
+FloodTuning current_tuning(double points_per_landmark = 0.0) {
     FloodTuning t;
+    t.points_per_landmark = points_per_landmark;
     t.pairs_per_task = g_pairs_per_task;
     t.profile = g_profile;
     t.algo = g_algo;
@@ -542,7 +543,7 @@ int fph_flood_interior(const double* points, int64_t n_points, int32_t dim,
         GridSlot slot;
         FPH_TRY(slot.acquire(gs.d_grid, hc.stream));
         rc = flood_interior(gs.d_grid, lm3, d_s, (int)n_simplices, k, grid_resolution, subset_mode,
-                            d_out, current_tuning(), hc.stream);
+                            d_out, current_tuning((double)n_points / n_landmarks), hc.stream);
         count_launches(4);
         if (rc == FPH_OK && memory == FPH_MEM_HOST)
             FPH_CUDA_TRY(cudaMemcpyAsync(out_sq, d_out, sizeof(double) * n_simplices,
@@ -593,7 +594,8 @@ int fph_flood_samples(const double* points, int64_t n_points, int32_t dim,
         GridSlot slot;
         FPH_TRY(slot.acquire(gs.d_grid, hc.stream));
         rc = flood_interior(gs.d_grid, lm3, d_s, (int)n_simplices, k, 1, subset_mode, d_out,
-                            current_tuning(), hc.stream, smp3, n_samples);
+                            current_tuning((double)n_points / n_landmarks), hc.stream, smp3,
+                            n_samples);
         count_launches(4);
         if (rc == FPH_OK && memory == FPH_MEM_HOST)
             FPH_CUDA_TRY(cudaMemcpyAsync(out_sq, d_out, sizeof(double) * n_simplices,
@@ -683,7 +685,7 @@ static int flood_rows(const double* points, int64_t n_points, int32_t dim,
         GridGuard gg{gs, hc.stream};
         FPH_TRY(build_grid_timed(d_pts, (int)n_points, dim, hc.stream, &gs));
         count_launches(4);
-        const FloodTuning tune = current_tuning();
+        const FloodTuning tune = current_tuning((double)n_points / n_landmarks);
         int64_t mine[4] = {0, 0, 0, 0};
         int* s4[4] = {nullptr, nullptr, nullptr, nullptr};
         double* d_out[4] = {nullptr, nullptr, nullptr, nullptr};
@@ -784,7 +786,7 @@ int fph_flood_filtration(const double* points, int64_t n_points, int32_t dim,
         GridGuard gg{gs, hc.stream};
         FPH_TRY(build_grid_timed(d_pts, (int)n_points, dim, hc.stream, &gs));
         count_launches(4);
-        const FloodTuning tune = current_tuning();
+        const FloodTuning tune = current_tuning((double)n_points / n_landmarks);
         GridSlot slot;
         FPH_TRY(slot.acquire(gs.d_grid, hc.stream));
         double* d_vals[4] = {nullptr, nullptr, nullptr, nullptr};

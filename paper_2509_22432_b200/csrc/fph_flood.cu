@@ -760,6 +760,7 @@ int range_prepare(const Grid* d_grid, const double* d_landmarks3, const int* d_s
     a.team_thr_dev = nullptr;
     a.exact_pairs = tune.exact_pairs;
     for (int i = 0; i < 4; ++i) a.exact_cand[i] = tune.exact_cand[i];
+    a.points_per_landmark = tune.points_per_landmark;
     a.tmpl = T.rows;
     a.blk_off = T.blk_off;
 

@@ -43,6 +43,7 @@ struct FloodArgs {
     long long* dbg;           // optional: per simplex 8 values (phase cycles, counters)
     double exact_pairs;       // bounded search: one exact pass when rows x candidates <= this
     long long exact_cand[4];  // bounded search: exact pass when candidates <= this, per dim
+    double points_per_landmark;  // work estimate of a launch: n x P x this
 };
 
 // debug capture of flood_interior calls (per-simplex phase cycles, times):
@@ -84,6 +85,7 @@ size_t search_smem_bytes(int P, int m);
 size_t search_smem_limit();
 
 struct FloodTuning {
+    double points_per_landmark = 0.0;  // cloud points / landmarks: scales the work estimate
     double pairs_per_task = 0.0;  // <= 0: default 2^21
     bool profile = false;         // time pass kernels with events
     int algo = 1;                 // 0: brute force over the Lemma-4.2 ball, 1: block search

@@ -1280,16 +1280,20 @@ int search_prepare(const FloodArgs& a, const SimplexGeom* d_geom, const int* d_c
     FPH_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     const bool sv = a.P <= kValsCap;
     p.smem = (int)search_smem_bytes(a.P, a.m);
-    // Complexes of >= 10 000 simplices run the phases as four kernels, A | B |
-    // C | F, each with its own register allocation (phase C alone lost a third
-    // of its cycles that way), chained per simplex by programmatic dependent
-    // launch so each kernel's tail overlaps the next one.  Small complexes
-    // keep one kernel, where the extra launches and tails do not amortise.
-    // FPH_SPLIT_MIN_SIMPLICES (environment) overrides the 10 000 cut-off;
+    // Launches with enough work run the phases as four kernels, A | B | C | F,
+    // each with its own register allocation (phase C alone lost a third of its
+    // cycles that way), chained per simplex by programmatic dependent launch so
+    // each kernel's tail overlaps the next one.  Light launches keep one
+    // kernel, where the extra launches and tails do not amortise.  Work
+    // estimate: simplices x rows x cloud points per landmark, >= 1e8 (a box
+    // shard of 4k tetrahedra of 10M points is heavy, 8k triangles of a 10k
+    // torus are not); without the ratio, >= 10 000 simplices.
+    // FPH_SPLIT_MIN_SIMPLICES (environment) overrides with a simplex count;
     // the tests set it to 0 to run the small golden complexes through the chain
-    long long split_min = 10000;
-    if (const char* e = getenv("FPH_SPLIT_MIN_SIMPLICES")) split_min = atoll(e);
-    const bool chain = a.n >= split_min;
+    bool chain = a.points_per_landmark > 0.0
+                     ? (double)a.n * (double)a.P * a.points_per_landmark >= 1e8
+                     : a.n >= 10000;
+    if (const char* e = getenv("FPH_SPLIT_MIN_SIMPLICES")) chain = a.n >= atoll(e);
     if (chain) {
         p.kern[0] = sv ? search_kernel<true, 1> : search_kernel<false, 1>;
         p.kern[1] = sv ? search_kernel<true, 5> : search_kernel<false, 5>;
