@@ -490,8 +490,8 @@ def test_concurrent_host_threads_share_the_device():
         assert all(f.result() for f in futs)
 
 
-@pytest.mark.parametrize("world", [2, 5])
-def test_spatial_shards_equal_single_gpu(world):
+@pytest.mark.parametrize("dim,world", [(3, 2), (3, 5), (3, 8), (2, 4)])
+def test_spatial_shards_equal_single_gpu(dim, world):
     """fph_flood_subset over spatially compact shards (the bench's multi-GPU
     partition), computed rank after rank on one GPU, reassembled and
     completed: equal to the single-call values."""
@@ -500,25 +500,29 @@ def test_spatial_shards_equal_single_gpu(world):
     from paper_2509_22432_b200.parallel import (complete, simplex_centers, spatial_partition,
                                                 subset_interior)
 
-    X = gen_sphere_torus_mix(150_000, seed=4).points
+    if dim == 3:
+        X = gen_sphere_torus_mix(150_000, seed=4).points
+    else:
+        X = np.random.default_rng(4).random((120_000, 2))
+    top = dim
     tri = delaunay(X[farthest_point_sampling(X, 400)])
-    want = flood_sq_values(X, tri, 10, True, 3)
+    want = flood_sq_values(X, tri, 10, True, top)
     dev = torch.device("cuda:0")
     Xd = torch.from_numpy(X).to(dev)
     lm = torch.from_numpy(np.ascontiguousarray(tri.points)).to(dev)
     by_dim = {k: torch.from_numpy(np.ascontiguousarray(tri.simplices_by_dim[k], dtype=np.int32)).to(dev)
-              for k in range(4)}
+              for k in range(top + 1)}
     fac = {k: torch.from_numpy(np.ascontiguousarray(tri.facet_links[k], dtype=np.int32)).to(dev)
-           for k in range(1, 4)}
+           for k in range(1, top + 1)}
     parts = {k: [torch.from_numpy(p).to(dev) for p in
                  spatial_partition(simplex_centers(tri.points, tri.simplices_by_dim[k]), None, world)]
-             for k in range(1, 4)}
+             for k in range(1, top + 1)}
     interior = {k: torch.full((by_dim[k].shape[0],), float("nan"), dtype=torch.float64, device=dev)
-                for k in range(1, 4)}
+                for k in range(1, top + 1)}
     for r in range(world):
-        share = subset_interior(Xd, lm, by_dim, 3, 10, True, {k: parts[k][r] for k in range(1, 4)})
-        for k in range(1, 4):
+        share = subset_interior(Xd, lm, by_dim, top, 10, True, {k: parts[k][r] for k in range(1, top + 1)})
+        for k in range(1, top + 1):
             interior[k][parts[k][r]] = share[k]
-    got = complete(interior, fac, by_dim[0].shape[0], 3, True)
-    for k in range(4):
+    got = complete(interior, fac, by_dim[0].shape[0], top, True)
+    for k in range(top + 1):
         assert np.array_equal(got[k].cpu().numpy(), want[k]), k
