@@ -306,6 +306,73 @@ __device__ __forceinline__ void load_rel(const Ctx& c, int idx, float& ax, float
     aw = fmaf(az, az, fmaf(ay, ay, ax * ax));
 }
 
+#ifndef FPH_PROBE_CAP
+#define FPH_PROBE_CAP 16
+#endif
+// Local probe of one sample point (one lane, phase B): its nearest
+// candidate among the first kProbeCap cloud points of the 3 cells of its
+// own grid row (kProbeRows 3 / 9: also the neighbouring rows of cells).
+// The representatives' bound U of a point in dense data is set by the
+// spacing of a ~reps_target sample of the whole masking ball -- an order of
+// magnitude above the point's nn distance for a long edge or a large hull
+// tetrahedron -- while a point of its own cells is nearly as close as the
+// nearest one.  The tight U prunes most rows in phase C without a search
+// (box_10m 39 -> 18 ms).  Any candidate gives an upper bound, so the cap
+// and the order are free; the value is the same fp32 expression (and error
+// bound) as every other minimum, so U stays a certified upper bound.
+constexpr int kProbeCap = FPH_PROBE_CAP;
+#ifndef FPH_PROBE_MIN
+#define FPH_PROBE_MIN 0.0f
+#endif
+// only points whose bound exceeds this many squared cell edges are probed
+// (below it the point's own exact search is small anyway)
+constexpr float kProbeMin = FPH_PROBE_MIN;
+#ifndef FPH_PROBE_ROWS
+#define FPH_PROBE_ROWS 1
+#endif
+// rows of cells probed: 1 (the point's own), 3 (its y-neighbours) or 9
+constexpr int kProbeRows = FPH_PROBE_ROWS;
+
+__device__ __forceinline__ float local_probe(const Ctx& c, const PointF& q) {
+    const Grid& g = c_grid;
+    const double px = c.G.cx + (double)q.bx, py = c.G.cy + (double)q.by,
+                 pz = c.G.cz + (double)q.bz;
+    const int ix = cell_coord(px, g.lox, g.inv_h, g.nx);
+    const int iy = cell_coord(py, g.loy, g.inv_h, g.ny);
+    const int iz = cell_coord(pz, g.loz, g.inv_h, g.nz);
+    const int x0 = max(ix - 1, 0), x1 = min(ix + 1, g.nx - 1);
+    float best = INFINITY;
+    int left = kProbeCap;
+    const int nt = g.nz > 1 ? kProbeRows : min(kProbeRows, 3);
+    for (int t = 0; t < nt && left > 0; ++t) {
+        // (dy, dz) in the order 0, -1, +1 each: the point's own row first
+        const int dy = (t % 3 == 0) ? 0 : (t % 3 == 1 ? -1 : 1);
+        const int dz = (t / 3 == 0) ? 0 : (t / 3 == 1 ? -1 : 1);
+        const int y = iy + dy, z = iz + dz;
+        if (y < 0 || y >= g.ny || z < 0 || z >= g.nz) continue;
+        const int base = (z * g.ny + y) * g.nx;
+        const int s = g.cell_start[base + x0];
+        const int e = min(g.cell_start[base + x1 + 1], s + left);
+        left -= e - s;
+        int i = s;
+        for (; i + 1 < e; i += 2) {  // two loads in flight
+            float ax, ay, az, aw, bx, by, bz, bw;
+            load_rel(c, i, ax, ay, az, aw);
+            load_rel(c, i + 1, bx, by, bz, bw);
+            if (aw <= c.thr) best = fminf(best, fmaf(q.px2, ax, fmaf(q.py2, ay, fmaf(q.pz2, az, aw))));
+            if (bw <= c.thr) best = fminf(best, fmaf(q.px2, bx, fmaf(q.py2, by, fmaf(q.pz2, bz, bw))));
+        }
+        if (i < e) {
+            float ax, ay, az, aw;
+            load_rel(c, i, ax, ay, az, aw);
+            if (aw <= c.thr) best = fminf(best, fmaf(q.px2, ax, fmaf(q.py2, ay, fmaf(q.pz2, az, aw))));
+        }
+    }
+    if (!(best < INFINITY)) return INFINITY;
+    const float m = best + q.bb;
+    return m + err_bound(m, q.B);
+}
+
 // append the kept candidates of the warp to the tile; returns the new size
 __device__ __forceinline__ int tile_push(WarpSmem& W, int n, bool keep, float ax, float ay,
                                          float az, float aw) {
@@ -883,7 +950,9 @@ __device__ void run_simplex(const Ctx& c, WarpSmem& W, const Team& tm, float* va
         for (int j = tm.rank * 32 + lane; j < a.P; j += tm.size * 32) {
             const PointF q = point_at(c, j);
             const float m = vals[j];
-            const float u = fminf(m + err_bound(m, q.B), vertex_bound(c, q));
+            float u = fminf(m + err_bound(m, q.B), vertex_bound(c, q));
+            if (kProbeCap > 0 && u > kProbeMin * (float)(c_grid.h * c_grid.h))
+                u = fminf(u, local_probe(c, q));
             vals[j] = u;
             if (u > umax) {
                 umax = u;
