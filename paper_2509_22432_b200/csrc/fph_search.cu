@@ -309,26 +309,34 @@ __device__ __forceinline__ void load_rel(const Ctx& c, int idx, float& ax, float
 #ifndef FPH_PROBE_CAP
 #define FPH_PROBE_CAP 16
 #endif
-// Local probe of one sample point (one lane, phase B): its nearest
-// candidate among the first kProbeCap cloud points of the 3 cells of its
-// own grid row (kProbeRows 3 / 9: also the neighbouring rows of cells).
+// Local probe of one sample point (one lane, phase A): its nearest
+// candidate among the first kProbeCap cloud points of the 3 x 3 cells of
+// its own grid row and the two rows beside it in y (kProbeRows 1: own row
+// only; 9: the full 3 x 3 x 3).
 // The representatives' bound U of a point in dense data is set by the
 // spacing of a ~reps_target sample of the whole masking ball -- an order of
 // magnitude above the point's nn distance for a long edge or a large hull
 // tetrahedron -- while a point of its own cells is nearly as close as the
 // nearest one.  The tight U prunes most rows in phase C without a search
-// (box_10m 39 -> 18 ms).  Any candidate gives an upper bound, so the cap
-// and the order are free; the value is the same fp32 expression (and error
-// bound) as every other minimum, so U stays a certified upper bound.
+// (box_10m 39 -> 12 ms, with the skipped representatives below).  Any candidate gives an upper bound, so the cap
+// and the order are free; the value is the same fp32 expression as every
+// other minimum (phase B adds the same error bound), so U stays a
+// certified upper bound.
 constexpr int kProbeCap = FPH_PROBE_CAP;
-#ifndef FPH_PROBE_MIN
-#define FPH_PROBE_MIN 0.0f
+#ifndef FPH_PROBE_SKIP
+#define FPH_PROBE_SKIP 1
 #endif
-// only points whose bound exceeds this many squared cell edges are probed
-// (below it the point's own exact search is small anyway)
-constexpr float kProbeMin = FPH_PROBE_MIN;
+// 1: a simplex whose every row's probe found a candidate skips the
+// representatives' pass ...
+constexpr bool kProbeSkip = FPH_PROBE_SKIP;
+#ifndef FPH_PROBE_TIGHT
+#define FPH_PROBE_TIGHT 4.0f
+#endif
+// ... provided every probe found one within sqrt(kProbeTight) cell edges
+// (looser probe bounds leave phase C more to search than the pass costs)
+constexpr float kProbeTight = FPH_PROBE_TIGHT;
 #ifndef FPH_PROBE_ROWS
-#define FPH_PROBE_ROWS 1
+#define FPH_PROBE_ROWS 3
 #endif
 // rows of cells probed: 1 (the point's own), 3 (its y-neighbours) or 9
 constexpr int kProbeRows = FPH_PROBE_ROWS;
@@ -343,8 +351,9 @@ __device__ __forceinline__ float local_probe(const Ctx& c, const PointF& q) {
     const int x0 = max(ix - 1, 0), x1 = min(ix + 1, g.nx - 1);
     float best = INFINITY;
     int left = kProbeCap;
-    const int nt = g.nz > 1 ? kProbeRows : min(kProbeRows, 3);
-    for (int t = 0; t < nt && left > 0; ++t) {
+    // one row of cells at a time, so a full own row costs no further loads
+    // (fetching every row's run up front: +1-2% on surface data)
+    for (int t = 0; t < kProbeRows && left > 0; ++t) {
         // (dy, dz) in the order 0, -1, +1 each: the point's own row first
         const int dy = (t % 3 == 0) ? 0 : (t % 3 == 1 ? -1 : 1);
         const int dz = (t / 3 == 0) ? 0 : (t / 3 == 1 ? -1 : 1);
@@ -368,9 +377,7 @@ __device__ __forceinline__ float local_probe(const Ctx& c, const PointF& q) {
             if (aw <= c.thr) best = fminf(best, fmaf(q.px2, ax, fmaf(q.py2, ay, fmaf(q.pz2, az, aw))));
         }
     }
-    if (!(best < INFINITY)) return INFINITY;
-    const float m = best + q.bb;
-    return m + err_bound(m, q.B);
+    return best < INFINITY ? best + q.bb : INFINITY;  // m32, as the folds give it
 }
 
 // append the kept candidates of the warp to the tile; returns the new size
@@ -927,7 +934,37 @@ __device__ void run_simplex(const Ctx& c, WarpSmem& W, const Team& tm, float* va
         // sample of ~reps_target candidates
         const bool exact = (double)C * (double)a.P <= a.exact_pairs || C <= a.exact_cand[a.k];
         stride = exact ? 1 : (int)max(1ll, (C + a.reps_target - 1) / a.reps_target);
-        reps_pass(c, W, stride, vals, tm, pairs, staged);
+        // sampled simplices: every row first probes its own cells; when all
+        // rows found a close candidate there (dense data) those bounds
+        // replace the representatives' -- whose pass enumerates every grid
+        // row of the masking ball, the dominant cost of a large simplex
+        bool reps = true;
+        if (stride > 1 && kProbeCap > 0) {
+            // batch by batch of rows; the first batch with a loose row ends
+            // the probing (the pass runs anyway, so further probes would
+            // only add their cost: surface data, voids)
+            const float tight = kProbeTight * (float)(c_grid.h * c_grid.h);
+            reps = false;
+            for (int j0 = 0; j0 < a.P; j0 += tm.size * 32) {
+                const int j = j0 + tm.rank * 32 + lane;
+                int miss = 0;
+                if (j < a.P) {
+                    const float m = local_probe(c, point_at(c, j));
+                    miss = !(m <= tight);  // none, or not within ~a cell edge
+                    if (m < INFINITY) {
+                        if (tm.size == 1) vals[j] = m;
+                        else atomicMin(reinterpret_cast<unsigned*>(vals) + j, f2ord(m));
+                    }
+                }
+                if (tm.sum((long long)__reduce_add_sync(0xffffffffu, (unsigned)miss)) > 0) {
+                    reps = true;
+                    break;
+                }
+            }
+            reps = reps || !kProbeSkip;
+            tm.sync();
+        }
+        if (reps) reps_pass(c, W, stride, vals, tm, pairs, staged);
         tm.sync();
         if (tm.size > 1) {  // decode the ordered minima
             __threadfence_block();
@@ -950,9 +987,7 @@ __device__ void run_simplex(const Ctx& c, WarpSmem& W, const Team& tm, float* va
         for (int j = tm.rank * 32 + lane; j < a.P; j += tm.size * 32) {
             const PointF q = point_at(c, j);
             const float m = vals[j];
-            float u = fminf(m + err_bound(m, q.B), vertex_bound(c, q));
-            if (kProbeCap > 0 && u > kProbeMin * (float)(c_grid.h * c_grid.h))
-                u = fminf(u, local_probe(c, q));
+            const float u = fminf(m + err_bound(m, q.B), vertex_bound(c, q));
             vals[j] = u;
             if (u > umax) {
                 umax = u;
