@@ -32,36 +32,50 @@ __host__ __device__ inline double ord2d(unsigned long long u) {
     return d;
 }
 
-// bbox[0..2] = ordered mins, bbox[3..5] = ordered maxes (block reduction,
-// then one atomic per block and value)
-__global__ void bbox_kernel(const double* __restrict__ pts, int n, int dim,
-                            unsigned long long* bbox) {
-    __shared__ double smn[3][32], smx[3][32];
-    double mn[3] = {INFINITY, INFINITY, INFINITY};
-    double mx[3] = {-INFINITY, -INFINITY, -INFINITY};
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-        for (int a = 0; a < dim; ++a) {
-            double v = pts[(size_t)i * dim + a];
-            mn[a] = fmin(mn[a], v);
-            mx[a] = fmax(mx[a], v);
-        }
+// bbox[0..2] = ordered mins, bbox[3..5] = ordered maxes.  The cloud is read
+// as one flat array of n * dim doubles, consecutive threads on consecutive
+// elements (fully coalesced; row-wise reads of the 24-byte rows ran at a
+// third of HBM speed); the grid stride is a multiple of dim, so a thread
+// always sees the same axis.  Block reduction per axis, then one atomic per
+// block and value.
+constexpr int kBoxThreads = 384;  // a multiple of 2 and 3
+
+__global__ void __launch_bounds__(kBoxThreads) bbox_kernel(const double* __restrict__ pts, int n,
+                                                           int dim, unsigned long long* bbox) {
+    __shared__ double smn[3][kBoxThreads / 32], smx[3][kBoxThreads / 32];
+    const long long total = (long long)n * dim;
+    const long long stride = (long long)gridDim.x * kBoxThreads;
+    const long long e0 = (long long)blockIdx.x * kBoxThreads + threadIdx.x;
+    const int axis = (int)(e0 % dim);
+    double mn = INFINITY, mx = -INFINITY;
+    long long e = e0;
+    for (; e + 3 * stride < total; e += 4 * stride) {  // four loads in flight
+        const double v0 = pts[e], v1 = pts[e + stride], v2 = pts[e + 2 * stride],
+                     v3 = pts[e + 3 * stride];
+        mn = fmin(mn, fmin(fmin(v0, v1), fmin(v2, v3)));
+        mx = fmax(mx, fmax(fmax(v0, v1), fmax(v2, v3)));
     }
-    const int w = threadIdx.x >> 5, l = threadIdx.x & 31, nw = blockDim.x >> 5;
+    for (; e < total; e += stride) {
+        mn = fmin(mn, pts[e]);
+        mx = fmax(mx, pts[e]);
+    }
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
     for (int a = 0; a < dim; ++a) {
+        double lo = axis == a ? mn : INFINITY, hi = axis == a ? mx : -INFINITY;
         for (int o = 16; o > 0; o >>= 1) {
-            mn[a] = fmin(mn[a], __shfl_xor_sync(0xffffffffu, mn[a], o));
-            mx[a] = fmax(mx[a], __shfl_xor_sync(0xffffffffu, mx[a], o));
+            lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+            hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
         }
         if (l == 0) {
-            smn[a][w] = mn[a];
-            smx[a][w] = mx[a];
+            smn[a][w] = lo;
+            smx[a][w] = hi;
         }
     }
     __syncthreads();
     if (threadIdx.x < dim) {
         const int a = threadIdx.x;
         double lo = smn[a][0], hi = smx[a][0];
-        for (int i = 1; i < nw; ++i) {
+        for (int i = 1; i < kBoxThreads / 32; ++i) {
             lo = fmin(lo, smn[a][i]);
             hi = fmax(hi, smx[a][i]);
         }
@@ -224,9 +238,9 @@ int grid_build(const double* d_pts, int n, int dim, double cell_size, double occ
     FPH_CUDA_TRY(cudaMemsetAsync(d_bbox, 0xff, 3 * sizeof(unsigned long long), stream));
     FPH_CUDA_TRY(cudaMemsetAsync(d_bbox + 3, 0, 3 * sizeof(unsigned long long), stream));
     FPH_CUDA_TRY(cudaMemsetAsync(counts, 0, sizeof(int) * (cap + 1), stream));
-    int blocks = (n + 255) / 256;
-    if (blocks > 592) blocks = 592;
-    bbox_kernel<<<blocks, 256, 0, stream>>>(d_pts, n, dim, d_bbox);
+    const long long elems = (long long)n * dim;
+    const int blocks = (int)std::min<long long>(4 * 148, (elems + 4 * kBoxThreads - 1) / (4 * kBoxThreads));
+    bbox_kernel<<<blocks, kBoxThreads, 0, stream>>>(d_pts, n, dim, d_bbox);
     grid_params_kernel<<<1, 1, 0, stream>>>(d_bbox, n, dim, cell_size, occupancy, cap, g,
                                             gs->d_grid);
     cell_id_kernel<<<(n + 255) / 256, 256, 0, stream>>>(d_pts, n, dim, gs->d_grid, keys, counts);
