@@ -139,7 +139,12 @@ __global__ void setup_kernel(FloodArgs a, SimplexGeom* __restrict__ geom,
         // an estimate suffices -- fp32 row clipping, every `step`-th row,
         // about 256 rows of a large ball (a hull simplex of box_10m spans
         // ~10^5 grid rows; every 4th of them made this kernel 0.14 ms)
-        const int step = rows > 1024 ? ((rows / 256) | 1) : (rows > 512 ? 4 : (rows > 128 ? 2 : 1));
+#ifndef FPH_SETUP_ROWS
+#define FPH_SETUP_ROWS 256
+#endif
+        const int step = (FPH_SETUP_ROWS > 0 && rows > 4 * FPH_SETUP_ROWS)
+                             ? ((rows / FPH_SETUP_ROWS) | 1)
+                             : (rows > 512 ? 4 : (rows > 128 ? 2 : 1));
         const RowClipF cf = make_clip_f(g, c[0], c[1], c[2], G.rho);
 #pragma unroll 4
         for (int rr = lane * step; rr < rows; rr += 32 * step) {

@@ -310,9 +310,11 @@ __device__ __forceinline__ void load_rel(const Ctx& c, int idx, float& ax, float
 #define FPH_PROBE_CAP 16
 #endif
 // Local probe of one sample point (one lane, phase A): its nearest
-// candidate among the first kProbeCap cloud points of the 3 x 3 cells of
-// its own grid row and the two rows beside it in y (kProbeRows 1: own row
-// only; 9: the full 3 x 3 x 3).
+// candidate among the first kProbeCap cloud points of the 3-cell runs of
+// its own grid row and the four rows beside it in y and z (kProbeRows 1:
+// own row only; 3: y only; 9: the full 3 x 3 x 3).  Without the z rows the
+// flat tetrahedra lying on a face of box_10m kept loose bounds and one
+// rank of eight took 3.2 ms against 2.4 ms for the others.
 // The representatives' bound U of a point in dense data is set by the
 // spacing of a ~reps_target sample of the whole masking ball -- an order of
 // magnitude above the point's nn distance for a long edge or a large hull
@@ -336,9 +338,10 @@ constexpr bool kProbeSkip = FPH_PROBE_SKIP;
 // (looser probe bounds leave phase C more to search than the pass costs)
 constexpr float kProbeTight = FPH_PROBE_TIGHT;
 #ifndef FPH_PROBE_ROWS
-#define FPH_PROBE_ROWS 3
+#define FPH_PROBE_ROWS 5
 #endif
-// rows of cells probed: 1 (the point's own), 3 (its y-neighbours) or 9
+// rows of cells probed: 1 (the point's own), 3 (its y-neighbours), 5 (its y-
+// and z-neighbours) or 9
 constexpr int kProbeRows = FPH_PROBE_ROWS;
 
 __device__ __forceinline__ float local_probe(const Ctx& c, const PointF& q) {
@@ -355,8 +358,10 @@ __device__ __forceinline__ float local_probe(const Ctx& c, const PointF& q) {
     // (fetching every row's run up front: +1-2% on surface data)
     for (int t = 0; t < kProbeRows && left > 0; ++t) {
         // (dy, dz) in the order 0, -1, +1 each: the point's own row first
-        const int dy = (t % 3 == 0) ? 0 : (t % 3 == 1 ? -1 : 1);
-        const int dz = (t / 3 == 0) ? 0 : (t / 3 == 1 ? -1 : 1);
+        // (5 rows: the cross (0, 0), (-1, 0), (+1, 0), (0, -1), (0, +1))
+        const int dy = (kProbeRows == 5 && t >= 3) ? 0 : ((t % 3 == 0) ? 0 : (t % 3 == 1 ? -1 : 1));
+        const int dz = (kProbeRows == 5 && t >= 3) ? (t == 3 ? -1 : 1)
+                                                   : ((t / 3 == 0) ? 0 : (t / 3 == 1 ? -1 : 1));
         const int y = iy + dy, z = iz + dz;
         if (y < 0 || y >= g.ny || z < 0 || z >= g.nz) continue;
         const int base = (z * g.ny + y) * g.nx;

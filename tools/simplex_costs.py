@@ -5,6 +5,7 @@ plus the heaviest simplices -- the ones that bound a shard's time at high
 GPU counts -- against the average load per resident warp.
 
   python tools/simplex_costs.py [--config sphere_torus_1m] [--top 10]
+                                [--world W --rank r]   (one rank's spatial share)
 
 (record fields: cycles A, B, C, F; blocks searched; candidate count;
 candidates staged; team size)
@@ -28,15 +29,20 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="sphere_torus_1m")
     ap.add_argument("--top", type=int, default=10)
+    ap.add_argument("--world", type=int, default=1)
+    ap.add_argument("--rank", type=int, default=0)
     args = ap.parse_args()
+    from paper_2509_22432_b200.parallel import simplex_centers, spatial_partition
     lib = _native.require_gpu()
     w = bench.prepare(args.config, 0)
     X, tri = w["X"], w["tri"]
     lms = np.ascontiguousarray(tri.points)
-    out = {"config": args.config}
+    out = {"config": args.config, "world": args.world, "rank": args.rank}
     clock_ghz = 1.965
     for k in range(1, w["max_dim"] + 1):
         rows = tri.simplices_by_dim[k]
+        if args.world > 1:
+            rows = rows[spatial_partition(simplex_centers(lms, rows), None, args.world)[args.rank]]
         s4 = np.full((rows.shape[0], 4), -1, dtype=np.int32)
         s4[:, : k + 1] = rows
         sq = np.empty(rows.shape[0])
