@@ -799,7 +799,9 @@ int range_prepare(const Grid* d_grid, const double* d_landmarks3, const int* d_s
     }
     long long* d_dbg = nullptr;
     if (rp.search && g_debug) {
-        FPH_CUDA_TRY(cudaMalloc(&d_dbg, sizeof(long long) * kDbgFields * n));
+        // stream-ordered: a plain cudaMalloc here could wait for the device
+        // and serialise the dimensions of the captured run
+        FPH_CUDA_TRY(cudaMallocAsync(&d_dbg, sizeof(long long) * kDbgFields * n, stream));
         FPH_CUDA_TRY(cudaMemsetAsync(d_dbg, 0, sizeof(long long) * kDbgFields * n, stream));
         g_debug_pending.push_back({d_dbg, n, k});
     }
