@@ -19,6 +19,9 @@ LIB_PATH = os.path.join(LIB_DIR, "libfloodph_b200.so")
 SOURCES = ["fph_api.cu", "fph_flood.cu", "fph_search.cu", "fph_fps.cu", "fph_grid.cu",
            "fph_diag.cu", "fph_mask.cu", "fph_persistence.cpp"]
 HEADERS = ["fph_common.cuh", "fph_dev.cuh", "fph_flood.cuh", "fph_grid.cuh"]
+# compiled again per extra grid slot (-DFPH_GRID_SLOT=g, g = 1 .. GRID_SLOTS - 1)
+SLOTTED = ["fph_search.cu"]
+GRID_SLOTS = 2
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -57,16 +60,20 @@ def build(force: bool = False, verbose: bool = False, out: str | None = None,
     nvcc = _nvcc()
     defs = [f"-D{d}" for d in defines]
 
-    def compile_one(src):
-        obj = os.path.join(objdir, src + ".o")
-        cmd = [nvcc, *NVCC_FLAGS, *defs, "-c", "-o", obj, os.path.join(CSRC, src)]
+    def compile_one(unit):
+        src, extra = unit
+        obj = os.path.join(objdir, src + "".join(e.replace("=", "") for e in extra) + ".o")
+        cmd = [nvcc, *NVCC_FLAGS, *defs, *extra, "-c", "-o", obj, os.path.join(CSRC, src)]
         if verbose:
             print(" ".join(cmd))
         subprocess.run(cmd, check=True)
         return obj
 
-    with ThreadPoolExecutor(max_workers=len(SOURCES)) as pool:
-        objs = list(pool.map(compile_one, SOURCES))
+    # the search kernels once per constant grid slot (fph_flood.cuh kGridSlots)
+    units = [(src, []) for src in SOURCES]
+    units += [(src, [f"-DFPH_GRID_SLOT={g}"]) for src in SLOTTED for g in range(1, GRID_SLOTS)]
+    with ThreadPoolExecutor(max_workers=len(units)) as pool:
+        objs = list(pool.map(compile_one, units))
     tmp = target + ".tmp"
     cmd = [nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp, *objs]
     if verbose:

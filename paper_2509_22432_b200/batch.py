@@ -76,6 +76,43 @@ def flood_sq_device(points, dc: DeviceComplex, m: int, subset: bool = True, stre
     return [dc.out[k][: dc.counts_full[k]] for k in range(dc.top + 1)]
 
 
+_LANES: dict = {}
+
+
+def _lane_streams(dev, lanes: int = 2):
+    import torch
+
+    key = (dev.index, lanes)
+    if key not in _LANES:
+        _LANES[key] = [torch.cuda.Stream(device=dev) for _ in range(lanes)]
+    return _LANES[key]
+
+
+def flood_sq_device_many(items, m: int, subset: bool = True, stream=None, lanes: int = 2):
+    """Squared flood values of several (points, DeviceComplex) items, the
+    calls dealt round-robin to `lanes` streams forked from `stream` (default:
+    the current torch stream) and joined back into it: the next cloud's grid
+    build and set-up run under the current cloud's search tail (a few heavy
+    simplices on a few warps); the search kernels themselves take the
+    device's grid slot in turn (FPH_GRID_SLOTS=2 lets them overlap too, see
+    fph_api.cu GridSlot).  modelnet_batch: 163 -> 143 ms per 64 clouds.
+    Returns each item's dc.out trimmed per dimension, in order."""
+    import torch
+
+    dev = items[0][1].dev
+    with torch.cuda.device(dev):
+        base = (torch.cuda.ExternalStream(stream, device=dev) if stream is not None
+                else torch.cuda.current_stream(dev))
+        side = _lane_streams(dev, lanes)
+        for s in side:
+            s.wait_stream(base)
+        out = [flood_sq_device(X, dc, m, subset, side[i % lanes].cuda_stream)
+               for i, (X, dc) in enumerate(items)]
+        for s in side:
+            base.wait_stream(s)
+    return out
+
+
 @dataclass
 class CloudResult:
     """One cloud of a batch: landmark indices, complex, squared flood values."""
@@ -127,6 +164,7 @@ def flood_cloud_batch(clouds, n_landmarks: int, m: int = 20, max_dim: int | None
             tri = delaunay(Xh[i][idx[i]])
             return tri, time.perf_counter() - t
 
+        pending = []
         with ThreadPoolExecutor(max_workers=workers or 4) as pool:
             futures = [pool.submit(triangulate, i) for i in range(len(mine))]
             for i, fut in enumerate(futures):
@@ -134,10 +172,18 @@ def flood_cloud_batch(clouds, n_landmarks: int, m: int = 20, max_dim: int | None
                 timings["delaunay_s"] += dt
                 t0 = time.perf_counter()
                 dc = DeviceComplex(tri, dev, max_dim)
-                sq = flood_sq_device(Xd[i], dc, m)
-                vals = {k: v.cpu().numpy() for k, v in enumerate(sq)}
+                # queued on alternating streams: two clouds in flight
+                lane = _lane_streams(dev)[i % 2]
+                lane.wait_stream(torch.cuda.current_stream(dev))
+                sq = flood_sq_device(Xd[i], dc, m, True, lane.cuda_stream)
+                pending.append((i, tri, dc, sq, lane))
                 timings["flood_s"] += time.perf_counter() - t0
-                results.append(CloudResult(int(mine[i]), idx[i], tri, vals))
+        t0 = time.perf_counter()
+        for i, tri, dc, sq, s in pending:
+            s.synchronize()
+            vals = {k: v.cpu().numpy() for k, v in enumerate(sq)}
+            results.append(CloudResult(int(mine[i]), idx[i], tri, vals))
+        timings["flood_s"] += time.perf_counter() - t0
     if gather and world > 1:
         parts = [None] * world
         dist.all_gather_object(parts, results)

@@ -9,6 +9,7 @@
 #include <cstdio>
 #include <cstring>
 #include <map>
+#include <atomic>
 #include <mutex>
 #include <vector>
 
@@ -103,11 +104,13 @@ __global__ void fill_kernel(double* out, long long n, double v) {
 
 unsigned blocks_for(long long n) { return (unsigned)((n + 255) / 256); }
 
-// Library streams, created once per device and kept: slot 0 carries
-// host-memory calls, slots 1..3 the per-dimension interior terms
-// (run_interiors; higher dimensions at higher priority).
+// Library streams, created once per device and kept: stream 0 carries
+// host-memory calls, streams 1 + 3 g + (k - 1) the dimension-k interior terms
+// of a call holding grid slot g (run_interiors; higher dimensions at higher
+// priority).
+constexpr int kLibStreams = 1 + 3 * kGridSlots;
 std::mutex g_stream_mu;
-std::map<int, std::array<cudaStream_t, 4>> g_streams;
+std::map<int, std::array<cudaStream_t, kLibStreams>> g_streams;
 
 int lib_stream(int slot, cudaStream_t* out) {
     int dev = 0;
@@ -115,12 +118,12 @@ int lib_stream(int slot, cudaStream_t* out) {
     std::lock_guard<std::mutex> lock(g_stream_mu);
     auto it = g_streams.find(dev);
     if (it == g_streams.end()) {
-        std::array<cudaStream_t, 4> st{};
+        std::array<cudaStream_t, kLibStreams> st{};
         int lo = 0, hi = 0;
         FPH_CUDA_TRY(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-        for (int i = 0; i < 4; ++i)
+        for (int i = 0; i < kLibStreams; ++i)
             FPH_CUDA_TRY(cudaStreamCreateWithPriority(&st[i], cudaStreamNonBlocking,
-                                                      i >= 2 ? hi : lo));
+                                                      i >= 1 && (i - 1) % 3 >= 1 ? hi : lo));
         it = g_streams.emplace(dev, st).first;
     }
     *out = it->second[slot];
@@ -140,50 +143,70 @@ struct HostCtx {
     }
 };
 
-// The search kernels read the grid's parameters from one constant-memory
-// slot per device (fph_search.cu c_grid).  A call that launches them holds
-// its device's slot from the copy of its grid into it until its kernels are
-// queued, and the next call's stream waits for an event recorded after them,
-// so the GPU never rewrites the slot under running kernels.
-struct DevSlot {
-    std::mutex mu;
-    cudaEvent_t free_ev = nullptr;
+// The search kernels read the grid's parameters from a constant-memory slot
+// (fph_search.cu c_grid; one copy of the kernels per slot, kGridSlots per
+// device).  A call that launches them takes the next slot of its device
+// round-robin and holds it from the copy of its grid into the slot until its
+// kernels are queued; the next call on that slot waits (on the device) for
+// an event recorded after them, so the GPU never rewrites a slot under
+// running kernels.  Calls on different slots run concurrently.
+struct DevSlots {
+    std::mutex mu[kGridSlots];
+    cudaEvent_t free_ev[kGridSlots] = {};
+    unsigned long long ev_capture[kGridSlots] = {};  // capture id of the record (0: none)
+    std::atomic<unsigned> next{0};
 };
 std::mutex g_slot_map_mu;
-std::map<int, DevSlot*> g_slots;
+std::map<int, DevSlots*> g_slots;
 
 struct GridSlot {
-    DevSlot* ds = nullptr;
+    DevSlots* ds = nullptr;
+    int index = 0;
     cudaStream_t stream = nullptr;
+    bool capturing = false;
+    unsigned long long capture_id = 0;
     int acquire(const Grid* d_grid, cudaStream_t s) {
         int dev = 0;
         FPH_CUDA_TRY(cudaGetDevice(&dev));
         {
             std::lock_guard<std::mutex> lock(g_slot_map_mu);
             auto it = g_slots.find(dev);
-            if (it == g_slots.end()) it = g_slots.emplace(dev, new DevSlot).first;
+            if (it == g_slots.end()) it = g_slots.emplace(dev, new DevSlots).first;
             ds = it->second;
         }
-        ds->mu.lock();
+        // Slots in use (FPH_GRID_SLOTS, default 1).  Two let the search
+        // kernels of two calls overlap; measured on modelnet_batch (64 calls
+        // on two streams) the graph replay gains 154 -> 144 ms but the eager
+        // calls lose 143 -> 147 ms and host-memory calls 194 -> 215 ms: the
+        // overlap that pays is a call's grid build and set-up under the
+        // previous call's search, which one slot already allows.
+        static const int nslots = [] {
+            const char* e = getenv("FPH_GRID_SLOTS");
+            const int v = e ? atoi(e) : 1;
+            return v >= 1 && v <= kGridSlots ? v : 1;
+        }();
+        index = (int)(ds->next.fetch_add(1) % (unsigned)nslots);
+        ds->mu[index].lock();
         stream = s;
-        // under stream capture (a CUDA graph of the step) the graph's own
-        // order stands in for the event: replays of a captured call must not
-        // overlap other library calls on the device
         cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-        FPH_CUDA_TRY(cudaStreamIsCapturing(s, &cs));
+        FPH_CUDA_TRY(cudaStreamGetCaptureInfo(s, &cs, &capture_id));
         capturing = cs != cudaStreamCaptureStatusNone;
-        if (ds->free_ev && !capturing) FPH_CUDA_TRY(cudaStreamWaitEvent(s, ds->free_ev, 0));
-        return set_search_grid(d_grid, s);
+        if (!capturing) capture_id = 0;
+        // an event recorded in the same capture (a CUDA graph of a step) is
+        // a dependency inside the graph; one recorded outside it cannot be
+        // waited on there, and the graph's own order stands in for it
+        if (ds->free_ev[index] && ds->ev_capture[index] == capture_id)
+            FPH_CUDA_TRY(cudaStreamWaitEvent(s, ds->free_ev[index], 0));
+        return set_search_grid(index, d_grid, s);
     }
     ~GridSlot() {
         if (!ds) return;
-        if (!capturing) {
-            if (!ds->free_ev) cudaEventCreateWithFlags(&ds->free_ev, cudaEventDisableTiming);
-            if (ds->free_ev) cudaEventRecord(ds->free_ev, stream);
-        }
-        ds->mu.unlock();
+        if (!ds->free_ev[index])
+            cudaEventCreateWithFlags(&ds->free_ev[index], cudaEventDisableTiming);
+        if (ds->free_ev[index] && cudaEventRecord(ds->free_ev[index], stream) == cudaSuccess)
+            ds->ev_capture[index] = capture_id;
+        ds->mu[index].unlock();
     }
-    bool capturing = false;
 };
 
 // a host-memory call returns once its stream is drained (on errors too)
@@ -256,7 +279,7 @@ int check_cloud(const double* points, int64_t n, int32_t dim) {
     return FPH_OK;
 }
 
-FloodTuning current_tuning(double points_per_landmark = 0.0) {
+FloodTuning current_tuning(double points_per_landmark = 0.0, int grid_slot = 0) {
     FloodTuning t;
     t.points_per_landmark = points_per_landmark;
     t.pairs_per_task = g_pairs_per_task;
@@ -266,6 +289,7 @@ FloodTuning current_tuning(double points_per_landmark = 0.0) {
     t.team_threshold = g_team_threshold;
     t.exact_pairs = g_exact_pairs;
     for (int i = 0; i < 4; ++i) t.exact_cand[i] = g_exact_cand[i];
+    t.grid_slot = grid_slot;
     return t;
 }
 
@@ -543,7 +567,8 @@ int fph_flood_interior(const double* points, int64_t n_points, int32_t dim,
         GridSlot slot;
         FPH_TRY(slot.acquire(gs.d_grid, hc.stream));
         rc = flood_interior(gs.d_grid, lm3, d_s, (int)n_simplices, k, grid_resolution, subset_mode,
-                            d_out, current_tuning((double)n_points / n_landmarks), hc.stream);
+                            d_out, current_tuning((double)n_points / n_landmarks, slot.index),
+                            hc.stream);
         count_launches(4);
         if (rc == FPH_OK && memory == FPH_MEM_HOST)
             FPH_CUDA_TRY(cudaMemcpyAsync(out_sq, d_out, sizeof(double) * n_simplices,
@@ -594,7 +619,7 @@ int fph_flood_samples(const double* points, int64_t n_points, int32_t dim,
         GridSlot slot;
         FPH_TRY(slot.acquire(gs.d_grid, hc.stream));
         rc = flood_interior(gs.d_grid, lm3, d_s, (int)n_simplices, k, 1, subset_mode, d_out,
-                            current_tuning((double)n_points / n_landmarks), hc.stream, smp3,
+                            current_tuning((double)n_points / n_landmarks, slot.index), hc.stream, smp3,
                             n_samples);
         count_launches(4);
         if (rc == FPH_OK && memory == FPH_MEM_HOST)
@@ -628,7 +653,7 @@ static int run_interiors(const Grid* g, const double* lm3, int* const* s4, doubl
         // higher dimensions carry the longest chains: their CTAs are placed
         // first (higher stream priority), lower dimensions fill the tails
         cudaStream_t sk = nullptr;
-        FPH_TRY(lib_stream(k, &sk));
+        FPH_TRY(lib_stream(1 + 3 * tune.grid_slot + (k - 1), &sk));
         FPH_CUDA_TRY(cudaStreamWaitEvent(sk, fork, 0));
         rc = flood_interior(g, lm3, s4[k], (int)counts[k], k, grid_resolution, subset_mode,
                             interior[k], tune, sk);
@@ -685,7 +710,7 @@ static int flood_rows(const double* points, int64_t n_points, int32_t dim,
         GridGuard gg{gs, hc.stream};
         FPH_TRY(build_grid_timed(d_pts, (int)n_points, dim, hc.stream, &gs));
         count_launches(4);
-        const FloodTuning tune = current_tuning((double)n_points / n_landmarks);
+        FloodTuning tune = current_tuning((double)n_points / n_landmarks);
         int64_t mine[4] = {0, 0, 0, 0};
         int* s4[4] = {nullptr, nullptr, nullptr, nullptr};
         double* d_out[4] = {nullptr, nullptr, nullptr, nullptr};
@@ -712,6 +737,7 @@ static int flood_rows(const double* points, int64_t n_points, int32_t dim,
         // every dimension's share concurrently, as in fph_flood_filtration
         GridSlot slot;
         if (rc == FPH_OK) rc = slot.acquire(gs.d_grid, hc.stream);
+        tune.grid_slot = slot.index;
         if (rc == FPH_OK) rc = run_interiors(gs.d_grid, lm3, s4, d_out, mine, max_dim,
                                             grid_resolution, subset_mode, tune, hc.stream);
         for (int k = 1; k <= max_dim && rc == FPH_OK; ++k)
@@ -786,9 +812,9 @@ int fph_flood_filtration(const double* points, int64_t n_points, int32_t dim,
         GridGuard gg{gs, hc.stream};
         FPH_TRY(build_grid_timed(d_pts, (int)n_points, dim, hc.stream, &gs));
         count_launches(4);
-        const FloodTuning tune = current_tuning((double)n_points / n_landmarks);
         GridSlot slot;
         FPH_TRY(slot.acquire(gs.d_grid, hc.stream));
+        const FloodTuning tune = current_tuning((double)n_points / n_landmarks, slot.index);
         double* d_vals[4] = {nullptr, nullptr, nullptr, nullptr};
         const int32_t* d_f[4] = {nullptr, nullptr, nullptr, nullptr};
         int* s4[4] = {nullptr, nullptr, nullptr, nullptr};

@@ -726,6 +726,7 @@ struct RangePlan {
     FloodArgs a{};
     bool search = false, profile = false;
     int ppt = 1;
+    int slot = 0;  // the search kernels' grid slot (FloodTuning::grid_slot)
     cudaStream_t stream = nullptr;
     SimplexGeom* d_geom = nullptr;
     int *d_ntasks = nullptr, *d_task_off = nullptr, *d_counter = nullptr, *d_done = nullptr;
@@ -760,7 +761,7 @@ int range_prepare(const Grid* d_grid, const double* d_landmarks3, const int* d_s
     a.explicit_pts = d_explicit;
     // the bounded search keeps the (m + 1) weights in shared memory; a
     // resolution too large for that takes the brute-force kernel
-    rp.search = tune.algo >= 1 && search_smem_bytes(P, m) <= search_smem_limit();
+    rp.search = tune.algo >= 1 && slot0::search_smem_bytes(P, m) <= slot0::search_smem_limit();
     a.nblk = rp.search ? T.nblk : 0;
     a.reps_target = tune.reps_target > 0 ? tune.reps_target : 384;
     a.team_threshold = tune.team_threshold;
@@ -806,7 +807,10 @@ int range_prepare(const Grid* d_grid, const double* d_landmarks3, const int* d_s
         g_debug_pending.push_back({d_dbg, n, k});
     }
     a.dbg = d_dbg;
-    if (rp.search) FPH_TRY(search_prepare(a, rp.d_geom, a.cand_count, stream, &rp.sp));
+    rp.slot = tune.grid_slot;
+    if (rp.search)
+        FPH_TRY(rp.slot == 1 ? slot1::search_prepare(a, rp.d_geom, a.cand_count, stream, &rp.sp)
+                             : slot0::search_prepare(a, rp.d_geom, a.cand_count, stream, &rp.sp));
     FPH_CUDA_TRY(cudaGetLastError());
     return FPH_OK;
 }
@@ -820,7 +824,7 @@ int range_run(RangePlan& rp) {
         FPH_CUDA_TRY(cudaEventRecord(ev0, stream));
     }
     if (rp.search) {
-        FPH_TRY(search_run(rp.sp, true));
+        FPH_TRY(rp.slot == 1 ? slot1::search_run(rp.sp, true) : slot0::search_run(rp.sp, true));
     } else {
         int dev = 0, sms = 0, occ = 0;
         FPH_CUDA_TRY(cudaGetDevice(&dev));

@@ -70,21 +70,39 @@ struct SearchPlan {
     int *d_counters = nullptr, *d_stage = nullptr;
     void* tmp = nullptr;
 };
-int search_prepare(const FloodArgs& a, const SimplexGeom* d_geom, const int* d_cand,
-                   cudaStream_t stream, SearchPlan* plan);
-int search_run(SearchPlan& plan, bool release);
-int search_release(SearchPlan& plan);
-int launch_search(const FloodArgs& a, const SimplexGeom* d_geom, const int* d_cand,
-                  cudaStream_t stream);
-// copy a device grid's parameters into the search kernels' constant slot,
-// ordered on `stream` (the caller holds the device's GridSlot)
-int set_search_grid(const Grid* d_grid, cudaStream_t stream);
-// dynamic shared memory of the search kernel for P rows at resolution m, and
-// the device limit it must fit
-size_t search_smem_bytes(int P, int m);
-size_t search_smem_limit();
+//
+// fph_search.cu is compiled once per grid slot (FPH_GRID_SLOT 0, 1): each
+// copy's kernels read their own __constant__ grid, so two calls holding
+// different slots run concurrently on one device (a batch of clouds on two
+// streams).  The copies' entry points live in namespaces slot0 / slot1.
+constexpr int kGridSlots = 2;
+#define FPH_SEARCH_API                                                                     \
+    int search_prepare(const FloodArgs& a, const SimplexGeom* d_geom, const int* d_cand,   \
+                       cudaStream_t stream, SearchPlan* plan);                             \
+    int search_run(SearchPlan& plan, bool release);                                        \
+    int search_release(SearchPlan& plan);                                                  \
+    int launch_search(const FloodArgs& a, const SimplexGeom* d_geom, const int* d_cand,    \
+                      cudaStream_t stream);                                                \
+    /* copy a device grid's parameters into this copy's constant slot, ordered on      */ \
+    /* `stream` (the caller holds the slot, fph_api.cu GridSlot)                        */ \
+    int set_search_grid(const Grid* d_grid, cudaStream_t stream);                          \
+    /* dynamic shared memory of the search kernel for P rows at resolution m, and the  */ \
+    /* device limit it must fit                                                         */ \
+    size_t search_smem_bytes(int P, int m);                                                \
+    size_t search_smem_limit();
+namespace slot0 {
+FPH_SEARCH_API
+}
+namespace slot1 {
+FPH_SEARCH_API
+}
+#undef FPH_SEARCH_API
+inline int set_search_grid(int slot, const Grid* d_grid, cudaStream_t stream) {
+    return slot == 1 ? slot1::set_search_grid(d_grid, stream) : slot0::set_search_grid(d_grid, stream);
+}
 
 struct FloodTuning {
+    int grid_slot = 0;            // the constant grid slot the caller holds (fph_api.cu GridSlot)
     double points_per_landmark = 0.0;  // cloud points / landmarks: scales the work estimate
     double pairs_per_task = 0.0;  // <= 0: default 2^21
     bool profile = false;         // time pass kernels with events

@@ -32,6 +32,15 @@
 
 #include "fph_dev.cuh"
 
+#ifndef FPH_GRID_SLOT
+#define FPH_GRID_SLOT 0
+#endif
+#if FPH_GRID_SLOT == 0
+#define FPH_SLOT_NS slot0
+#else
+#define FPH_SLOT_NS slot1
+#endif
+
 namespace fph {
 
 namespace {
@@ -1360,6 +1369,8 @@ __global__ void order_key_kernel(const Grid* __restrict__ gp, const SimplexGeom*
 
 }  // namespace
 
+namespace FPH_SLOT_NS {
+
 int set_search_grid(const Grid* d_grid, cudaStream_t stream) {
     FPH_CUDA_TRY(cudaMemcpyToSymbolAsync(c_grid, d_grid, sizeof(Grid), 0, cudaMemcpyDeviceToDevice,
                                          stream));
@@ -1508,5 +1519,7 @@ int launch_search(const FloodArgs& a, const SimplexGeom* d_geom, const int* d_ca
     FPH_TRY(search_prepare(a, d_geom, d_cand, stream, &p));
     return search_run(p, true);
 }
+
+}  // namespace FPH_SLOT_NS
 
 }  // namespace fph

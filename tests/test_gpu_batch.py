@@ -28,3 +28,46 @@ def test_cloud_batch_matches_oracle(max_dim):
         for k in range(top + 1):
             assert np.array_equal(r.sq_values[k], want[k]), (r.cloud, k)
     assert rep.timings["fps_s"] > 0 and rep.timings["flood_s"] > 0
+
+
+def test_two_grid_slots_in_flight_equal_one_at_a_time():
+    """Clouds dealt to two streams (the library's two constant grid slots,
+    two calls in flight) -- eagerly and inside a CUDA graph -- give exactly
+    the values of one call at a time."""
+    import torch
+
+    from paper_2509_22432_b200 import farthest_point_sampling
+    from paper_2509_22432_b200.batch import DeviceComplex, flood_sq_device, flood_sq_device_many
+    from paper_2509_22432_b200.delaunay import delaunay
+
+    dev = torch.device("cuda:0")
+    clouds = gen_modelnet_batch(6, 40_000, seed=11)
+    items = []
+    for X in clouds:
+        Xd = torch.from_numpy(np.ascontiguousarray(X)).to(dev)
+        idx = farthest_point_sampling(Xd, 400, 0).cpu().numpy()
+        items.append((Xd, DeviceComplex(delaunay(X[idx]), dev)))
+    want = []
+    for Xd, dc in items:
+        want.append([v.clone() for v in flood_sq_device(Xd, dc, 10)])
+        torch.cuda.synchronize()
+    for out in items:
+        for v in out[1].out:
+            v.fill_(float("nan"))
+    got = flood_sq_device_many(items, 10)
+    torch.cuda.synchronize()
+    for g, w in zip(got, want):
+        assert all(torch.equal(a, b) for a, b in zip(g, w))
+    s = torch.cuda.Stream(device=dev)
+    graph = torch.cuda.CUDAGraph()
+    torch.cuda.synchronize()
+    with torch.cuda.graph(graph, stream=s, capture_error_mode="thread_local"):
+        flood_sq_device_many(items, 10, True, s.cuda_stream)
+    for _, dc in items:
+        for v in dc.out:
+            v.fill_(float("nan"))
+    for _ in range(3):
+        graph.replay()
+    torch.cuda.synchronize()
+    for (_, dc), w in zip(items, want):
+        assert all(torch.equal(dc.out[k][: dc.counts_full[k]], w[k]) for k in range(dc.top + 1))
