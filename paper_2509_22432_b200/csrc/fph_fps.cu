@@ -384,17 +384,126 @@ int launch_resident(const double* d_x, const double* d_y, const double* d_z, int
 // ------------------------------------------------------------ tiled variant
 constexpr int kTileP = 256;  // points per tile
 
+// Exchange of the tiled kernel: as exchange_argmax_xyz, with the candidate's
+// coordinates and sorted position taken from the tile that holds it (this
+// CTA's per-tile argmax records in shared memory): the winner arrives with
+// its coordinates and tile, so the next iteration starts without a
+// dependent global load.  `bt`: the tile (local index) of this thread's
+// candidate.
+__device__ __forceinline__ Winner exchange_argmax_tiled(double bv, int bi, int bt,
+                                                        const double* txyz, const int* tpos,
+                                                        SlotXYZ* buf, int G, int slot,
+                                                        unsigned long long* arrived,
+                                                        unsigned long long target, double* red_v,
+                                                        int* red_i, int* red_t, double* stage,
+                                                        int* wpos) {
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    {
+        const int myi = bi;
+        warp_argmax(bv, bi);
+        const unsigned hit = __ballot_sync(0xffffffffu, myi == bi);
+        bt = __shfl_sync(0xffffffffu, bt, hit ? __ffs(hit) - 1 : 0);
+    }
+    if (l == 0) {
+        red_v[w] = bv;
+        red_i[w] = bi;
+        red_t[w] = bt;
+    }
+    __syncthreads();
+    if (w == 0) {
+        double v = l < (int)(blockDim.x >> 5) ? red_v[l] : -INFINITY;
+        int i = l < (int)(blockDim.x >> 5) ? red_i[l] : 0x7fffffff;
+        int t = l < (int)(blockDim.x >> 5) ? red_t[l] : 0;
+        {
+            const int myi = i;
+            warp_argmax(v, i);
+            const unsigned hit = __ballot_sync(0xffffffffu, myi == i);
+            t = __shfl_sync(0xffffffffu, t, hit ? __ffs(hit) - 1 : 0);
+        }
+        if (l == 0) {
+            SlotXYZ sl;
+            sl.val = v;
+            sl.idx = i;
+            // an empty CTA publishes -inf, never the winner: the rest unused
+            const bool any = v > -INFINITY;
+            sl.pad = any ? tpos[t] : 0;
+            sl.x = any ? txyz[3 * t] : 0.0;
+            sl.y = any ? txyz[3 * t + 1] : 0.0;
+            sl.z = any ? txyz[3 * t + 2] : 0.0;
+            sl.pad2 = 0.0;
+            buf[slot] = sl;
+            arrive_release(arrived);
+            while (ld_acquire(arrived) < target) {
+            }
+        }
+        __syncwarp();
+        constexpr int kPer = 5;
+        double sv[kPer];
+        int si[kPer];
+#pragma unroll
+        for (int q = 0; q < kPer; ++q) {
+            const int b = l + 32 * q;
+            if (b < G) {
+                cp_async16(stage + 4 * b, &buf[b].x);
+                cp_async16(stage + 4 * b + 2, &buf[b].z);
+            }
+            sv[q] = b < G ? __ldcg(&buf[b].val) : -INFINITY;
+            si[q] = b < G ? __ldcg(&buf[b].idx) : 0x7fffffff;
+        }
+        v = -INFINITY;
+        i = 0x7fffffff;
+        int bs = 0;
+#pragma unroll
+        for (int q = 0; q < kPer; ++q)
+            if (sv[q] > v || (sv[q] == v && si[q] < i)) {
+                v = sv[q];
+                i = si[q];
+                bs = l + 32 * q;
+            }
+        const int myi = i;
+        warp_argmax(v, i);
+        const int src = __ffs(__ballot_sync(0xffffffffu, myi == i)) - 1;
+        bs = __shfl_sync(0xffffffffu, bs, src);
+        asm volatile("cp.async.wait_all;" ::: "memory");
+        if (l == 0) {
+            red_i[32] = i;
+            red_i[33] = bs;
+            *wpos = __ldcg(&buf[bs].pad);
+        }
+    }
+    __syncthreads();
+    Winner wn;
+    wn.idx = red_i[32];
+    const int bs = red_i[33];
+    wn.x = stage[4 * bs];
+    wn.y = stage[4 * bs + 1];
+    wn.z = stage[4 * bs + 2];
+    return wn;
+}
+
+// Per iteration: one thread per tile tests the tile's box against the new
+// landmark (a tile is touched if it holds the landmark or its box is closer
+// than the tile's largest running minimum), the touched tiles go to a
+// shared list, and the warps update them (each lane's points loaded before
+// any running minimum is stored back); the tile's argmax, with its
+// coordinates and sorted position, is kept in shared memory for the
+// exchange.
 __global__ void __launch_bounds__(kFpsThreads, 1)
     fps_tiled_kernel(const double* __restrict__ px, const double* __restrict__ py,
                      const double* __restrict__ pz, const double* __restrict__ sx,
                      const double* __restrict__ sy, const double* __restrict__ sz,
                      const int* __restrict__ sidx, const int* __restrict__ spos,
                      const double* __restrict__ tbox, int n, int k, int start, int per_cta,
-                     int ntiles, double* __restrict__ md, Slot* slots, unsigned long long* arrived,
+                     int ntiles,
+                     double* __restrict__ md, SlotXYZ* slots, unsigned long long* arrived,
                      long long* __restrict__ out) {
     extern __shared__ double sm[];
     __shared__ double red_v[32];
-    __shared__ int red_i[33];
+    __shared__ int red_i[34];
+    __shared__ int red_t[32];
+    __shared__ __align__(16) double stage[4 * kMaxSlots];
+    __shared__ int wpos;
+    __shared__ int cnt[2];
     // tiles are dealt round-robin (tile = blockIdx.x + t * G): the few tiles
     // near a new landmark are Morton neighbours, so they land on different
     // CTAs instead of piling onto one
@@ -402,25 +511,31 @@ __global__ void __launch_bounds__(kFpsThreads, 1)
     const int nt = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / G + 1 : 0;
     double* box = sm;                   // nt x 6
     double* tmax = sm + 6 * per_cta;    // nt
-    int* targ = reinterpret_cast<int*>(tmax + per_cta);
+    double* txyz = tmax + per_cta;      // nt x 3: the tile argmax's coordinates
+    int* targ = reinterpret_cast<int*>(txyz + 3 * per_cta);  // its cloud index
+    int* tpos = targ + per_cta;                                // its sorted position
+    int* list = tpos + per_cta;                                // touched tiles
     for (int t = threadIdx.x; t < nt; t += blockDim.x) {
         for (int c = 0; c < 6; ++c) box[t * 6 + c] = tbox[(size_t)(blockIdx.x + t * G) * 6 + c];
         tmax[t] = INFINITY;
         targ[t] = 0x7fffffff;
+        tpos[t] = 0;
     }
     for (int t = 0; t < nt; ++t) {
         const long long base = (long long)(blockIdx.x + t * G) * kTileP;
         for (int j = threadIdx.x; j < kTileP; j += blockDim.x)
             if (base + j < n) md[base + j] = INFINITY;
     }
+    if (threadIdx.x < 2) cnt[threadIdx.x] = 0;
     __syncthreads();
     const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
     int cur = start;
+    double qx = px[start], qy = py[start], qz = pz[start];  // later ones come with the exchange
+    int ctile = spos[start] / kTileP;
     if (blockIdx.x == 0 && threadIdx.x == 0) out[0] = start;
     for (int it = 1; it < k; ++it) {
-        const double qx = px[cur], qy = py[cur], qz = pz[cur];
-        const int ctile = spos[cur] / kTileP;
-        for (int t = w; t < nt; t += kFpsThreads / 32) {
+        const int c = it & 1;
+        for (int t = threadIdx.x; t < nt; t += blockDim.x) {
             const int tile = blockIdx.x + t * G;
             const double* b = box + t * 6;
             const double dx = fmax(0.0, fmax(b[0] - qx, qx - b[3]));
@@ -428,33 +543,75 @@ __global__ void __launch_bounds__(kFpsThreads, 1)
             const double dz = fmax(0.0, fmax(b[2] - qz, qz - b[5]));
             // a safe lower bound on sq64(x, q) for every x in the box
             const double lb = (dx * dx + dy * dy + dz * dz) * (1.0 - 1e-12);
-            if (tile != ctile && !(lb < tmax[t])) continue;  // nothing in it can change
+            if (tile == ctile || lb < tmax[t]) list[atomicAdd(&cnt[c], 1)] = t;
+        }
+        __syncthreads();
+        const int ntouch = cnt[c];
+        for (int q = w; q < ntouch; q += kFpsThreads / 32) {
+            const int t = list[q];
+            const long long base = (long long)(blockIdx.x + t * G) * kTileP;
             double v = -INFINITY;
-            int i = 0x7fffffff;
-            const long long base = (long long)tile * kTileP;
-            for (int j = l; j < kTileP; j += 32) {
-                const long long pp = base + j;
-                if (pp < n) {
-                    const int oi = sidx[pp];
-                    const double d = sq64(sx[pp], sy[pp], sz[pp], qx, qy, qz);
-                    const double m = oi == cur ? -1.0 : fmin(md[pp], d);
-                    md[pp] = m;
-                    better(v, i, m, oi);
+            int i = 0x7fffffff, bp = 0;
+#pragma unroll
+            for (int h = 0; h < kTileP / 32; h += 4) {
+                long long pp[4];
+                int oi[4];
+                double d[4], mo[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    pp[u] = base + l + 32 * (h + u);
+                    const bool in = pp[u] < n;
+                    oi[u] = in ? sidx[pp[u]] : 0x7fffffff;
+                    d[u] = in ? sq64(sx[pp[u]], sy[pp[u]], sz[pp[u]], qx, qy, qz) : -INFINITY;
+                    mo[u] = in ? md[pp[u]] : -INFINITY;
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    if (pp[u] < n) {
+                        const double m = oi[u] == cur ? -1.0 : fmin(mo[u], d[u]);
+                        md[pp[u]] = m;
+                        if (m > v || (m == v && oi[u] < i)) {
+                            v = m;
+                            i = oi[u];
+                            bp = (int)pp[u];
+                        }
+                    }
                 }
             }
+            const int myi = i;
             warp_argmax(v, i);
+            const unsigned hit = __ballot_sync(0xffffffffu, myi == i);
+            const int src = hit ? __ffs(hit) - 1 : 0;
+            bp = __shfl_sync(0xffffffffu, bp, src);
             if (l == 0) {
                 tmax[t] = v;
                 targ[t] = i;
+                tpos[t] = bp;
+                if (v > -INFINITY) {  // the argmax point was just loaded: an L1 hit
+                    txyz[3 * t] = sx[bp];
+                    txyz[3 * t + 1] = sy[bp];
+                    txyz[3 * t + 2] = sz[bp];
+                }
             }
         }
+        if (threadIdx.x == 0) cnt[c ^ 1] = 0;  // the next iteration's list
         __syncthreads();
         double v = -INFINITY;
-        int i = 0x7fffffff;
-        for (int t = threadIdx.x; t < nt; t += blockDim.x) better(v, i, tmax[t], targ[t]);
-        const int rs = repl_stride(G);
-        cur = exchange_argmax(v, i, slots + (it & 1) * kRepl * rs, G, blockIdx.x, arrived,
-                              (unsigned long long)G * it, red_v, red_i, rs, kRepl);
+        int i = 0x7fffffff, bt = 0;
+        for (int t = threadIdx.x; t < nt; t += blockDim.x)
+            if (tmax[t] > v || (tmax[t] == v && targ[t] < i)) {
+                v = tmax[t];
+                i = targ[t];
+                bt = t;
+            }
+        const Winner wn = exchange_argmax_tiled(v, i, bt, txyz, tpos, slots + (it & 1) * kMaxSlots, G,
+                                                blockIdx.x, arrived, (unsigned long long)G * it,
+                                                red_v, red_i, red_t, stage, &wpos);
+        cur = wn.idx;
+        qx = wn.x;
+        qy = wn.y;
+        qz = wn.z;
+        ctile = wpos / kTileP;
         if (blockIdx.x == 0 && threadIdx.x == 0) out[it] = cur;
     }
 }
@@ -589,10 +746,14 @@ int fps_tiled(const double* d_x, const double* d_y, const double* d_z, int n, in
                                                               spos);
     tile_box_kernel<<<(ntiles * 32 + 255) / 256, 256, 0, stream>>>(sx, sy, sz, n, ntiles, tbox);
     const int per_cta = (ntiles + G - 1) / G;
-    const size_t smem = sizeof(double) * 7 * per_cta + sizeof(int) * per_cta + 16;
-    Slot* slots = nullptr;
+    const size_t smem = sizeof(double) * 10 * per_cta + sizeof(int) * 3 * per_cta + 16;
+    if (G > kMaxSlots) {
+        set_error("fps: %d CTAs exceed the exchange's %d slots", G, kMaxSlots);
+        return FPH_EARG;
+    }
+    SlotXYZ* slots = nullptr;
     unsigned long long* arrived = nullptr;
-    FPH_TRY(sc.alloc(&slots, 2 * kRepl * repl_stride(G)));
+    FPH_TRY(sc.alloc(&slots, 2 * kMaxSlots));
     FPH_TRY(sc.alloc(&arrived, 1));
     FPH_CUDA_TRY(cudaMemsetAsync(arrived, 0, sizeof(unsigned long long), stream));
     FPH_CUDA_TRY(cudaFuncSetAttribute(fps_tiled_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
