@@ -488,7 +488,18 @@ __device__ __forceinline__ Winner exchange_argmax_tiled(double bv, int bi, int b
 // any running minimum is stored back); the tile's argmax, with its
 // coordinates and sorted position, is kept in shared memory for the
 // exchange.
-__global__ void __launch_bounds__(kFpsThreads, 1)
+#ifndef FPH_FPS_TILED_NT
+#define FPH_FPS_TILED_NT 512
+#endif
+#ifndef FPH_FPS_TILED_U
+#define FPH_FPS_TILED_U 8
+#endif
+// 512 threads (128 registers): a lane loads all 8 of its points of a
+// touched tile in one round trip
+constexpr int kTiledNT = FPH_FPS_TILED_NT;
+constexpr int kTiledU = FPH_FPS_TILED_U;  // points per lane loaded together
+
+__global__ void __launch_bounds__(kTiledNT, 1)
     fps_tiled_kernel(const double* __restrict__ px, const double* __restrict__ py,
                      const double* __restrict__ pz, const double* __restrict__ sx,
                      const double* __restrict__ sy, const double* __restrict__ sz,
@@ -547,18 +558,18 @@ __global__ void __launch_bounds__(kFpsThreads, 1)
         }
         __syncthreads();
         const int ntouch = cnt[c];
-        for (int q = w; q < ntouch; q += kFpsThreads / 32) {
+        for (int q = w; q < ntouch; q += kTiledNT / 32) {
             const int t = list[q];
             const long long base = (long long)(blockIdx.x + t * G) * kTileP;
             double v = -INFINITY;
             int i = 0x7fffffff, bp = 0;
 #pragma unroll
-            for (int h = 0; h < kTileP / 32; h += 4) {
-                long long pp[4];
-                int oi[4];
-                double d[4], mo[4];
+            for (int h = 0; h < kTileP / 32; h += kTiledU) {
+                long long pp[kTiledU];
+                int oi[kTiledU];
+                double d[kTiledU], mo[kTiledU];
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {
+                for (int u = 0; u < kTiledU; ++u) {
                     pp[u] = base + l + 32 * (h + u);
                     const bool in = pp[u] < n;
                     oi[u] = in ? sidx[pp[u]] : 0x7fffffff;
@@ -566,7 +577,7 @@ __global__ void __launch_bounds__(kFpsThreads, 1)
                     mo[u] = in ? md[pp[u]] : -INFINITY;
                 }
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {
+                for (int u = 0; u < kTiledU; ++u) {
                     if (pp[u] < n) {
                         const double m = oi[u] == cur ? -1.0 : fmin(mo[u], d[u]);
                         md[pp[u]] = m;
@@ -763,7 +774,7 @@ int fps_tiled(const double* d_x, const double* d_y, const double* d_z, int n, in
                     (void*)&sz,   (void*)&sidx, (void*)&spos,  (void*)&tbox,    (void*)&n,
                     (void*)&k,    (void*)&start, (void*)&per_cta, (void*)&ntl,  (void*)&md,
                     (void*)&slots, (void*)&arrived, (void*)&d_out};
-    FPH_CUDA_TRY(cudaLaunchCooperativeKernel((void*)fps_tiled_kernel, dim3(G), dim3(kFpsThreads),
+    FPH_CUDA_TRY(cudaLaunchCooperativeKernel((void*)fps_tiled_kernel, dim3(G), dim3(kTiledNT),
                                              args, smem, stream));
     FPH_CUDA_TRY(cudaGetLastError());
     return FPH_OK;
