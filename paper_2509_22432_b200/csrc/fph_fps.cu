@@ -889,7 +889,12 @@ int fps_run(const double* d_x, const double* d_y, const double* d_z, int n, int 
         smem = (size_t)chunk * 3 * sizeof(double);
         use_smem = true;
     }
-    if (!use_smem && k > 1) return fps_tiled(d_x, d_y, d_z, n, k, start, d_out, G, stream);
+    static const bool force_tiled = [] {  // experiments: the tiled kernel at any size
+        const char* e = getenv("FPH_FPS_TILED");
+        return e && e[0] == '1';
+    }();
+    if ((!use_smem || force_tiled) && k > 1 && n >= 4096)
+        return fps_tiled(d_x, d_y, d_z, n, k, start, d_out, G, stream);
     Scratch sc(stream);
     Slot* slots = nullptr;
     double* mind = nullptr;
