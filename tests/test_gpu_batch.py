@@ -71,3 +71,40 @@ def test_two_grid_slots_in_flight_equal_one_at_a_time():
     torch.cuda.synchronize()
     for (_, dc), w in zip(items, want):
         assert all(torch.equal(dc.out[k][: dc.counts_full[k]], w[k]) for k in range(dc.top + 1))
+
+
+def test_second_grid_slot_kernels_bit_exact():
+    """FPH_GRID_SLOTS=2 (both compiled copies of the search kernels in use,
+    two calls' searches in flight): the same values as one call at a time.
+    Run in a fresh process, since the slot count is read once per process."""
+    import os
+    import subprocess
+    import sys
+
+    script = r'''
+import numpy as np, torch
+from paper_2509_22432_b200 import farthest_point_sampling
+from paper_2509_22432_b200.batch import DeviceComplex, flood_sq_device, flood_sq_device_many
+from paper_2509_22432_b200.datagen import gen_modelnet_batch
+from paper_2509_22432_b200.delaunay import delaunay
+dev = torch.device("cuda:0")
+items = []
+for X in gen_modelnet_batch(5, 30_000, seed=3):
+    Xd = torch.from_numpy(np.ascontiguousarray(X)).to(dev)
+    idx = farthest_point_sampling(Xd, 300, 0).cpu().numpy()
+    items.append((Xd, DeviceComplex(delaunay(X[idx]), dev)))
+want = []
+for Xd, dc in items:
+    want.append([v.clone() for v in flood_sq_device(Xd, dc, 9)])
+    torch.cuda.synchronize()
+for _ in range(2):
+    got = flood_sq_device_many(items, 9)
+    torch.cuda.synchronize()
+    assert all(torch.equal(a, b) for g, w in zip(got, want) for a, b in zip(g, w))
+print("ok")
+'''
+    env = dict(os.environ, FPH_GRID_SLOTS="2")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", script], env=env, cwd=root, capture_output=True,
+                       text=True, timeout=600)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stderr[-2000:]
