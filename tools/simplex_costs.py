@@ -70,6 +70,12 @@ def main():
             "top1pct_share": float(tot[top1].sum() / tot.sum()),
             "phase_share": [float(d[:, i].sum() / tot.sum()) for i in range(4)],
             "team_simplices": int((d[:, 7] > 1).sum()),
+            # simplices valued by one exact pass in phase A (no B / C work)
+            "exact_pass_simplices": int(((d[:, 1] == 0) & (d[:, 2] == 0)).sum()),
+            "exact_pass_share_of_A": float(d[(d[:, 1] == 0) & (d[:, 2] == 0), 0].sum() /
+                                           max(d[:, 0].sum(), 1)),
+            "exact_pass_share_of_all": float(d[(d[:, 1] == 0) & (d[:, 2] == 0), :4].sum() /
+                                             max(tot.sum(), 1)),
             "cost_vs_cand_loglog_slope": float(np.polyfit(np.log(np.maximum(d[:, 5], 1)),
                                                           np.log(np.maximum(tot, 1)), 1)[0]),
             "cost_per_cand_by_cand_decile": [
