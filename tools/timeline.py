@@ -26,19 +26,31 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="sphere_torus_1m")
     ap.add_argument("--bins", type=int, default=60)
+    ap.add_argument("--world", type=int, default=1)
+    ap.add_argument("--rank", type=int, default=0)
     args = ap.parse_args()
     lib = _native.require_gpu()
     w = bench.prepare(args.config, 0)
     Xd, dc = w["items"][0]
+    call = lambda: flood_sq_device(Xd, dc, w["m"])  # noqa: E731
+    if args.world > 1:  # one rank's spatial share (fph_flood_subset)
+        from paper_2509_22432_b200.parallel import simplex_centers, spatial_partition, subset_interior
+
+        tri = w["tri"]
+        by_dim = {0: torch.arange(dc.counts_full[0], dtype=torch.int32, device=dc.dev), **dc.simp}
+        parts = {k: torch.from_numpy(spatial_partition(simplex_centers(tri.points, tri.simplices_by_dim[k]),
+                                                       None, args.world)[args.rank]).to(dc.dev)
+                 for k in range(1, dc.top + 1)}
+        call = lambda: subset_interior(Xd, dc.lm, by_dim, dc.top, w["m"], True, parts)  # noqa: E731
     for _ in range(3):
-        flood_sq_device(Xd, dc, w["m"])
+        call()
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dc.dev)
     flush.zero_()
     torch.cuda.synchronize()
     lib.fph_debug_simplex_cycles(1, None, 0, None)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    flood_sq_device(Xd, dc, w["m"])
+    call()
     e1.record()
     torch.cuda.synchronize()
     n = np.zeros(1, dtype=np.int64)
@@ -74,7 +86,8 @@ def main():
                     if ov > 0:
                         busy[i] += t * ov / (edges[i + 1] - edges[i])
     capacity = 2368.0
-    out = {"config": args.config, "step_ms_events": e0.elapsed_time(e1),
+    out = {"config": args.config, "world": args.world, "rank": args.rank,
+           "step_ms_events": e0.elapsed_time(e1),
            "first_claim_to_last_publish_us": span_us,
            "busy_warps_by_bin": [round(float(b), 1) for b in busy],
            "bin_us": float(edges[1] - edges[0]), "capacity_warps": capacity,
