@@ -223,9 +223,10 @@ int grid_build(const double* d_pts, int n, int dim, double cell_size, double occ
         FPH_TRY(sc.alloc(&cursor, cap));
         FPH_CUDA_TRY(cudaMemsetAsync(cursor, 0, sizeof(int) * cap, stream));
     }
-    FPH_CUDA_TRY(cudaMallocAsync(&gs->x, sizeof(double) * n, stream));
-    FPH_CUDA_TRY(cudaMallocAsync(&gs->y, sizeof(double) * n, stream));
-    FPH_CUDA_TRY(cudaMallocAsync(&gs->z, sizeof(double) * n, stream));
+    // +2: a 16-byte aligned bulk copy of a run may read one point past the end
+    FPH_CUDA_TRY(cudaMallocAsync(&gs->x, sizeof(double) * (n + 2), stream));
+    FPH_CUDA_TRY(cudaMallocAsync(&gs->y, sizeof(double) * (n + 2), stream));
+    FPH_CUDA_TRY(cudaMallocAsync(&gs->z, sizeof(double) * (n + 2), stream));
     FPH_CUDA_TRY(cudaMallocAsync(&gs->cell_start, sizeof(int) * (cap + 1), stream));
     FPH_CUDA_TRY(cudaMallocAsync(&gs->d_grid, sizeof(Grid), stream));
     if (keep_index) FPH_CUDA_TRY(cudaMallocAsync(&gs->idx, sizeof(int) * n, stream));

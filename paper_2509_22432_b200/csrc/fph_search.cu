@@ -47,8 +47,11 @@ namespace {
 
 constexpr int kSW = 8;          // warps per CTA
 constexpr int kSThreads = 32 * kSW;
+#ifndef FPH_STAGE_BULK
+#define FPH_STAGE_BULK 0
+#endif
 #ifndef FPH_WT
-#define FPH_WT 512
+#define FPH_WT (FPH_STAGE_BULK ? 256 : 512)  // bulk staging: the buffers take the difference
 #endif
 #ifndef FPH_SEARCH_MINB
 #define FPH_SEARCH_MINB 2
@@ -76,7 +79,24 @@ constexpr double kSpreadRatio = FPH_SPREAD_RATIO;
 // phase C: sampling passes a large block region may get before its exact pass
 constexpr int kSamplePasses = FPH_SAMPLE_PASSES;
 
+// 1: phase C's exact pass stages each window of candidates with bulk copies
+// (cp.async.bulk, the TMA engine's 1-D form): every lane copies the piece of
+// its grid row's run that falls in the window, 16-byte aligned (up to one
+// neighbouring point either side -- real cloud points, filtered like any
+// other), completing on the warp's mbarrier; the candidates are then read
+// from shared memory in order, without window_index.
+constexpr bool kStageBulk = FPH_STAGE_BULK;
+constexpr int kBulkW = 96;            // real candidates per window
+constexpr int kBulkN = kBulkW + 64;   // + alignment padding (<= 2 per piece)
+
 struct WarpSmem {
+#if FPH_STAGE_BULK
+    __align__(16) double bx[kBulkN];
+    __align__(16) double by[kBulkN];
+    __align__(16) double bz[kBulkN];
+    unsigned long long bar;  // the warp's mbarrier
+    unsigned bphase;         // its current phase parity
+#endif
     float4 tA[kWT / 2];  // pair p: (c0.x, c1.x, c0.y, c1.y)
     float4 tB[kWT / 2];  //         (c0.z, c1.z, |c0|^2, |c1|^2)
     int row_off[32];
@@ -393,6 +413,36 @@ __device__ __forceinline__ float local_probe(const Ctx& c, const PointF& q) {
     }
     return best < INFINITY ? best + q.bb : INFINITY;  // m32, as the folds give it
 }
+
+__device__ __forceinline__ void rel_of(const Ctx& c, double x, double y, double z, float& ax,
+                                       float& ay, float& az, float& aw) {
+    ax = __double2float_rn(__dsub_rn(x, c.G.cx));
+    ay = __double2float_rn(__dsub_rn(y, c.G.cy));
+    az = __double2float_rn(__dsub_rn(z, c.G.cz));
+    aw = fmaf(az, az, fmaf(ay, ay, ax * ax));
+}
+
+#if FPH_STAGE_BULK
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, void* bar) {
+    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+    const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(d),
+        "l"(src), "r"(bytes), "r"(b)
+        : "memory");
+}
+__device__ __forceinline__ void bar_expect(void* bar, unsigned bytes) {
+    const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bar_wait(void* bar, unsigned parity) {
+    const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
+    asm volatile(
+        "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra WAIT_%=;\n}" ::"r"(b), "r"(parity)
+        : "memory");
+}
+#endif
 
 // append the kept candidates of the warp to the tile; returns the new size
 __device__ __forceinline__ int tile_push(WarpSmem& W, int n, bool keep, float ax, float ay,
@@ -808,7 +858,52 @@ __device__ void search_block(const Ctx& c, WarpSmem& W, int nb, float* vals, flo
             for (int rb = tm.rank * 32; rb < rows; rb += tm.size * 32) {
                 const Batch bt = row_batch(rw, W, rb);
                 const int total = bt.total;
-                if (stride == 1) {
+                if (stride == 1 && kStageBulk) {
+#if FPH_STAGE_BULK
+                    for (int f0 = 0; f0 < total; f0 += kBulkW) {
+                        const int fe = min(f0 + kBulkW, total);
+                        int ps = 0, pe = 0;  // this lane's run piece, sorted indices
+                        if (lane < bt.nne) {
+                            const int ro = W.row_off[lane];
+                            const int re = lane + 1 < bt.nne ? W.row_off[lane + 1] : total;
+                            const int lo = max(ro, f0), hi = min(re, fe);
+                            if (hi > lo) {
+                                ps = W.row_beg[lane] + (lo - ro);
+                                pe = ps + (hi - lo);
+                            }
+                        }
+                        const int as = ps & ~1, ae = (pe + 1) & ~1;
+                        const int len = pe > ps ? ae - as : 0;
+                        int incl = len;
+#pragma unroll
+                        for (int o = 1; o < 32; o <<= 1) {
+                            const int t = __shfl_up_sync(0xffffffffu, incl, o);
+                            if (lane >= o) incl += t;
+                        }
+                        const int off = incl - len;
+                        const int tot = __shfl_sync(0xffffffffu, incl, 31);
+                        // the previous window's shared reads before the async writes
+                        __syncwarp();
+                        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                        if (lane == 0) bar_expect(&W.bar, (unsigned)tot * 24u);
+                        if (len > 0) {
+                            bulk_g2s(W.bx + off, c_grid.x + as, (unsigned)len * 8u, &W.bar);
+                            bulk_g2s(W.by + off, c_grid.y + as, (unsigned)len * 8u, &W.bar);
+                            bulk_g2s(W.bz + off, c_grid.z + as, (unsigned)len * 8u, &W.bar);
+                        }
+                        bar_wait(&W.bar, W.bphase);
+                        __syncwarp();
+                        if (lane == 0) W.bphase ^= 1u;
+                        for (int g0 = 0; g0 < tot; g0 += 32) {
+                            const int g = g0 + lane;
+                            const bool v = g < tot;
+                            float x = 0.f, y = 0.f, z = 0.f, ww = 0.f;
+                            if (v) rel_of(c, W.bx[g], W.by[g], W.bz[g], x, y, z, ww);
+                            take(v && accept(x, y, z, ww), x, y, z, ww);
+                        }
+                    }
+#endif
+                } else if (stride == 1) {
                     // two windows in flight: both loads issue before either is used
                     for (int f0 = 0; f0 < total; f0 += 64) {
                         const int i0 = window_index(W, bt, f0);
@@ -1164,6 +1259,15 @@ __global__ void __launch_bounds__(kSThreads, FPH_SEARCH_MINB)
     for (int i = threadIdx.x; i <= a.m; i += blockDim.x) wt[i] = __ddiv_rn((double)i, (double)a.m);
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     WarpSmem& W = S.w[w];
+#if FPH_STAGE_BULK
+    if (lane == 0) {
+        const unsigned b = (unsigned)__cvta_generic_to_shared(&W.bar);
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(b) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        W.bphase = 0;
+    }
+    __syncwarp();
+#endif
     const long long team_thr = a.team_thr_dev ? *a.team_thr_dev : (long long)a.team_threshold;
     // team mode: the whole CTA per simplex while the queue (sorted by
     // candidate count, largest first) holds big simplices; then warp mode.
