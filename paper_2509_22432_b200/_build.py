@@ -21,7 +21,9 @@ SOURCES = ["fph_api.cu", "fph_flood.cu", "fph_search.cu", "fph_fps.cu", "fph_gri
 HEADERS = ["fph_common.cuh", "fph_dev.cuh", "fph_flood.cuh", "fph_grid.cuh"]
 # compiled again per extra grid slot (-DFPH_GRID_SLOT=g, g = 1 .. GRID_SLOTS - 1)
 SLOTTED = ["fph_search.cu"]
-GRID_SLOTS = 2
+GRID_SLOTS = 3
+# slot 2: the build for clouds beyond L2 (fph_flood.cuh kBigSlot)
+SLOT_DEFINES = {2: ["-DFPH_SEARCH_MINB=3", "-DFPH_WT=256", "-DFPH_VALS_CAP=512"]}
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -62,7 +64,7 @@ def build(force: bool = False, verbose: bool = False, out: str | None = None,
 
     def compile_one(unit):
         src, extra = unit
-        obj = os.path.join(objdir, src + "".join(e.replace("=", "") for e in extra) + ".o")
+        obj = os.path.join(objdir, src + "".join(e.replace("=", "").replace("-D", "_") for e in extra) + ".o")
         cmd = [nvcc, *NVCC_FLAGS, *defs, *extra, "-c", "-o", obj, os.path.join(CSRC, src)]
         if verbose:
             print(" ".join(cmd))
@@ -71,7 +73,8 @@ def build(force: bool = False, verbose: bool = False, out: str | None = None,
 
     # the search kernels once per constant grid slot (fph_flood.cuh kGridSlots)
     units = [(src, []) for src in SOURCES]
-    units += [(src, [f"-DFPH_GRID_SLOT={g}"]) for src in SLOTTED for g in range(1, GRID_SLOTS)]
+    units += [(src, [f"-DFPH_GRID_SLOT={g}", *SLOT_DEFINES.get(g, [])]) for src in SLOTTED
+              for g in range(1, GRID_SLOTS)]
     with ThreadPoolExecutor(max_workers=len(units)) as pool:
         objs = list(pool.map(compile_one, units))
     tmp = target + ".tmp"

@@ -165,7 +165,10 @@ struct GridSlot {
     cudaStream_t stream = nullptr;
     bool capturing = false;
     unsigned long long capture_id = 0;
-    int acquire(const Grid* d_grid, cudaStream_t s) {
+    // cloud_bytes: the call's cloud (n x dim float64); clouds of at least
+    // FPH_BIG_MIN_BYTES (default 64 MiB, i.e. beyond L2 once binned) take
+    // the big-cloud build of the search kernels (kBigSlot)
+    int acquire(const Grid* d_grid, cudaStream_t s, size_t cloud_bytes) {
         int dev = 0;
         FPH_CUDA_TRY(cudaGetDevice(&dev));
         {
@@ -183,9 +186,14 @@ struct GridSlot {
         static const int nslots = [] {
             const char* e = getenv("FPH_GRID_SLOTS");
             const int v = e ? atoi(e) : 1;
-            return v >= 1 && v <= kGridSlots ? v : 1;
+            return v >= 1 && v <= 2 ? v : 1;
         }();
-        index = (int)(ds->next.fetch_add(1) % (unsigned)nslots);
+        static const size_t big_bytes = [] {
+            const char* e = getenv("FPH_BIG_MIN_BYTES");
+            return e ? (size_t)atoll(e) : ((size_t)64 << 20);
+        }();
+        index = cloud_bytes >= big_bytes ? kBigSlot
+                                         : (int)(ds->next.fetch_add(1) % (unsigned)nslots);
         ds->mu[index].lock();
         stream = s;
         cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
@@ -565,7 +573,7 @@ int fph_flood_interior(const double* points, int64_t n_points, int32_t dim,
         double* d_out = out_sq;
         if (memory == FPH_MEM_HOST) FPH_TRY(sc.alloc(&d_out, n_simplices));
         GridSlot slot;
-        FPH_TRY(slot.acquire(gs.d_grid, hc.stream));
+        FPH_TRY(slot.acquire(gs.d_grid, hc.stream, (size_t)n_points * dim * sizeof(double)));
         rc = flood_interior(gs.d_grid, lm3, d_s, (int)n_simplices, k, grid_resolution, subset_mode,
                             d_out, current_tuning((double)n_points / n_landmarks, slot.index),
                             hc.stream);
@@ -617,7 +625,7 @@ int fph_flood_samples(const double* points, int64_t n_points, int32_t dim,
         double* d_out = out_sq;
         if (memory == FPH_MEM_HOST) FPH_TRY(sc.alloc(&d_out, n_simplices));
         GridSlot slot;
-        FPH_TRY(slot.acquire(gs.d_grid, hc.stream));
+        FPH_TRY(slot.acquire(gs.d_grid, hc.stream, (size_t)n_points * dim * sizeof(double)));
         rc = flood_interior(gs.d_grid, lm3, d_s, (int)n_simplices, k, 1, subset_mode, d_out,
                             current_tuning((double)n_points / n_landmarks, slot.index), hc.stream, smp3,
                             n_samples);
@@ -736,7 +744,7 @@ static int flood_rows(const double* points, int64_t n_points, int32_t dim,
         }
         // every dimension's share concurrently, as in fph_flood_filtration
         GridSlot slot;
-        if (rc == FPH_OK) rc = slot.acquire(gs.d_grid, hc.stream);
+        if (rc == FPH_OK) rc = slot.acquire(gs.d_grid, hc.stream, (size_t)n_points * dim * sizeof(double));
         tune.grid_slot = slot.index;
         if (rc == FPH_OK) rc = run_interiors(gs.d_grid, lm3, s4, d_out, mine, max_dim,
                                             grid_resolution, subset_mode, tune, hc.stream);
@@ -813,7 +821,7 @@ int fph_flood_filtration(const double* points, int64_t n_points, int32_t dim,
         FPH_TRY(build_grid_timed(d_pts, (int)n_points, dim, hc.stream, &gs));
         count_launches(4);
         GridSlot slot;
-        FPH_TRY(slot.acquire(gs.d_grid, hc.stream));
+        FPH_TRY(slot.acquire(gs.d_grid, hc.stream, (size_t)n_points * dim * sizeof(double)));
         const FloodTuning tune = current_tuning((double)n_points / n_landmarks, slot.index);
         double* d_vals[4] = {nullptr, nullptr, nullptr, nullptr};
         const int32_t* d_f[4] = {nullptr, nullptr, nullptr, nullptr};

@@ -761,7 +761,11 @@ int range_prepare(const Grid* d_grid, const double* d_landmarks3, const int* d_s
     a.explicit_pts = d_explicit;
     // the bounded search keeps the (m + 1) weights in shared memory; a
     // resolution too large for that takes the brute-force kernel
-    rp.search = tune.algo >= 1 && slot0::search_smem_bytes(P, m) <= slot0::search_smem_limit();
+    const int gslot = tune.grid_slot;
+    const size_t sbytes = gslot == 2 ? slot2::search_smem_bytes(P, m)
+                                     : slot0::search_smem_bytes(P, m);  // slots 0, 1: one build
+    const size_t slimit = gslot == 2 ? slot2::search_smem_limit() : slot0::search_smem_limit();
+    rp.search = tune.algo >= 1 && sbytes <= slimit;
     a.nblk = rp.search ? T.nblk : 0;
     a.reps_target = tune.reps_target > 0 ? tune.reps_target : 384;
     a.team_threshold = tune.team_threshold;
@@ -809,8 +813,9 @@ int range_prepare(const Grid* d_grid, const double* d_landmarks3, const int* d_s
     a.dbg = d_dbg;
     rp.slot = tune.grid_slot;
     if (rp.search)
-        FPH_TRY(rp.slot == 1 ? slot1::search_prepare(a, rp.d_geom, a.cand_count, stream, &rp.sp)
-                             : slot0::search_prepare(a, rp.d_geom, a.cand_count, stream, &rp.sp));
+        FPH_TRY(rp.slot == 2   ? slot2::search_prepare(a, rp.d_geom, a.cand_count, stream, &rp.sp)
+                : rp.slot == 1 ? slot1::search_prepare(a, rp.d_geom, a.cand_count, stream, &rp.sp)
+                               : slot0::search_prepare(a, rp.d_geom, a.cand_count, stream, &rp.sp));
     FPH_CUDA_TRY(cudaGetLastError());
     return FPH_OK;
 }
@@ -824,7 +829,9 @@ int range_run(RangePlan& rp) {
         FPH_CUDA_TRY(cudaEventRecord(ev0, stream));
     }
     if (rp.search) {
-        FPH_TRY(rp.slot == 1 ? slot1::search_run(rp.sp, true) : slot0::search_run(rp.sp, true));
+        FPH_TRY(rp.slot == 2   ? slot2::search_run(rp.sp, true)
+                : rp.slot == 1 ? slot1::search_run(rp.sp, true)
+                               : slot0::search_run(rp.sp, true));
     } else {
         int dev = 0, sms = 0, occ = 0;
         FPH_CUDA_TRY(cudaGetDevice(&dev));

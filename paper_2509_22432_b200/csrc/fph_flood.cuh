@@ -75,7 +75,13 @@ struct SearchPlan {
 // copy's kernels read their own __constant__ grid, so two calls holding
 // different slots run concurrently on one device (a batch of clouds on two
 // streams).  The copies' entry points live in namespaces slot0 / slot1.
-constexpr int kGridSlots = 2;
+// A third copy, slot2, is built for clouds too large for L2 (kBigSlot): 3
+// search CTAs per SM (80 registers, 256-candidate tiles, rows' values in
+// shared memory up to 512 rows), so more warps hide the DRAM latency of
+// the candidate loads (box_10m 12.5 -> 11.1 ms; on L2-resident clouds the
+// spills and smaller tiles cost 9-28%).
+constexpr int kGridSlots = 3;
+constexpr int kBigSlot = 2;
 #define FPH_SEARCH_API                                                                     \
     int search_prepare(const FloodArgs& a, const SimplexGeom* d_geom, const int* d_cand,   \
                        cudaStream_t stream, SearchPlan* plan);                             \
@@ -96,9 +102,14 @@ FPH_SEARCH_API
 namespace slot1 {
 FPH_SEARCH_API
 }
+namespace slot2 {
+FPH_SEARCH_API
+}
 #undef FPH_SEARCH_API
 inline int set_search_grid(int slot, const Grid* d_grid, cudaStream_t stream) {
-    return slot == 1 ? slot1::set_search_grid(d_grid, stream) : slot0::set_search_grid(d_grid, stream);
+    return slot == 2   ? slot2::set_search_grid(d_grid, stream)
+           : slot == 1 ? slot1::set_search_grid(d_grid, stream)
+                       : slot0::set_search_grid(d_grid, stream);
 }
 
 struct FloodTuning {

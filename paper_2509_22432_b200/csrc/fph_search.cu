@@ -37,8 +37,10 @@
 #endif
 #if FPH_GRID_SLOT == 0
 #define FPH_SLOT_NS slot0
-#else
+#elif FPH_GRID_SLOT == 1
 #define FPH_SLOT_NS slot1
+#else
+#define FPH_SLOT_NS slot2
 #endif
 
 namespace fph {
@@ -128,7 +130,10 @@ struct SearchSmem {
 // kValsCap rows: every phase reads and writes them, and an L2 round trip per
 // access was a large part of a block search's latency.  A team uses warp
 // 0's array.  Larger templates use the global scratch (a.perpoint).
-constexpr int kValsCap = 1024;
+#ifndef FPH_VALS_CAP
+#define FPH_VALS_CAP 1024
+#endif
+constexpr int kValsCap = FPH_VALS_CAP;
 constexpr size_t kSmemVals = sizeof(SearchSmem) + sizeof(float) * kSW * kValsCap;
 static_assert(kSmemVals + 8 * 256 + 1024 <= 233472 / 2, "two search CTAs per SM up to m = 255");
 

@@ -1,0 +1,24 @@
+"""GPU: the big-cloud build of the search kernels (slot 2: 3 CTAs per SM,
+80 registers, 256-candidate tiles; taken for clouds of >= 64 MiB) passes
+the same parity suite when every call is forced onto it
+(FPH_BIG_MIN_BYTES=0).  Run in a fresh process: the threshold is read once
+per process."""
+
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_big_cloud_kernels_pass_the_parity_suite():
+    env = dict(os.environ, FPH_BIG_MIN_BYTES="0")
+    r = subprocess.run([sys.executable, "-m", "pytest", "tests/test_gpu_parity.py", "-m", "gpu", "-q",
+                        "-x", "-k", "not fps", "-p", "no:cacheprovider"],
+                       env=env, cwd=ROOT, capture_output=True, text=True, timeout=1800)
+    assert r.returncode == 0, (r.stdout[-3000:], r.stderr[-2000:])
+    assert " passed" in r.stdout
