@@ -23,7 +23,7 @@ HEADERS = ["fph_common.cuh", "fph_dev.cuh", "fph_flood.cuh", "fph_grid.cuh"]
 SLOTTED = ["fph_search.cu"]
 GRID_SLOTS = 3
 # slot 2: the build for clouds beyond L2 (fph_flood.cuh kBigSlot)
-SLOT_DEFINES = {2: ["-DFPH_SEARCH_MINB=3", "-DFPH_WT=256", "-DFPH_VALS_CAP=512"]}
+SLOT_DEFINES = {2: ["-DFPH_SEARCH_MINB=4", "-DFPH_WT=128", "-DFPH_VALS_CAP=256"]}
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -75,11 +75,11 @@ struct SearchPlan {
 // copy's kernels read their own __constant__ grid, so two calls holding
 // different slots run concurrently on one device (a batch of clouds on two
 // streams).  The copies' entry points live in namespaces slot0 / slot1.
-// A third copy, slot2, is built for clouds too large for L2 (kBigSlot): 3
-// search CTAs per SM (80 registers, 256-candidate tiles, rows' values in
-// shared memory up to 512 rows), so more warps hide the DRAM latency of
-// the candidate loads (box_10m 12.5 -> 11.1 ms; on L2-resident clouds the
-// spills and smaller tiles cost 9-28%).
+// A third copy, slot2, is built for clouds too large for L2 (kBigSlot): 4
+// search CTAs per SM (64 registers, 128-candidate tiles, rows' values in
+// shared memory up to 256 rows), so more warps hide the DRAM latency of
+// the candidate loads (box_10m 12.5 -> 10.75 ms; 3 CTAs: 11.2, 5: 11.1;
+// on L2-resident clouds such builds lose 9-28% to spills and small tiles).
 constexpr int kGridSlots = 3;
 constexpr int kBigSlot = 2;
 #define FPH_SEARCH_API                                                                     \

@@ -1,5 +1,5 @@
-"""GPU: the big-cloud build of the search kernels (slot 2: 3 CTAs per SM,
-80 registers, 256-candidate tiles; taken for clouds of >= 64 MiB) passes
+"""GPU: the big-cloud build of the search kernels (slot 2: 4 CTAs per SM,
+64 registers, 128-candidate tiles; taken for clouds of >= 64 MiB) passes
 the same parity suite when every call is forced onto it
 (FPH_BIG_MIN_BYTES=0).  Run in a fresh process: the threshold is read once
 per process."""
