@@ -78,6 +78,9 @@ constexpr double kSpreadRatio = FPH_SPREAD_RATIO;
 #ifndef FPH_SAMPLE_PASSES
 #define FPH_SAMPLE_PASSES 1
 #endif
+#ifndef FPH_COUNT_EST
+#define FPH_COUNT_EST 1
+#endif
 // phase C: sampling passes a large block region may get before its exact pass
 constexpr int kSamplePasses = FPH_SAMPLE_PASSES;
 
@@ -836,10 +839,17 @@ __device__ void search_block(const Ctx& c, WarpSmem& W, int nb, float* vals, flo
         const bool small = a.subset && rho2 > 0.0 &&
                            c.cnt * fmin(rho2, R * R) <= 2.0 * a.reps_target * rho2;
         if (pass == 0 && !small) {
-            // count the region; a large one is sampled first to tighten U
+            // the region's candidate count, estimated from the simplex's by
+            // the area ratio (an over-estimate for volume data; counting the
+            // region's rows exactly, FPH_COUNT_EST=0, cost phase C 3%): a
+            // large region is sampled first to tighten U
             long long cnt = 0;
-            for (int rb = tm.rank * 32; rb < rows; rb += tm.size * 32) cnt += row_batch(rw, W, rb).total;
-            cnt = tm.sum(cnt);
+            if (FPH_COUNT_EST && rho2 > 0.0) {
+                cnt = (long long)(c.cnt * fmin(1.0, R * R / rho2));
+            } else {
+                for (int rb = tm.rank * 32; rb < rows; rb += tm.size * 32) cnt += row_batch(rw, W, rb).total;
+                cnt = tm.sum(cnt);
+            }
             if (cnt > 4ll * a.reps_target) stride = (int)((cnt + a.reps_target - 1) / a.reps_target);
         }
         if (pass == 1 || stride > 1) {
