@@ -29,7 +29,7 @@ static int g_algo = 1;
 static int g_reps_target = 512;
 static int g_team_threshold = 0;  // auto (derived per launch on the device)
 static double g_exact_pairs = 65536.0;
-static long long g_exact_cand[4] = {0, 0, 2500, 0};
+static long long g_exact_cand[4] = {0, 0, 1000, 0};
 static thread_local long long g_launches = 0;
 
 void set_error(const char* fmt, ...) {

@@ -29,7 +29,7 @@ def main():
     ap.add_argument("--reps", type=int, nargs="+", default=[512])
     ap.add_argument("--team", type=int, nargs="+", default=[0])
     ap.add_argument("--exact-pairs", type=float, nargs="+", default=[65536.0])
-    ap.add_argument("--exact-cand2", type=int, nargs="+", default=[2500])
+    ap.add_argument("--exact-cand2", type=int, nargs="+", default=[1000])
     args = ap.parse_args()
     lib = _native.require_gpu()
     w = bench.prepare(args.config, 0)
@@ -69,7 +69,7 @@ def main():
             print(json.dumps(rows[-1]), flush=True)
     _native.check(lib.fph_set_search(1, 0, 0))
     _native.check(lib.fph_set_exact_pairs(-1))
-    _native.check(lib.fph_set_exact_candidates(2, 2500))
+    _native.check(lib.fph_set_exact_candidates(2, 1000))
 
 
 if __name__ == "__main__":
