@@ -30,6 +30,7 @@ def main():
     ap.add_argument("--team", type=int, nargs="+", default=[0])
     ap.add_argument("--exact-pairs", type=float, nargs="+", default=[65536.0])
     ap.add_argument("--exact-cand2", type=int, nargs="+", default=[1000])
+    ap.add_argument("--exact-cand1", type=int, nargs="+", default=[0])
     args = ap.parse_args()
     lib = _native.require_gpu()
     w = bench.prepare(args.config, 0)
@@ -52,17 +53,19 @@ def main():
     rows = []
     import itertools
 
-    for reps, team, ep, ec in itertools.product(args.reps, args.team, args.exact_pairs,
-                                                args.exact_cand2):
+    for reps, team, ep, ec, ec1 in itertools.product(args.reps, args.team, args.exact_pairs,
+                                                     args.exact_cand2, args.exact_cand1):
         if True:
             _native.check(lib.fph_set_search(1, reps, team))
             _native.check(lib.fph_set_exact_pairs(ep))
             _native.check(lib.fph_set_exact_candidates(2, ec))
+            _native.check(lib.fph_set_exact_candidates(1, ec1))
             t1 = timed(lambda: flood_sq_device(Xd, dc, w["m"]))
             W = args.world
             per = [timed(lambda: shard_interior(Xd, dc.lm, by_dim, dc.top, w["m"], True, r, W), 1)
                    for r in range(W)] if W > 1 else [t1]
             rows.append({"reps": reps, "team": team, "exact_pairs": ep, "exact_cand2": ec,
+                         "exact_cand1": ec1,
                          "single_ms": t1, "max_rank_ms": max(per),
                          "mean_rank_ms": float(np.mean(per)),
                          "predicted_efficiency": t1 / (W * (max(per) + 0.05))})
@@ -70,6 +73,7 @@ def main():
     _native.check(lib.fph_set_search(1, 0, 0))
     _native.check(lib.fph_set_exact_pairs(-1))
     _native.check(lib.fph_set_exact_candidates(2, 1000))
+    _native.check(lib.fph_set_exact_candidates(1, 0))
 
 
 if __name__ == "__main__":
