@@ -85,7 +85,10 @@ def main():
                     ov = min(b, edges[i + 1]) - max(a, edges[i])
                     if ov > 0:
                         busy[i] += t * ov / (edges[i + 1] - edges[i])
-    capacity = 2368.0
+    # resident warps: 148 SMs x 8 warps x CTAs per SM (2; 4 for the big-cloud
+    # build, clouds of >= 64 MiB, fph_flood.cuh kBigSlot)
+    big = Xd.shape[0] * Xd.shape[1] * 8 >= (64 << 20)
+    capacity = 148.0 * 8 * (4 if big else 2)
     out = {"config": args.config, "world": args.world, "rank": args.rank,
            "step_ms_events": e0.elapsed_time(e1),
            "first_claim_to_last_publish_us": span_us,
