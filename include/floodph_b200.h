@@ -6,6 +6,8 @@
  *   FPH_MEM_HOST    all array arguments are host pointers; the call copies
  *                   them to the GPU, runs, copies results back and returns
  *                   when they are ready (the drop-in for the CPU reference);
+ *                   it runs on a stream of the calling thread, so calls from
+ *                   different host threads overlap on the device;
  *   FPH_MEM_DEVICE  all data arrays (coordinates, simplices, facets, values,
  *                   indices) are device pointers on the current CUDA device;
  *                   work is ordered on `stream` (a cudaStream_t, NULL =

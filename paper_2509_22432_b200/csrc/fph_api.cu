@@ -104,8 +104,9 @@ __global__ void fill_kernel(double* out, long long n, double v) {
 
 unsigned blocks_for(long long n) { return (unsigned)((n + 255) / 256); }
 
-// Library streams, created once per device and kept: stream 0 carries
-// host-memory calls, streams 1 + 3 g + (k - 1) the dimension-k interior terms
+// Library streams, created once per device and kept: stream 0 (unused since
+// host-memory calls moved to per-thread streams), streams 1 + 3 g + (k - 1)
+// the dimension-k interior terms
 // of a call holding grid slot g (run_interiors; higher dimensions at higher
 // priority).
 constexpr int kLibStreams = 1 + 3 * kGridSlots;
@@ -130,8 +131,27 @@ int lib_stream(int slot, cudaStream_t* out) {
     return FPH_OK;
 }
 
-// Host-call context: the library's stream on the current device (host
-// calls), or the caller's stream (device calls)
+// Host-memory calls run on a stream of the calling thread (one per thread
+// and device, created on first use, kept): calls from different host
+// threads overlap on the device -- the next call's copies and grid build
+// under the current call's search -- while each call still returns only
+// when its own work is done.
+int thread_host_stream(cudaStream_t* out) {
+    int dev = 0;
+    FPH_CUDA_TRY(cudaGetDevice(&dev));
+    thread_local std::map<int, cudaStream_t> streams;
+    auto it = streams.find(dev);
+    if (it == streams.end()) {
+        cudaStream_t st = nullptr;
+        FPH_CUDA_TRY(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+        it = streams.emplace(dev, st).first;
+    }
+    *out = it->second;
+    return FPH_OK;
+}
+
+// Host-call context: the calling thread's library stream on the current
+// device (host calls), or the caller's stream (device calls)
 struct HostCtx {
     cudaStream_t stream = nullptr;
     int init(int memory, void* user_stream) {
@@ -139,7 +159,7 @@ struct HostCtx {
             stream = static_cast<cudaStream_t>(user_stream);
             return FPH_OK;
         }
-        return lib_stream(0, &stream);
+        return thread_host_stream(&stream);
     }
 };
 
