@@ -119,6 +119,11 @@ __device__ __forceinline__ void warp_argmax(double& v, int& i) {
 #define FPH_FPS_REPL 4
 #endif
 constexpr int kRepl = FPH_FPS_REPL;
+#ifndef FPH_FPS_CTRS
+#define FPH_FPS_CTRS 4
+#endif
+constexpr int kCtrs = FPH_FPS_CTRS;     // arrival counters of exchange_argmax
+constexpr int kCtrStride = 32;          // 256 bytes apart
 __host__ __device__ __forceinline__ int repl_stride(int G) { return ((G + 63) & ~63) + 40; }
 
 __device__ __forceinline__ int exchange_argmax(double bv, int bi, Slot* buf, int G, int slot,
@@ -136,13 +141,21 @@ __device__ __forceinline__ int exchange_argmax(double bv, int bi, Slot* buf, int
         double v = l < (int)(blockDim.x >> 5) ? red_v[l] : -INFINITY;
         int i = l < (int)(blockDim.x >> 5) ? red_i[l] : 0x7fffffff;
         warp_argmax(v, i);
+        // arrivals spread over kCtrs counters (CTA c on counter c % kCtrs,
+        // kCtrStride words apart): the same-address atomics of 148 CTAs
+        // serialise at one L2 slice; lane r < kCtrs waits for counter r
         if (l == 0) {
             for (int r = 0; r < nrep; ++r) {
                 buf[r * rs + slot].val = v;
                 buf[r * rs + slot].idx = i;
             }
-            arrive_release(arrived);
-            while (ld_acquire(arrived) < target) {
+            arrive_release(arrived + (slot % kCtrs) * kCtrStride);
+        }
+        if (l < kCtrs) {
+            // CTAs on counter l per iteration: ceil((G - l) / kCtrs); target = G * it overall
+            const unsigned long long per = (unsigned long long)((G - l + kCtrs - 1) / kCtrs);
+            const unsigned long long tgt = per * (target / (unsigned long long)G);
+            while (ld_acquire(arrived + l * kCtrStride) < tgt) {
             }
         }
         __syncwarp();
@@ -432,6 +445,8 @@ __device__ __forceinline__ Winner exchange_argmax_tiled(double bv, int bi, int b
             sl.z = any ? txyz[3 * t + 2] : 0.0;
             sl.pad2 = 0.0;
             buf[slot] = sl;
+            // one counter: spreading the arrivals as exchange_argmax does
+            // measured 27.6 -> 30.5 ms on the 10M tiled run
             arrive_release(arrived);
             while (ld_acquire(arrived) < target) {
             }
@@ -765,8 +780,8 @@ int fps_tiled(const double* d_x, const double* d_y, const double* d_z, int n, in
     SlotXYZ* slots = nullptr;
     unsigned long long* arrived = nullptr;
     FPH_TRY(sc.alloc(&slots, 2 * kMaxSlots));
-    FPH_TRY(sc.alloc(&arrived, 1));
-    FPH_CUDA_TRY(cudaMemsetAsync(arrived, 0, sizeof(unsigned long long), stream));
+    FPH_TRY(sc.alloc(&arrived, kCtrs * kCtrStride));
+    FPH_CUDA_TRY(cudaMemsetAsync(arrived, 0, sizeof(unsigned long long) * kCtrs * kCtrStride, stream));
     FPH_CUDA_TRY(cudaFuncSetAttribute(fps_tiled_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)smem));
     int ntl = ntiles;
@@ -900,8 +915,8 @@ int fps_run(const double* d_x, const double* d_y, const double* d_z, int n, int 
     double* mind = nullptr;
     unsigned long long* arrived = nullptr;
     FPH_TRY(sc.alloc(&slots, 2 * kRepl * repl_stride(G)));
-    FPH_TRY(sc.alloc(&arrived, 1));
-    FPH_CUDA_TRY(cudaMemsetAsync(arrived, 0, sizeof(unsigned long long), stream));
+    FPH_TRY(sc.alloc(&arrived, kCtrs * kCtrStride));
+    FPH_CUDA_TRY(cudaMemsetAsync(arrived, 0, sizeof(unsigned long long) * kCtrs * kCtrStride, stream));
     if (!use_smem) FPH_TRY(sc.alloc(&mind, n));
     if (use_smem) {
         int rc = FPH_OK;
