@@ -44,7 +44,9 @@ constexpr int kFpsThreads = 1024;
 #endif
 constexpr int kResNT = FPH_FPS_RES_NT;  // threads per CTA of the resident kernel
 constexpr int kFpsMaxPT = 9;  // points per thread in the shared-memory variants
-constexpr int kMaxSlots = 160;  // CTAs per exchange of the batched (coordinate-carrying) kernel
+constexpr int kMaxSlots = 160;
+constexpr int kSortedMin = 262144;  // clouds at least this large take fps_sorted_kernel
+constexpr int kSortedMaxPT = 15;    // its shared slice: PT x 512 x 28 bytes  // CTAs per exchange of the batched (coordinate-carrying) kernel
 constexpr int kStaticSmem = 4 * kMaxSlots * 8 + 1024;  // batched kernel: stage + reduction scratch
 
 struct __align__(16) Slot {
@@ -360,8 +362,11 @@ __global__ void __launch_bounds__(kResNT, 1)
         const int jc = cur >= beg && cur < beg + cnt ? cur - beg - (int)threadIdx.x : -1;
         double bv = -INFINITY;
         int bi = 0x7fffffff;
+#ifndef FPH_FPS_NOUPDATE
+#define FPH_FPS_NOUPDATE 0
+#endif
 #pragma unroll
-        for (int t = 0; t < PT; ++t) {
+        for (int t = 0; t < (FPH_FPS_NOUPDATE ? 1 : PT); ++t) {  // NOUPDATE: timing experiment only
             const int j = threadIdx.x + t * kResNT;
             const double2 xy = sxy[j];
             const double d = sq64(xy.x, xy.y, sz[j], qx, qy, qz);
@@ -378,6 +383,122 @@ __global__ void __launch_bounds__(kResNT, 1)
                               (unsigned long long)G * it, red_v, red_i, rs, kRepl);
         if (blockIdx.x == 0 && threadIdx.x == 0) out[it] = cur;
     }
+}
+
+// Resident variant over the Morton-sorted cloud: warp w of a CTA holds
+// 32 x PT consecutive sorted points (spatially compact), with their box
+// kept in registers.  An iteration updates a warp's points only if the new
+// landmark is among them or its box is closer to the landmark than the
+// warp's largest running minimum; otherwise no point of the warp can
+// change and its threads keep their argmax records.  Late iterations touch
+// a few warps near the landmark instead of every point.  Ties still go to
+// the lowest cloud index (sidx, shared memory, read only when a value can
+// tie or win).  Shared memory: PT x 512 x (24 + 4) bytes, PT <= 15.
+template <int PT>
+__global__ void __launch_bounds__(kResNT, 1)
+    fps_sorted_kernel(const double* __restrict__ px, const double* __restrict__ py,
+                      const double* __restrict__ pz, const double* __restrict__ sx,
+                      const double* __restrict__ sy, const double* __restrict__ szg,
+                      const int* __restrict__ sidx, const int* __restrict__ spos, int n, int k,
+                      int start, int chunk, Slot* slots, unsigned long long* arrived,
+                      long long* __restrict__ out) {
+    extern __shared__ double sm[];
+    __shared__ double red_v[32];
+    __shared__ int red_i[33];
+    constexpr int kSlice = PT * kResNT;
+    const int beg = blockIdx.x * chunk;
+    const int cnt = max(0, min(n, beg + chunk) - beg);
+    double2* sxy = reinterpret_cast<double2*>(sm);
+    double* sz = sm + 2 * kSlice;
+    int* soi = reinterpret_cast<int*>(sm + 3 * kSlice);
+    for (int j = threadIdx.x; j < kSlice; j += blockDim.x) {
+        const bool in = j < cnt;
+        sxy[j] = in ? make_double2(sx[beg + j], sy[beg + j]) : make_double2(0.0, 0.0);
+        sz[j] = in ? szg[beg + j] : 0.0;
+        soi[j] = in ? sidx[beg + j] : 0x7fffffff;
+    }
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    const int wbeg = w * 32 * PT;  // this warp's points: wbeg + 32 t + lane
+    double md[PT];
+    double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+    __syncthreads();
+#pragma unroll
+    for (int t = 0; t < PT; ++t) {
+        const int j = wbeg + 32 * t + l;
+        md[t] = j < cnt ? INFINITY : -INFINITY;
+        if (j < cnt) {
+            const double2 xy = sxy[j];
+            lo[0] = fmin(lo[0], xy.x); hi[0] = fmax(hi[0], xy.x);
+            lo[1] = fmin(lo[1], xy.y); hi[1] = fmax(hi[1], xy.y);
+            lo[2] = fmin(lo[2], sz[j]); hi[2] = fmax(hi[2], sz[j]);
+        }
+    }
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        lo[a] = warp_min_d(lo[a]);
+        for (int o = 16; o > 0; o >>= 1) hi[a] = fmax(hi[a], __shfl_xor_sync(0xffffffffu, hi[a], o));
+    }
+    int cur = start;
+    if (blockIdx.x == 0 && threadIdx.x == 0) out[0] = start;
+    const int G = gridDim.x, rs = repl_stride(G);
+    double bv = -INFINITY, wmax = INFINITY;  // this thread's record; the warp's largest minimum
+    int bi = 0x7fffffff;
+    for (int it = 1; it <= k; ++it) {
+        const double qx = px[cur], qy = py[cur], qz = pz[cur];
+        const int pc = spos[cur] - beg - wbeg;  // the landmark's place in this warp's points
+        const double dx = fmax(0.0, fmax(lo[0] - qx, qx - hi[0]));
+        const double dy = fmax(0.0, fmax(lo[1] - qy, qy - hi[1]));
+        const double dz = fmax(0.0, fmax(lo[2] - qz, qz - hi[2]));
+        // a safe lower bound on sq64(x, q) for every point of the warp
+        const double lb = (dx * dx + dy * dy + dz * dz) * (1.0 - 1e-12);
+        if ((pc >= 0 && pc < 32 * PT) || lb < wmax) {  // warp-uniform
+            bv = -INFINITY;
+            bi = 0x7fffffff;
+#pragma unroll
+            for (int t = 0; t < PT; ++t) {
+                const int j = wbeg + 32 * t + l;
+                const double2 xy = sxy[j];
+                const double d = sq64(xy.x, xy.y, sz[j], qx, qy, qz);
+                double m = d < md[t] ? d : md[t];
+                m = pc == 32 * t + l ? -1.0 : m;
+                md[t] = m;
+                if (m >= bv) {
+                    const int oi = soi[j];
+                    if (m > bv || oi < bi) {
+                        bv = m;
+                        bi = oi;
+                    }
+                }
+            }
+            // the warp's largest running minimum (a monotone 64-bit key)
+            const unsigned long long b = (unsigned long long)__double_as_longlong(bv);
+            const unsigned long long key = (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+            const unsigned mhi = __reduce_max_sync(0xffffffffu, (unsigned)(key >> 32));
+            const unsigned mlo = __reduce_max_sync(0xffffffffu, (unsigned)(key >> 32) == mhi ? (unsigned)key : 0u);
+            const unsigned long long mk = ((unsigned long long)mhi << 32) | mlo;
+            wmax = __longlong_as_double((long long)((mk >> 63) ? (mk & 0x7fffffffffffffffull) : ~mk));
+        }
+        if (it == k) break;
+        cur = exchange_argmax(bv, bi, slots + (it & 1) * kRepl * rs, G, blockIdx.x, arrived,
+                              (unsigned long long)G * it, red_v, red_i, rs, kRepl);
+        if (blockIdx.x == 0 && threadIdx.x == 0) out[it] = cur;
+    }
+}
+
+template <int PT>
+int launch_sorted(const double* d_x, const double* d_y, const double* d_z, const double* sx,
+                  const double* sy, const double* sz, const int* sidx, const int* spos, int n,
+                  int k, int start, int chunk, int G, Slot* slots, unsigned long long* arrived,
+                  long long* d_out, cudaStream_t stream) {
+    const size_t smem = (sizeof(double) * 3 + sizeof(int)) * PT * kResNT;
+    FPH_CUDA_TRY(cudaFuncSetAttribute(fps_sorted_kernel<PT>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    void* args[] = {(void*)&d_x,  (void*)&d_y,   (void*)&d_z,   (void*)&sx,    (void*)&sy,
+                    (void*)&sz,   (void*)&sidx,  (void*)&spos,  (void*)&n,     (void*)&k,
+                    (void*)&start, (void*)&chunk, (void*)&slots, (void*)&arrived, (void*)&d_out};
+    FPH_CUDA_TRY(cudaLaunchCooperativeKernel((void*)fps_sorted_kernel<PT>, dim3(G), dim3(kResNT),
+                                             args, smem, stream));
+    return FPH_OK;
 }
 
 template <int PT>
@@ -737,6 +858,40 @@ __global__ void minmax_kernel(const double* __restrict__ v, int n, double* __res
     }
 }
 
+// Morton order of the cloud (the box is read on the device): sorted copies
+// sx, sy, sz, the cloud index of each sorted point (sidx) and the sorted
+// position of each cloud point (spos), allocated in `sc`.
+int morton_sort(const double* d_x, const double* d_y, const double* d_z, int n, Scratch& sc,
+                cudaStream_t stream, double** sx, double** sy, double** sz, int** sidx, int** spos) {
+    double* mm = nullptr;
+    FPH_TRY(sc.alloc(&mm, 6));
+    minmax_init_kernel<<<1, 6, 0, stream>>>(mm);
+    minmax_kernel<<<1024, 256, 0, stream>>>(d_x, n, mm);
+    minmax_kernel<<<1024, 256, 0, stream>>>(d_y, n, mm + 2);
+    minmax_kernel<<<1024, 256, 0, stream>>>(d_z, n, mm + 4);
+    unsigned *code = nullptr, *code2 = nullptr;
+    int* idx = nullptr;
+    FPH_TRY(sc.alloc(&code, n));
+    FPH_TRY(sc.alloc(&code2, n));
+    FPH_TRY(sc.alloc(&idx, n));
+    FPH_TRY(sc.alloc(sidx, n));
+    FPH_TRY(sc.alloc(spos, n));
+    FPH_TRY(sc.alloc(sx, n));
+    FPH_TRY(sc.alloc(sy, n));
+    FPH_TRY(sc.alloc(sz, n));
+    morton_kernel<<<(n + 255) / 256, 256, 0, stream>>>(d_x, d_y, d_z, n, mm, code, idx);
+    size_t tmp_bytes = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, code, code2, idx, *sidx, n, 0, 30, stream);
+    unsigned char* tmp = nullptr;
+    FPH_TRY(sc.alloc(&tmp, tmp_bytes));
+    FPH_CUDA_TRY(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, code, code2, idx, *sidx, n, 0, 30,
+                                                 stream));
+    gather_sorted_kernel<<<(n + 255) / 256, 256, 0, stream>>>(d_x, d_y, d_z, *sidx, n, *sx, *sy,
+                                                              *sz, *spos);
+    FPH_CUDA_TRY(cudaGetLastError());
+    return FPH_OK;
+}
+
 int fps_tiled(const double* d_x, const double* d_y, const double* d_z, int n, int k, int start,
               long long* d_out, int G, cudaStream_t stream) {
     // bounding box (for the Morton quantisation only: any box works)
@@ -918,6 +1073,50 @@ int fps_run(const double* d_x, const double* d_y, const double* d_z, int n, int 
     FPH_TRY(sc.alloc(&arrived, kCtrs * kCtrStride));
     FPH_CUDA_TRY(cudaMemsetAsync(arrived, 0, sizeof(unsigned long long) * kCtrs * kCtrStride, stream));
     if (!use_smem) FPH_TRY(sc.alloc(&mind, n));
+    // large resident clouds: the Morton-sorted variant (warps skip the
+    // iterations that cannot change their points)
+    static const bool sorted_on = [] {
+        const char* e = getenv("FPH_FPS_SORTED");
+        return !(e && e[0] == '0');
+    }();
+    static const long long sorted_min = [] {  // FPH_FPS_SORTED_MIN: tests force it on small clouds
+        const char* e = getenv("FPH_FPS_SORTED_MIN");
+        return e ? atoll(e) : (long long)kSortedMin;
+    }();
+    const int pt_need = (chunk + kResNT - 1) / kResNT;
+    if (use_smem && sorted_on && n >= sorted_min && pt_need <= kSortedMaxPT && k > 1) {
+        double *sx = nullptr, *sy = nullptr, *sz = nullptr;
+        int *sidx = nullptr, *spos = nullptr;
+        FPH_TRY(morton_sort(d_x, d_y, d_z, n, sc, stream, &sx, &sy, &sz, &sidx, &spos));
+        int rc = FPH_OK;
+#define FPH_SORTED_CASE(P)                                                                     \
+    case P:                                                                                    \
+        rc = launch_sorted<P>(d_x, d_y, d_z, sx, sy, sz, sidx, spos, n, k, start, chunk, G,   \
+                              slots, arrived, d_out, stream);                                  \
+        break;
+        switch (pt_need) {
+            FPH_SORTED_CASE(1)
+            FPH_SORTED_CASE(2)
+            FPH_SORTED_CASE(3)
+            FPH_SORTED_CASE(4)
+            FPH_SORTED_CASE(5)
+            FPH_SORTED_CASE(6)
+            FPH_SORTED_CASE(7)
+            FPH_SORTED_CASE(8)
+            FPH_SORTED_CASE(9)
+            FPH_SORTED_CASE(10)
+            FPH_SORTED_CASE(11)
+            FPH_SORTED_CASE(12)
+            FPH_SORTED_CASE(13)
+            FPH_SORTED_CASE(14)
+            default:
+                FPH_SORTED_CASE(15)
+        }
+#undef FPH_SORTED_CASE
+        if (rc != FPH_OK) return rc;
+        FPH_CUDA_TRY(cudaGetLastError());
+        return FPH_OK;
+    }
     if (use_smem) {
         int rc = FPH_OK;
 #define FPH_RESIDENT_CASE(P)                                                                   \
