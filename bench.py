@@ -62,37 +62,79 @@ def _cloud(kind: str, n: int, seed: int = 0):
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clocks + throttle reasons sampled during the timed region, in
+    process through NVML (initialised before the region starts): spawning
+    nvidia-smi inside the region stalled kernel launches -- an eager box_10m
+    step read ~2x slow whenever a spawn landed in it.  Falls back to
+    nvidia-smi when NVML is unavailable."""
 
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
               "clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, index: int):
+    def __init__(self, index: int, period: float = 0.05):
         self.index = index
+        self.period = period
         self.rows = []
         self._stop = threading.Event()
         self._t = threading.Thread(target=self._run, daemon=True)
+        self._nvml = None
+        self._h = None
+
+    def _sample_nvml(self):
+        n = self._nvml
+        sm = n.nvmlDeviceGetClockInfo(self._h, n.NVML_CLOCK_SM)
+        mx = n.nvmlDeviceGetMaxClockInfo(self._h, n.NVML_CLOCK_SM)
+        r = n.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+        flags = [n.nvmlClocksEventReasonHwSlowdown, n.nvmlClocksEventReasonHwThermalSlowdown,
+                 n.nvmlClocksEventReasonSwThermalSlowdown, n.nvmlClocksEventReasonSwPowerCap]
+        return [str(sm), str(mx)] + ["Active" if r & f else "Not Active" for f in flags]
+
+    def _sample_smi(self):
+        out = subprocess.run(
+            ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+             "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+        if out.returncode == 0 and out.stdout.strip():
+            return [c.strip() for c in out.stdout.strip().split(",")]
+        return None
 
     def _run(self):
         while not self._stop.is_set():
             try:
-                out = subprocess.run(
-                    ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                     "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
-                if out.returncode == 0 and out.stdout.strip():
-                    self.rows.append([c.strip() for c in out.stdout.strip().split(",")])
+                row = self._sample_nvml() if self._nvml is not None else self._sample_smi()
+                if row:
+                    self.rows.append(row)
             except Exception:
                 pass
-            self._stop.wait(0.2)
+            self._stop.wait(self.period if self._nvml is not None else 0.2)
 
     def __enter__(self):
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            try:  # the CUDA device's own GPU (NVML indices ignore CUDA_VISIBLE_DEVICES)
+                import torch
+
+                pr = torch.cuda.get_device_properties(self.index)
+                bus = f"{pr.pci_domain_id:08x}:{pr.pci_bus_id:02x}:{pr.pci_device_id:02x}.0"
+                self._h = pynvml.nvmlDeviceGetHandleByPciBusId(bus)
+            except Exception:
+                self._h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self._nvml = pynvml
+        except Exception:
+            self._nvml = None
         self._t.start()
         return self
 
     def __exit__(self, *exc):
         self._stop.set()
         self._t.join(timeout=10)
+        if self._nvml is not None:
+            try:
+                self._nvml.nvmlShutdown()
+            except Exception:
+                pass
 
     def summary(self):
         if not self.rows:
@@ -103,7 +145,8 @@ class ClockSampler:
         reasons = sorted({names[i] for r in self.rows for i in range(4)
                           if len(r) > 2 + i and r[2 + i].lower().startswith("active")})
         return {"sm_mhz": float(np.median(sm)) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(self.rows)}
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(self.rows),
+                "source": "nvml" if self._nvml is not None else "nvidia-smi"}
 
 
 def _peaks():
