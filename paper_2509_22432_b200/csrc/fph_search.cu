@@ -422,6 +422,7 @@ __device__ __forceinline__ float local_probe(const Ctx& c, const PointF& q) {
     return best < INFINITY ? best + q.bb : INFINITY;  // m32, as the folds give it
 }
 
+#if FPH_STAGE_BULK
 __device__ __forceinline__ void rel_of(const Ctx& c, double x, double y, double z, float& ax,
                                        float& ay, float& az, float& aw) {
     ax = __double2float_rn(__dsub_rn(x, c.G.cx));
@@ -430,7 +431,6 @@ __device__ __forceinline__ void rel_of(const Ctx& c, double x, double y, double 
     aw = fmaf(az, az, fmaf(ay, ay, ax * ax));
 }
 
-#if FPH_STAGE_BULK
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, void* bar) {
     const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
     const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
