@@ -91,8 +91,10 @@ constexpr int kSamplePasses = FPH_SAMPLE_PASSES;
 // other), completing on the warp's mbarrier; the candidates are then read
 // from shared memory in order, without window_index.
 constexpr bool kStageBulk = FPH_STAGE_BULK;
+#if FPH_STAGE_BULK
 constexpr int kBulkW = 96;            // real candidates per window
 constexpr int kBulkN = kBulkW + 64;   // + alignment padding (<= 2 per piece)
+#endif
 
 struct WarpSmem {
 #if FPH_STAGE_BULK
