@@ -1398,7 +1398,10 @@ __global__ void __launch_bounds__(kSThreads, FPH_SEARCH_MINB)
 // others ran dry.  Cost grows sublinearly with the candidate count C
 // (measured log-log slopes 0.24..0.52, tools/simplex_costs.py), modelled as
 // C^p; the threshold is returned in candidates: (beta sum C^p / warps)^(1/p).
-constexpr double kTeamBeta = 2.0;
+#ifndef FPH_TEAM_BETA
+#define FPH_TEAM_BETA 2.0
+#endif
+constexpr double kTeamBeta = FPH_TEAM_BETA;
 constexpr long long kTeamMin = 32768;
 #ifndef FPH_TEAM_POW
 #define FPH_TEAM_POW 1.0
