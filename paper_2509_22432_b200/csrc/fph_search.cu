@@ -78,6 +78,11 @@ constexpr double kSpreadRatio = FPH_SPREAD_RATIO;
 #ifndef FPH_SAMPLE_PASSES
 #define FPH_SAMPLE_PASSES 1
 #endif
+#ifndef FPH_TEAM_REPS
+#define FPH_TEAM_REPS 1
+#endif
+// representative sample of a CTA team's simplex, in units of reps_target
+constexpr int kTeamReps = FPH_TEAM_REPS;
 #ifndef FPH_COUNT_EST
 #define FPH_COUNT_EST 1
 #endif
@@ -1059,7 +1064,11 @@ __device__ void run_simplex(const Ctx& c, WarpSmem& W, const Team& tm, float* va
         // small enough for one exact pass (every row x every candidate), else a
         // sample of ~reps_target candidates
         const bool exact = (double)C * (double)a.P <= a.exact_pairs || C <= a.exact_cand[a.k];
-        stride = exact ? 1 : (int)max(1ll, (C + a.reps_target - 1) / a.reps_target);
+        // a CTA team takes kTeamReps x the sample (a team simplex has at
+        // least kTeamMin candidates, so its stride stays > 1 as the B / C
+        // kernels assume)
+        const long long n_reps = tm.size > 1 ? (long long)a.reps_target * kTeamReps : a.reps_target;
+        stride = exact ? 1 : (int)max(1ll, (C + n_reps - 1) / n_reps);
         // sampled simplices: every row first probes its own cells; when all
         // rows found a close candidate there (dense data) those bounds
         // replace the representatives' -- whose pass enumerates every grid
