@@ -83,6 +83,13 @@ constexpr double kSpreadRatio = FPH_SPREAD_RATIO;
 #endif
 // representative sample of a CTA team's simplex, in units of reps_target
 constexpr int kTeamReps = FPH_TEAM_REPS;
+#ifndef FPH_TET_REPS_SCALE
+#define FPH_TET_REPS_SCALE 0.5
+#endif
+// tetrahedra (1771 rows at m = 20): representative sample scale -- the
+// fold of 512 reps against every row outweighed the tighter bounds
+// (modelnet_batch 143 -> 140 ms at 0.5; 0.35 the same, 2 -> 151)
+constexpr double kTetRepsScale = FPH_TET_REPS_SCALE;
 #ifndef FPH_COUNT_EST
 #define FPH_COUNT_EST 1
 #endif
@@ -1036,6 +1043,17 @@ __device__ double finalize_team(const Ctx& c, WarpSmem& W, float* vals, const Te
     return M;
 }
 
+// Phase A's candidate stride for a simplex of C candidates: 1 (one exact
+// pass) when small, else about C / reps (reps_target, x kTeamReps for a CTA
+// team, x kTetRepsScale for tetrahedra).  Every phase kernel must derive it
+// the same way -- B and C skip the simplices whose stride is 1.
+__device__ __forceinline__ int sample_stride(const FloodArgs& a, long long C, bool team) {
+    if ((double)C * (double)a.P <= a.exact_pairs || C <= a.exact_cand[a.k]) return 1;
+    long long n_reps = team ? (long long)a.reps_target * kTeamReps : a.reps_target;
+    if (a.k == 3) n_reps = max(32ll, (long long)(n_reps * kTetRepsScale));
+    return (int)max(1ll, (C + n_reps - 1) / n_reps);
+}
+
 // ------------------------------------------------------- one simplex
 // kPh: 0 = every phase (one kernel, small complexes); the four-kernel chain
 // runs 1 = phase A only (the rows' values go to the next kernel through
@@ -1051,24 +1069,15 @@ __device__ void run_simplex(const Ctx& c, WarpSmem& W, const Team& tm, float* va
     clk[0] = clock64();
     // ---- A
     int stride = 1;
-    if (kPh == 5 || kPh == 6) {
-        const long long C = a.cand_count[c.s];
-        const bool exact = (double)C * (double)a.P <= a.exact_pairs || C <= a.exact_cand[a.k];
-        stride = exact ? 1 : (int)max(1ll, (C + a.reps_target - 1) / a.reps_target);
-    }
+    if (kPh == 5 || kPh == 6) stride = sample_stride(a, a.cand_count[c.s], tm.size > 1);
     if (kPh == 0 || kPh == 1) {
         for (int j = tm.rank * 32 + lane; j < a.P; j += tm.size * 32)
             vals[j] = tm.size == 1 ? INFINITY : __uint_as_float(f2ord(INFINITY));
         tm.sync();
-        const long long C = a.cand_count[c.s];
         // small enough for one exact pass (every row x every candidate), else a
-        // sample of ~reps_target candidates
-        const bool exact = (double)C * (double)a.P <= a.exact_pairs || C <= a.exact_cand[a.k];
-        // a CTA team takes kTeamReps x the sample (a team simplex has at
-        // least kTeamMin candidates, so its stride stays > 1 as the B / C
-        // kernels assume)
-        const long long n_reps = tm.size > 1 ? (long long)a.reps_target * kTeamReps : a.reps_target;
-        stride = exact ? 1 : (int)max(1ll, (C + n_reps - 1) / n_reps);
+        // sample of ~reps_target candidates (the same stride in every phase
+        // kernel: stride 1 means phase A was exact and B / C have nothing to do)
+        stride = sample_stride(a, a.cand_count[c.s], tm.size > 1);
         // sampled simplices: every row first probes its own cells; when all
         // rows found a close candidate there (dense data) those bounds
         // replace the representatives' -- whose pass enumerates every grid
