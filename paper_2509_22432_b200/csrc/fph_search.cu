@@ -90,6 +90,13 @@ constexpr int kTeamReps = FPH_TEAM_REPS;
 // fold of 512 reps against every row outweighed the tighter bounds
 // (modelnet_batch 143 -> 140 ms at 0.5; 0.35 the same, 2 -> 151)
 constexpr double kTetRepsScale = FPH_TET_REPS_SCALE;
+#ifndef FPH_TRI_REPS_SCALE
+#define FPH_TRI_REPS_SCALE 0.75
+#endif
+// the same for triangles: 0.5 / 0.75 / 1 / 1.5 -> configs[1] 3.49 / 3.47 /
+// 3.50 / 3.52 ms, dense30 4.47 / 4.49 / 4.53 / 4.61, modelnet_batch 139.5 /
+// 139.9 / 141.0 / 142.1
+constexpr double kTriRepsScale = FPH_TRI_REPS_SCALE;
 #ifndef FPH_COUNT_EST
 #define FPH_COUNT_EST 1
 #endif
@@ -1051,6 +1058,7 @@ __device__ __forceinline__ int sample_stride(const FloodArgs& a, long long C, bo
     if ((double)C * (double)a.P <= a.exact_pairs || C <= a.exact_cand[a.k]) return 1;
     long long n_reps = team ? (long long)a.reps_target * kTeamReps : a.reps_target;
     if (a.k == 3) n_reps = max(32ll, (long long)(n_reps * kTetRepsScale));
+    if (a.k == 2) n_reps = max(32ll, (long long)(n_reps * kTriRepsScale));
     return (int)max(1ll, (C + n_reps - 1) / n_reps);
 }
 
