@@ -97,6 +97,10 @@ constexpr double kTetRepsScale = FPH_TET_REPS_SCALE;
 // 3.50 / 3.52 ms, dense30 4.47 / 4.49 / 4.53 / 4.61, modelnet_batch 139.5 /
 // 139.9 / 141.0 / 142.1
 constexpr double kTriRepsScale = FPH_TRI_REPS_SCALE;
+#ifndef FPH_EDGE_REPS_SCALE
+#define FPH_EDGE_REPS_SCALE 1.0
+#endif
+constexpr double kEdgeRepsScale = FPH_EDGE_REPS_SCALE;  // and for edges
 #ifndef FPH_COUNT_EST
 #define FPH_COUNT_EST 1
 #endif
@@ -1059,6 +1063,7 @@ __device__ __forceinline__ int sample_stride(const FloodArgs& a, long long C, bo
     long long n_reps = team ? (long long)a.reps_target * kTeamReps : a.reps_target;
     if (a.k == 3) n_reps = max(32ll, (long long)(n_reps * kTetRepsScale));
     if (a.k == 2) n_reps = max(32ll, (long long)(n_reps * kTriRepsScale));
+    if (a.k == 1) n_reps = max(32ll, (long long)(n_reps * kEdgeRepsScale));
     return (int)max(1ll, (C + n_reps - 1) / n_reps);
 }
 
