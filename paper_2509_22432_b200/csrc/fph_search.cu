@@ -387,6 +387,10 @@ __device__ __forceinline__ void load_rel(const Ctx& c, int idx, float& ax, float
 // other minimum (phase B adds the same error bound), so U stays a
 // certified upper bound.
 constexpr int kProbeCap = FPH_PROBE_CAP;
+#ifndef FPH_PROBE_CAP_TET
+#define FPH_PROBE_CAP_TET FPH_PROBE_CAP
+#endif
+constexpr int kProbeCapTet = FPH_PROBE_CAP_TET;  // tetrahedra (1771 rows each)
 #ifndef FPH_PROBE_SKIP
 #define FPH_PROBE_SKIP 1
 #endif
@@ -415,7 +419,7 @@ __device__ __forceinline__ float local_probe(const Ctx& c, const PointF& q) {
     const int iz = cell_coord(pz, g.loz, g.inv_h, g.nz);
     const int x0 = max(ix - 1, 0), x1 = min(ix + 1, g.nx - 1);
     float best = INFINITY;
-    int left = kProbeCap;
+    int left = c.a->k == 3 ? kProbeCapTet : kProbeCap;
     // one row of cells at a time, so a full own row costs no further loads
     // (fetching every row's run up front: +1-2% on surface data)
     for (int t = 0; t < kProbeRows && left > 0; ++t) {
