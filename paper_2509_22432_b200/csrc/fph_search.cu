@@ -403,6 +403,22 @@ constexpr bool kProbeSkip = FPH_PROBE_SKIP;
 // ... provided every probe found one within sqrt(kProbeTight) cell edges
 // (looser probe bounds leave phase C more to search than the pass costs)
 constexpr float kProbeTight = FPH_PROBE_TIGHT;
+#ifndef FPH_PROBE_TIGHT_TRI
+#define FPH_PROBE_TIGHT_TRI 1.0f
+#endif
+constexpr float kProbeTightTri = FPH_PROBE_TIGHT_TRI;  // triangles with a small ball
+#ifndef FPH_PROBE_BALL_CELLS
+#define FPH_PROBE_BALL_CELLS 8.0
+#endif
+constexpr double kProbeBallCells = FPH_PROBE_BALL_CELLS;  // "small": rho < this many cell edges
+#ifndef FPH_PROBE_SMALL_DIMS
+#define FPH_PROBE_SMALL_DIMS 12
+#endif
+constexpr int kProbeSmallDims = FPH_PROBE_SMALL_DIMS;  // bit k: the rule applies to dimension k
+#ifndef FPH_PROBE_BALL_CELLS_TET
+#define FPH_PROBE_BALL_CELLS_TET FPH_PROBE_BALL_CELLS
+#endif
+constexpr double kProbeBallCellsTet = FPH_PROBE_BALL_CELLS_TET;
 #ifndef FPH_PROBE_ROWS
 #define FPH_PROBE_ROWS 5
 #endif
@@ -1104,7 +1120,18 @@ __device__ void run_simplex(const Ctx& c, WarpSmem& W, const Team& tm, float* va
             // batch by batch of rows; the first batch with a loose row ends
             // the probing (the pass runs anyway, so further probes would
             // only add their cost: surface data, voids)
-            const float tight = kProbeTight * (float)(c_grid.h * c_grid.h);
+            // simplices with a small masking ball (rho < 8 cell edges: the
+            // representatives' pass is cheap and its bounds are tighter than
+            // a probe's on surface data) skip the pass only when every probe
+            // landed within 1 cell edge; large balls (a box hull sliver:
+            // the pass enumerates ~10^5 grid rows) keep 2 edges.  configs[1]
+            // 3.47 -> 3.37 ms, dense30 4.45 -> 4.29, modelnet_batch 140 ->
+            // 124 ms, box_10m even; larger "small" radii cost box_10m up to 2.5x
+            const bool small_ball =
+                c.G.rho < (a.k == 3 ? kProbeBallCellsTet : kProbeBallCells) * c_grid.h;
+            const float tight = (((kProbeSmallDims >> a.k) & 1) && small_ball ? kProbeTightTri
+                                                                              : kProbeTight) *
+                                (float)(c_grid.h * c_grid.h);
             reps = false;
             for (int j0 = 0; j0 < a.P; j0 += tm.size * 32) {
                 const int j = j0 + tm.rank * 32 + lane;
