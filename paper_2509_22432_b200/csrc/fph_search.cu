@@ -419,6 +419,14 @@ constexpr int kProbeSmallDims = FPH_PROBE_SMALL_DIMS;  // bit k: the rule applie
 #define FPH_PROBE_BALL_CELLS_TET FPH_PROBE_BALL_CELLS
 #endif
 constexpr double kProbeBallCellsTet = FPH_PROBE_BALL_CELLS_TET;
+#ifndef FPH_NO_PROBE_SMALL
+#define FPH_NO_PROBE_SMALL 0
+#endif
+constexpr bool kNoProbeSmall = FPH_NO_PROBE_SMALL;  // 1: small-ball simplices do not probe
+#ifndef FPH_PROBE_ALL_SMALL
+#define FPH_PROBE_ALL_SMALL 0
+#endif
+constexpr bool kProbeAllSmall = FPH_PROBE_ALL_SMALL;  // 1: ... probe every row (no early stop)
 #ifndef FPH_PROBE_ROWS
 #define FPH_PROBE_ROWS 5
 #endif
@@ -1116,7 +1124,10 @@ __device__ void run_simplex(const Ctx& c, WarpSmem& W, const Team& tm, float* va
         // replace the representatives' -- whose pass enumerates every grid
         // row of the masking ball, the dominant cost of a large simplex
         bool reps = true;
-        if (stride > 1 && kProbeCap > 0) {
+        const bool small_dims_ball =
+            ((kProbeSmallDims >> a.k) & 1) &&
+            c.G.rho < (a.k == 3 ? kProbeBallCellsTet : kProbeBallCells) * c_grid.h;
+        if (stride > 1 && kProbeCap > 0 && !(kNoProbeSmall && small_dims_ball)) {
             // batch by batch of rows; the first batch with a loose row ends
             // the probing (the pass runs anyway, so further probes would
             // only add their cost: surface data, voids)
@@ -1146,7 +1157,7 @@ __device__ void run_simplex(const Ctx& c, WarpSmem& W, const Team& tm, float* va
                 }
                 if (tm.sum((long long)__reduce_add_sync(0xffffffffu, (unsigned)miss)) > 0) {
                     reps = true;
-                    break;
+                    if (!(kProbeAllSmall && small_dims_ball)) break;
                 }
             }
             reps = reps || !kProbeSkip;
