@@ -219,7 +219,8 @@ def step_single(lib, native, w, stream):
         Xd, dc = w["items"][0]
         flood_sq_device(Xd, dc, w["m"], True, stream)
     else:
-        flood_sq_device_many(w["items"], w["m"], True, stream)
+        flood_sq_device_many(w["items"], w["m"], True, stream,
+                             lanes=int(os.environ.get("FPH_BENCH_LANES", "2")))
 
 
 def step_sharded(lib, native, w, stream):
