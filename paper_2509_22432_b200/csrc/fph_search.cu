@@ -369,7 +369,7 @@ __device__ __forceinline__ void load_rel(const Ctx& c, int idx, float& ax, float
 }
 
 #ifndef FPH_PROBE_CAP
-#define FPH_PROBE_CAP 16
+#define FPH_PROBE_CAP 48
 #endif
 // Local probe of one sample point (one lane, phase A): its nearest
 // candidate among the first kProbeCap cloud points of the 3-cell runs of
@@ -388,9 +388,13 @@ __device__ __forceinline__ void load_rel(const Ctx& c, int idx, float& ax, float
 // certified upper bound.
 constexpr int kProbeCap = FPH_PROBE_CAP;
 #ifndef FPH_PROBE_CAP_TET
-#define FPH_PROBE_CAP_TET FPH_PROBE_CAP
+#define FPH_PROBE_CAP_TET 16
 #endif
 constexpr int kProbeCapTet = FPH_PROBE_CAP_TET;  // tetrahedra (1771 rows each)
+// (edges and triangles: cap 16 / 24 / 32 / 48 / 64 / 96 -> configs[1] 3.39 /
+// 3.35 / 3.34 / 3.27 / 3.31 / 3.43 ms, dense30 4.30 / 4.26 / 4.21 / 4.13 /
+// 4.23 / 4.51; box_10m and modelnet_batch within 1% up to 48.  Tetrahedra:
+// 16, box_10m 15.2 ms at 8, 11.0 at 24)
 #ifndef FPH_PROBE_SKIP
 #define FPH_PROBE_SKIP 1
 #endif
