@@ -316,6 +316,11 @@ FloodTuning current_tuning(double points_per_landmark = 0.0, int grid_slot = 0) 
     t.reps_target = g_reps_target;
     t.team_threshold = g_team_threshold;
     t.exact_pairs = g_exact_pairs;
+    static const double env_pairs = [] {  // experiments: FPH_EXACT_PAIRS overrides the default
+        const char* e = getenv("FPH_EXACT_PAIRS");
+        return e ? atof(e) : -1.0;
+    }();
+    if (env_pairs >= 0.0 && g_exact_pairs == 65536.0) t.exact_pairs = env_pairs;
     for (int i = 0; i < 4; ++i) t.exact_cand[i] = g_exact_cand[i];
     t.grid_slot = grid_slot;
     return t;
