@@ -30,6 +30,10 @@ static int g_reps_target = 512;
 static int g_team_threshold = 0;  // auto (derived per launch on the device)
 static double g_exact_pairs = 65536.0;
 static long long g_exact_cand[4] = {0, 0, 1000, 0};
+#ifndef FPH_SPARSE_PPL
+#define FPH_SPARSE_PPL 50.0
+#endif
+constexpr double kSparsePPL = FPH_SPARSE_PPL;
 static thread_local long long g_launches = 0;
 
 void set_error(const char* fmt, ...) {
@@ -322,6 +326,10 @@ FloodTuning current_tuning(double points_per_landmark = 0.0, int grid_slot = 0) 
     }();
     if (env_pairs >= 0.0 && g_exact_pairs == 65536.0) t.exact_pairs = env_pairs;
     for (int i = 0; i < 4; ++i) t.exact_cand[i] = g_exact_cand[i];
+    // sparse clouds (few points per landmark, e.g. configs[0]'s 20): the
+    // one-pass exact phase A stays cheaper up to 2500 triangle candidates
+    if (g_exact_cand[2] == 1000 && points_per_landmark > 0.0 && points_per_landmark < kSparsePPL)
+        t.exact_cand[2] = 2500;
     t.grid_slot = grid_slot;
     return t;
 }
