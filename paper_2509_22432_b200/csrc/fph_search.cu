@@ -70,7 +70,7 @@ constexpr int kWT = FPH_WT;     // candidates per warp tile
 __constant__ Grid c_grid;
 constexpr int kMaxBlk = 160;    // blocks ordered best-first per simplex
 #ifndef FPH_SPREAD_RATIO
-#define FPH_SPREAD_RATIO 8.0
+#define FPH_SPREAD_RATIO 16.0
 #endif
 // phase C searches a block's rows one by one when the region around all
 // their U-balls has more than this many times their summed volume
